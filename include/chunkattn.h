@@ -1,0 +1,182 @@
+/*
+ * chunkattn.h — C ABI of the B200-native ChunkAttention decode library.
+ *
+ * What it computes (PAPER.md = arXiv 2402.15220 text under /root/reference):
+ *   decode-time self-attention over a prefix-aware chunked KV cache (PAKV,
+ *   §3.1) with the two-phase partition (TPP, §3.2,
+ *   PAPER.md:51-158):
+ *     chunk-first  (Alg 1):  every chunk C shared by rows i..j
+ *                  is attended by Q[i..j] at once -> partial (O, m, n) (Eqn 1,
+ *                  PAPER.md:95-108);
+ *     seq-first    (Alg 2): every row walks its private
+ *                  chunks and merges all partials with attn_reduce (Eqn 2,
+ *                  PAPER.md:145-158), then O / n.
+ *   The result equals softmax(s * q K^T) V per sequence over its whole KV
+ *    up to rounding.  The prefix tree lives in host memory
+ *   (PAPER.md:162); the context (C, i, j) plus private lists is built on the
+ *   host and copied lazily (triggers "chunk full", "new sequence
+ *   joining", "completed sequence leaving").
+ *
+ * Conventions
+ *   - All functions return chunkattn_status; no C++ exception crosses the ABI.
+ *     On any error the host state is unchanged (strong guarantee) and
+ *     chunkattn_last_error() (thread-local) describes it.
+ *   - A CUDA error makes the handle sticky-failed: every later call that would
+ *     touch the device returns CA_ECUDA.
+ *   - A handle is NOT thread-safe (single writer).  All calls that take a
+ *     `stream` must be issued on one stream (or be ordered by the caller); the
+ *     library keeps one set of device tables and relies on stream order.
+ *   - "device" pointers are CUDA device pointers valid on config.device;
+ *     "host" pointers are plain host memory.  Device inputs must stay valid
+ *     until `stream` has passed the call (as with cudaMemcpyAsync).
+ *   - Layouts are dense, row-major, element type config.dtype unless stated.
+ *     h = num_heads, d = head_dim, c = chunk_size, L = num_layers.
+ *   - Host-only mode: config.device = -1 builds the prefix tree and tables
+ *     without touching CUDA (k/v/q pointers ignored; attend/append return
+ *     CA_EINVAL).  Used for host-logic tests on machines without a GPU.
+ */
+#ifndef CHUNKATTN_H
+#define CHUNKATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct chunkattn* chunkattn_t; /* opaque handle */
+
+typedef enum {
+  CA_OK = 0,
+  CA_EINVAL = -1,  /* bad argument (null pointer, size, layer, shape)            */
+  CA_ENOSEQ = -2,  /* unknown (or removed) sequence id                           */
+  CA_ENOMEM = -3,  /* chunk pool / table / workspace capacity exhausted          */
+  CA_ESTATE = -4,  /* attend: n != live count, duplicate ids                     */
+  CA_ECUDA = -5,   /* CUDA runtime error (sticky)                                */
+  CA_EDTYPE = -6,  /* unsupported dtype / head_dim / chunk_size combination      */
+  CA_ERANGE = -7   /* output buffer too small (export_context, batch_order)      */
+} chunkattn_status;
+
+typedef enum { CA_F32 = 0, CA_F16 = 1, CA_BF16 = 2 } chunkattn_dtype;
+
+/* Static configuration (h = 32, d = 128, c = 64, FP16 in the
+ * paper's experiments).  Supported: d in {64, 128}; c in [1, 256] (the tensor
+ * core chunk-first path needs c % 16 == 0 and dtype F16/BF16; other shapes use
+ * the SIMT chunk-first path). */
+typedef struct {
+  int32_t num_heads;       /* heads held by THIS handle (a rank's head slice)          */
+  int32_t head_dim;        /* d                                                        */
+  int32_t chunk_size;      /* c ("a segment of c context tokens")          */
+  int32_t num_layers;      /* layers sharing one tree and one context (>= 1)           */
+  int32_t dtype;           /* chunkattn_dtype of K, V, Q                               */
+  int32_t out_dtype;       /* chunkattn_dtype of the attention output                   */
+  int32_t share_threshold; /* chunk-first takes chunks with ref >= this (default 2,
+                              PAPER.md:80 "shared by multiple sequences"); a huge value
+                              disables TPP (baseline B1 = the paper's PagedAttn*)     */
+  int32_t prefix_match;    /* 1: share matched prompt prefixes (PAKV); 0: every
+                              sequence owns private copies (baseline B0 = PagedAttn)  */
+  float scale;             /* softmax scale s; 0 -> 1/sqrt(d)           */
+  int32_t device;          /* CUDA ordinal, or -1 for host-only mode                   */
+  int64_t max_chunks;      /* pool capacity in chunks                                  */
+  int64_t max_batch;       /* max live sequences                                       */
+  int64_t max_seq_len;     /* max tokens per sequence                                  */
+} chunkattn_config;
+
+/* Caller-owned device memory (the library never calls cudaMalloc). */
+typedef struct {
+  void* k_pool;            /* device [L][max_chunks][h][c][d] dtype; chunk id = index  */
+  void* v_pool;            /* device, same layout as k_pool                            */
+  void* workspace;         /* device, >= chunkattn_workspace_bytes(config) bytes,
+                              16-byte aligned; holds the context tables and the
+                              fp32 partials [slot][h][d] + (m, n)[slot][h]            */
+  size_t workspace_bytes;
+} chunkattn_buffers;
+
+/* Bytes of device workspace the handle needs for `cfg` (0 on invalid cfg). */
+size_t chunkattn_workspace_bytes(const chunkattn_config* cfg);
+
+/* Create a handle.  Pools and workspace must outlive it.  The pool contents
+ * need not be initialised (stale slots are masked by select). */
+chunkattn_status chunkattn_create(const chunkattn_config* cfg, const chunkattn_buffers* buf,
+                                  chunkattn_t* out);
+chunkattn_status chunkattn_destroy(chunkattn_t h);
+
+/* Prefix lookup without mutation ("prefix lookup to avoid repeated
+ * computation of KV projection"): *matched = number of leading tokens covered
+ * by full, aligned, matching chunks (a multiple of c).  tokens: host int32[n]. */
+chunkattn_status chunkattn_match_prefix(chunkattn_t h, const int32_t* tokens, int64_t n,
+                                        int64_t* matched);
+
+/* New sequence joins (PAPER.md:507 scenario i): match the longest prefix of full
+ * chunks, insert private chunks for the rest, copy their K/V into the pool.
+ *   tokens        host int32[n], n >= 1
+ *   k, v          device [n - kv_first_pos][L][h][d] dtype: K/V of positions
+ *                 kv_first_pos..n-1 (rows for matched positions are skipped)
+ *   kv_first_pos  0 <= kv_first_pos <= matched (call match_prefix first to
+ *                 skip computing K/V for the matched prefix); CA_EINVAL if the
+ *                 K/V rows do not cover every unmatched position
+ *   *seq_id       new id (monotone 0, 1, 2, ...; never reused)
+ *   *matched      matched token count */
+chunkattn_status chunkattn_add_sequence(chunkattn_t h, const int32_t* tokens, int64_t n,
+                                        const void* k, const void* v, int64_t kv_first_pos,
+                                        void* stream, int64_t* seq_id, int64_t* matched);
+
+/* One decode step for n sequences (PAPER.md:507 scenario iii: "append new
+ * tokens into leaf chunks or grow a new chunk when the leaf chunk is full").
+ * Processed in call order.  seq_ids host int64[n] (distinct, live); tokens
+ * host int32[n]; k, v device [n][L][h][d] dtype in seq_ids order.  Must precede
+ * the attend of the same step (the query attends to its own key). */
+chunkattn_status chunkattn_append_kv(chunkattn_t h, int64_t n, const int64_t* seq_ids,
+                                     const int32_t* tokens, const void* k, const void* v,
+                                     void* stream);
+
+/* Completed sequence leaves (PAPER.md:507 scenario ii): release the chunks its
+ * path held alone (leaf -> root) to the LIFO free list.
+ * *released = number of chunks released (may be NULL). */
+chunkattn_status chunkattn_remove_sequence(chunkattn_t h, int64_t seq_id, int64_t* released);
+
+/* Two-phase attention of one layer for ALL live sequences.
+ *   seq_ids  host int64[n], n == live count, any order (CA_ESTATE otherwise)
+ *   q        device [n][h][d] dtype, row k is the query of seq_ids[k]
+ *   out      device [n][h][d] out_dtype, row k receives seq_ids[k]'s output
+ * Asynchronous on `stream` (cudaStream_t; NULL = legacy default stream). */
+chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const int64_t* seq_ids,
+                                  const void* q, void* out, void* stream);
+
+/* Sequence ids in batch-row order (DFS of the prefix tree). */
+chunkattn_status chunkattn_batch_order(chunkattn_t h, int64_t* seq_ids_out, int64_t cap,
+                                       int64_t* n);
+
+/* Canonical text of the tree and context (format in DESIGN.md §T5); *len is the
+ * byte length without the trailing NUL.  CA_ERANGE if cap <= *len. */
+chunkattn_status chunkattn_export_context(chunkattn_t h, char* buf, size_t cap, size_t* len);
+
+/* out[6] = {chunks used, chunks free, chunks created, high-water mark,
+ *           K+V bytes of used chunks (all layers), unused token slots}. */
+chunkattn_status chunkattn_memory_stats(chunkattn_t h, int64_t out[6]);
+
+/* out[6] = {context builds, H2D table uploads, H2D bytes uploaded,
+ *           kernels launched, current epoch, partial slots of the context}. */
+chunkattn_status chunkattn_counters(chunkattn_t h, int64_t out[6]);
+
+/* Tuning / test knobs (host-side scheduling only; any setting gives the same
+ * result within rounding, and a fixed setting is bitwise reproducible):
+ *   "cf_splits"        0 = auto, else force chunks-per-split of chunk-first tiles
+ *   "cf_target_ctas"   chunk-first CTA target for the auto split rule
+ *   "cf_simt"          1 = force the SIMT chunk-first kernel (no tensor cores)
+ *   "sf_seg_chunks"    0 = auto, else max private chunks per seq-first tile  */
+chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t value);
+
+/* Copy the device-resident context tables (int32) to host memory `dst` (for
+ * tests: they must equal the host-built tables).  *len = bytes. */
+chunkattn_status chunkattn_download_tables(chunkattn_t h, void* dst, size_t cap, size_t* len,
+                                           void* stream);
+
+/* Message of the last error on this thread ("" if none). */
+const char* chunkattn_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHUNKATTN_H */

@@ -248,11 +248,11 @@ class TreeModel:
         lines = ["chunks:"]
         for (cid, par, sp, ln, ref, ft, lt, i, j) in ctx["chunks"]:
             lines.append(f"{cid} {par} {sp} {ln} {ref} {ft} {lt}")
-        lines.append("order: " + " ".join(str(s) for s in ctx["order"]))
-        lines.append("shared: " + " ".join(f"({c},{i},{j})" for (c, i, j) in ctx["shared"]))
+        lines.append("order:" + "".join(f" {s}" for s in ctx["order"]))
+        lines.append("shared:" + "".join(f" ({c},{i},{j})" for (c, i, j) in ctx["shared"]))
         for r, lst in enumerate(ctx["private"]):
-            lines.append(f"private[{r}]: " + " ".join(str(c) for c in lst))
-        lines.append("tuples: " + " ".join(f"({c},{i},{j})" for (c, i, j) in ctx["tuples"]))
+            lines.append(f"private[{r}]:" + "".join(f" {c}" for c in lst))
+        lines.append("tuples:" + "".join(f" ({c},{i},{j})" for (c, i, j) in ctx["tuples"]))
         u, f, cr, hw = ctx["alloc"]
         lines.append(f"alloc: {u} {f} {cr} {hw}")
         return "\n".join(lines) + "\n"

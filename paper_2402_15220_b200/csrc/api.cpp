@@ -1,0 +1,525 @@
+// C ABI of the ChunkAttention decode library (include/chunkattn.h).
+//
+// Host side of PAPER.md §3.3: the prefix tree is kept in CPU
+// memory, the context (C, i, j) + private lists is generated on the CPU and
+// copied to the GPU only when the tree structure changed ("lazy context copy",
+// triggers: chunk full, sequence joins, sequence leaves), through a pinned,
+// double-buffered staging area and one cudaMemcpyAsync on the caller's stream.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/chunkattn.h"
+#include "host/schedule.h"
+#include "host/tree.h"
+#include "kernels/kernels.h"
+
+using namespace pakv;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+chunkattn_status fail(chunkattn_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct WsLayout {
+  size_t attend_perm, append_row, tables, pO, pMN, total;
+  int64_t table_cap, slot_cap;
+};
+
+bool valid_config(const chunkattn_config* c, std::string* why) {
+  if (!c) return (*why = "null config", false);
+  if (c->num_heads < 1 || c->num_layers < 1) return (*why = "num_heads and num_layers must be >= 1", false);
+  if (c->head_dim != 64 && c->head_dim != 128) return (*why = "head_dim must be 64 or 128", false);
+  if (c->chunk_size < 1 || c->chunk_size > 256) return (*why = "chunk_size must be in [1, 256]", false);
+  if (c->dtype < 0 || c->dtype > 2 || c->out_dtype < 0 || c->out_dtype > 2) return (*why = "bad dtype", false);
+  if (c->share_threshold < 2) return (*why = "share_threshold must be >= 2", false);
+  if (c->max_chunks < 1 || c->max_chunks > (1LL << 31) - 1) return (*why = "bad max_chunks", false);
+  if (c->max_batch < 1 || c->max_batch > (1LL << 24)) return (*why = "bad max_batch", false);
+  if (c->max_seq_len < 1 || c->max_seq_len > (1LL << 30)) return (*why = "bad max_seq_len", false);
+  if ((int64_t)c->num_layers * c->max_chunks * c->num_heads * c->chunk_size > (1LL << 31) - 1)
+    return (*why = "pool too large for 32-bit row coordinates", false);
+  return true;
+}
+
+WsLayout ws_layout(const chunkattn_config* c) {
+  WsLayout w{};
+  const int64_t B = c->max_batch;
+  const int64_t msc = (c->max_seq_len + c->chunk_size - 1) / c->chunk_size;
+  w.slot_cap = B * msc;
+  const int64_t sfcap = B * msc;
+  w.table_cap = 4 * (B + 4) + 2 * (B + 5) + (sfcap + 4) + (w.slot_cap + 4) + (c->max_chunks + 4) +
+                kCfTileInts * (w.slot_cap + 1);
+  size_t o = 0;
+  w.attend_perm = o;
+  o = align_up(o + 4 * B, 256);
+  w.append_row = o;
+  o = align_up(o + 4 * B, 256);
+  w.tables = o;
+  o = align_up(o + 4 * w.table_cap, 256);
+  w.pO = o;
+  o = align_up(o + (size_t)4 * w.slot_cap * c->num_heads * c->head_dim, 256);
+  w.pMN = o;
+  o = align_up(o + (size_t)8 * w.slot_cap * c->num_heads, 256);
+  w.total = o;
+  return w;
+}
+
+}  // namespace
+
+struct chunkattn {
+  chunkattn_config cfg{};
+  bool host_only = true;
+  PrefixTree tree;
+  ScheduleOptions sopt;
+  Context ctx;
+  WsLayout ws{};
+  std::string build_err;
+  // device
+  PoolGeom pool{};
+  char* wsp = nullptr;
+  CUtensorMap tmk{}, tmv{};
+  bool tma_ok = false;
+  bool cf_simt = false;
+  bool use_pdl = true;
+  int num_sms = 148;
+  int64_t cf_cpt_forced = 0;
+  // staging
+  int32_t* pinned[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  bool ev_live[2] = {false, false};
+  int next_stage = 0;
+  int64_t uploaded_epoch = -1;
+  std::vector<int64_t> attend_ids;
+  int64_t attend_epoch = -1;
+  std::vector<int64_t> append_ids;
+  int64_t append_epoch = -1;
+  // counters
+  int64_t n_builds = 0, n_uploads = 0, upload_bytes = 0, n_launches = 0;
+  bool failed = false;
+
+  explicit chunkattn(const chunkattn_config& c)
+      : cfg(c), tree(c.chunk_size, c.max_chunks, c.prefix_match != 0) {}
+
+  float scale() const { return cfg.scale > 0.f ? cfg.scale : 1.0f / std::sqrt((float)cfg.head_dim); }
+
+  chunkattn_status cuda_fail(cudaError_t e, const char* where) {
+    failed = true;
+    return fail(CA_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+  }
+
+  chunkattn_status set_device() {
+    int cur = -1;
+    cudaError_t e = cudaGetDevice(&cur);
+    if (e == cudaSuccess && cur != cfg.device) e = cudaSetDevice(cfg.device);
+    return e == cudaSuccess ? CA_OK : cuda_fail(e, "cudaSetDevice");
+  }
+
+  // H2D copy through pinned double-buffered staging (stream ordered).
+  chunkattn_status upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return CA_OK;
+    const int k = next_stage;
+    next_stage ^= 1;
+    if (ev_live[k]) {
+      cudaError_t e = cudaEventSynchronize(ev[k]);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+    }
+    std::memcpy(pinned[k], src, bytes);
+    cudaError_t e = cudaMemcpyAsync(dst, pinned[k], bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync");
+    e = cudaEventRecord(ev[k], st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    ev_live[k] = true;
+    ++n_uploads;
+    upload_bytes += (int64_t)bytes;
+    return CA_OK;
+  }
+
+  // Rebuild the context if the tree changed; upload it (device mode).
+  chunkattn_status ensure_context(cudaStream_t st) {
+    if (ctx.epoch == tree.epoch()) return CA_OK;
+    sopt.cf_chunks_per_tile = cf_cpt_forced;
+    Context nc;
+    std::string err;
+    if (!build_context(tree, sopt, &nc, &err)) return fail(CA_ENOMEM, err);
+    ctx = std::move(nc);
+    ++n_builds;
+    if (!host_only) {
+      chunkattn_status s = upload(wsp + ws.tables, ctx.blob.data(), ctx.blob.size() * 4, st);
+      if (s != CA_OK) return s;
+      uploaded_epoch = ctx.epoch;
+    }
+    return CA_OK;
+  }
+
+  DevTables dev_tables() const {
+    DevTables t{};
+    const int32_t* base = reinterpret_cast<const int32_t*>(wsp + ws.tables);
+    const BlobLayout& L = ctx.lay;
+    t.row_caller = reinterpret_cast<const int32_t*>(wsp + ws.attend_perm);
+    t.append_row = reinterpret_cast<const int32_t*>(wsp + ws.append_row);
+    t.seq_len = const_cast<int32_t*>(base + L.seq_len);
+    t.sf_first = base + L.sf_first;
+    t.last_chunk = base + L.last_chunk;
+    t.last_start = base + L.last_start;
+    t.sf_ptr = base + L.sf_ptr;
+    t.mg_ptr = base + L.mg_ptr;
+    t.sf_chunk = base + L.sf_chunk;
+    t.mg_slot = base + L.mg_slot;
+    t.cf_chunk = base + L.cf_chunk;
+    t.cf_tile = base + L.cf_tile;
+    t.b = ctx.b;
+    t.n_cf_tiles = ctx.n_cf_tiles;
+    t.max_tile_rows = ctx.max_tile_rows;
+    return t;
+  }
+};
+
+namespace {
+
+#define CA_GUARD_BEGIN try {
+#define CA_GUARD_END                                              \
+  }                                                               \
+  catch (const PoolExhausted&) {                                  \
+    return fail(CA_ENOMEM, "chunk pool exhausted");               \
+  }                                                               \
+  catch (const std::bad_alloc&) {                                 \
+    return fail(CA_ENOMEM, "host allocation failed");             \
+  }                                                               \
+  catch (const std::exception& ex) {                              \
+    return fail(CA_EINVAL, std::string("internal: ") + ex.what()); \
+  }
+
+}  // namespace
+
+extern "C" {
+
+const char* chunkattn_last_error(void) { return g_last_error.c_str(); }
+
+size_t chunkattn_workspace_bytes(const chunkattn_config* cfg) {
+  std::string why;
+  if (!valid_config(cfg, &why)) return 0;
+  return ws_layout(cfg).total;
+}
+
+chunkattn_status chunkattn_create(const chunkattn_config* cfg, const chunkattn_buffers* buf, chunkattn_t* out) {
+  CA_GUARD_BEGIN
+  std::string why;
+  if (!out) return fail(CA_EINVAL, "null out");
+  *out = nullptr;
+  if (!valid_config(cfg, &why)) return fail(CA_EINVAL, why);
+  auto* h = new chunkattn(*cfg);
+  h->host_only = cfg->device < 0;
+  h->ws = ws_layout(cfg);
+  h->sopt.share_threshold = cfg->share_threshold;
+  h->sopt.num_heads = cfg->num_heads;
+  h->sopt.slot_capacity = h->ws.slot_cap;
+  h->sopt.table_capacity = h->ws.table_cap;
+  h->sopt.cf_target_ctas = 148;
+  if (!h->host_only) {
+    if (!buf || !buf->k_pool || !buf->v_pool || !buf->workspace) {
+      delete h;
+      return fail(CA_EINVAL, "null device buffer");
+    }
+    if (buf->workspace_bytes < h->ws.total) {
+      delete h;
+      return fail(CA_EINVAL, "workspace too small: need " + std::to_string(h->ws.total));
+    }
+    if (((uintptr_t)buf->k_pool | (uintptr_t)buf->v_pool | (uintptr_t)buf->workspace) & 15) {
+      delete h;
+      return fail(CA_EINVAL, "device buffers must be 16-byte aligned");
+    }
+    if (h->set_device() != CA_OK) {
+      delete h;
+      return CA_ECUDA;
+    }
+    h->wsp = static_cast<char*>(buf->workspace);
+    h->pool.k = buf->k_pool;
+    h->pool.v = buf->v_pool;
+    h->pool.max_chunks = cfg->max_chunks;
+    h->pool.layer_stride = cfg->max_chunks * cfg->num_heads * cfg->chunk_size * (int64_t)cfg->head_dim;
+    h->pool.h = cfg->num_heads;
+    h->pool.c = cfg->chunk_size;
+    h->pool.d = cfg->head_dim;
+    h->pool.num_layers = cfg->num_layers;
+    h->pool.dtype = cfg->dtype;
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device) == cudaSuccess && sms > 0)
+      h->num_sms = sms;
+    h->sopt.cf_target_ctas = h->num_sms;
+    h->tma_ok = make_pool_tmaps(h->pool, &h->tmk, &h->tmv);
+    const size_t pin_bytes = (size_t)4 * (h->ws.table_cap + 2 * cfg->max_batch + 64);
+    for (int k = 0; k < 2; ++k) {
+      cudaError_t e = cudaHostAlloc((void**)&h->pinned[k], pin_bytes, cudaHostAllocDefault);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev[k], cudaEventDisableTiming);
+      if (e != cudaSuccess) {
+        chunkattn_destroy(h);
+        return fail(CA_ECUDA, std::string("staging alloc: ") + cudaGetErrorString(e));
+      }
+    }
+  }
+  *out = h;
+  return CA_OK;
+  CA_GUARD_END
+}
+
+chunkattn_status chunkattn_destroy(chunkattn_t h) {
+  if (!h) return CA_OK;
+  for (int k = 0; k < 2; ++k) {
+    if (h->ev[k]) {
+      cudaEventSynchronize(h->ev[k]);
+      cudaEventDestroy(h->ev[k]);
+    }
+    if (h->pinned[k]) cudaFreeHost(h->pinned[k]);
+  }
+  delete h;
+  return CA_OK;
+}
+
+chunkattn_status chunkattn_match_prefix(chunkattn_t h, const int32_t* tokens, int64_t n, int64_t* matched) {
+  CA_GUARD_BEGIN
+  if (!h || !matched || (n > 0 && !tokens) || n < 0) return fail(CA_EINVAL, "bad argument");
+  *matched = (int64_t)h->tree.match(tokens, n).size() * h->cfg.chunk_size;
+  return CA_OK;
+  CA_GUARD_END
+}
+
+chunkattn_status chunkattn_add_sequence(chunkattn_t h, const int32_t* tokens, int64_t n, const void* k,
+                                        const void* v, int64_t kv_first_pos, void* stream, int64_t* seq_id,
+                                        int64_t* matched) {
+  CA_GUARD_BEGIN
+  if (!h || !tokens || n < 1 || !seq_id) return fail(CA_EINVAL, "bad argument");
+  if (h->failed) return fail(CA_ECUDA, "handle failed on an earlier CUDA error");
+  if (n > h->cfg.max_seq_len) return fail(CA_EINVAL, "sequence longer than max_seq_len");
+  if (h->tree.live_count() >= h->cfg.max_batch) return fail(CA_ENOMEM, "max_batch live sequences reached");
+  const int64_t m = (int64_t)h->tree.match(tokens, n).size() * h->cfg.chunk_size;
+  if (kv_first_pos < 0 || kv_first_pos > m) return fail(CA_EINVAL, "kv_first_pos must be in [0, matched]");
+  if (!h->host_only && m < n && (!k || !v)) return fail(CA_EINVAL, "null k/v");
+  std::vector<int32_t> fresh;
+  int64_t mm = 0;
+  const int64_t sid = h->tree.add(tokens, n, &fresh, &mm);  // throws PoolExhausted before any change
+  if (!h->host_only && !fresh.empty()) {
+    if (h->set_device() != CA_OK) return CA_ECUDA;
+    const size_t row_bytes = (size_t)h->cfg.num_layers * h->cfg.num_heads * h->cfg.head_dim * dtype_bytes(h->cfg.dtype);
+    const size_t skip = (size_t)(mm - kv_first_pos) * row_bytes;
+    cudaError_t e = launch_copy_rows(h->pool, fresh.data(), (int32_t)fresh.size(), mm, n - mm,
+                                     static_cast<const char*>(k) + skip, static_cast<const char*>(v) + skip,
+                                     static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return h->cuda_fail(e, "copy_rows");
+    h->n_launches += (n - mm + 256LL * h->cfg.chunk_size - 1) / (256LL * h->cfg.chunk_size);
+  }
+  *seq_id = sid;
+  if (matched) *matched = mm;
+  return CA_OK;
+  CA_GUARD_END
+}
+
+chunkattn_status chunkattn_append_kv(chunkattn_t h, int64_t n, const int64_t* seq_ids, const int32_t* tokens,
+                                     const void* k, const void* v, void* stream) {
+  CA_GUARD_BEGIN
+  if (!h || n < 0 || (n > 0 && (!seq_ids || !tokens))) return fail(CA_EINVAL, "bad argument");
+  if (h->failed) return fail(CA_ECUDA, "handle failed on an earlier CUDA error");
+  if (n == 0) return CA_OK;
+  if (!h->host_only && (!k || !v)) return fail(CA_EINVAL, "null k/v");
+  {
+    std::unordered_set<int64_t> seen;
+    seen.reserve(n * 2);
+    for (int64_t i = 0; i < n; ++i) {
+      const Sequence* s = h->tree.find(seq_ids[i]);
+      if (!s) return fail(CA_ENOSEQ, "unknown seq id " + std::to_string(seq_ids[i]));
+      if (!seen.insert(seq_ids[i]).second) return fail(CA_EINVAL, "duplicate seq id in append");
+      if (s->len + 1 > h->cfg.max_seq_len) return fail(CA_EINVAL, "sequence would exceed max_seq_len");
+    }
+  }
+  const int64_t need = h->tree.append_needs(seq_ids, n);
+  if (need > h->tree.pool().available()) return fail(CA_ENOMEM, "chunk pool exhausted");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!h->host_only && h->set_device() != CA_OK) return CA_ECUDA;
+  if (need > 0) h->tree.append_grow(seq_ids, n);  // structural: "chunk full" trigger
+  chunkattn_status s = h->ensure_context(st);       // tables with pre-step lengths
+  if (s != CA_OK) return s;
+  if (!h->host_only) {
+    const bool same = h->append_epoch == h->ctx.epoch && (int64_t)h->append_ids.size() == n &&
+                      std::memcmp(h->append_ids.data(), seq_ids, n * sizeof(int64_t)) == 0;
+    if (!same) {
+      std::vector<int32_t> rows(n);
+      for (int64_t i = 0; i < n; ++i) rows[i] = h->ctx.row_of.at(seq_ids[i]);
+      s = h->upload(h->wsp + h->ws.append_row, rows.data(), n * 4, st);
+      if (s != CA_OK) return s;
+      h->append_ids.assign(seq_ids, seq_ids + n);
+      h->append_epoch = h->ctx.epoch;
+    }
+    cudaError_t e = launch_append_kv(h->pool, h->dev_tables(), (int32_t)n, k, v, st);
+    if (e != cudaSuccess) return h->cuda_fail(e, "append_kv");
+    ++h->n_launches;
+  }
+  h->tree.append_tokens(seq_ids, tokens, n);
+  return CA_OK;
+  CA_GUARD_END
+}
+
+chunkattn_status chunkattn_remove_sequence(chunkattn_t h, int64_t seq_id, int64_t* released) {
+  CA_GUARD_BEGIN
+  if (!h) return fail(CA_EINVAL, "null handle");
+  if (!h->tree.find(seq_id)) return fail(CA_ENOSEQ, "unknown seq id " + std::to_string(seq_id));
+  const auto rel = h->tree.remove(seq_id);
+  if (released) *released = (int64_t)rel.size();
+  return CA_OK;
+  CA_GUARD_END
+}
+
+chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const int64_t* seq_ids, const void* q,
+                                  void* out, void* stream) {
+  CA_GUARD_BEGIN
+  if (!h || n < 0 || (n > 0 && !seq_ids)) return fail(CA_EINVAL, "bad argument");
+  if (h->failed) return fail(CA_ECUDA, "handle failed on an earlier CUDA error");
+  if (layer < 0 || layer >= h->cfg.num_layers) return fail(CA_EINVAL, "layer out of range");
+  if (n != h->tree.live_count())
+    return fail(CA_ESTATE, "attend needs all " + std::to_string(h->tree.live_count()) + " live sequences");
+  if (!h->host_only && n > 0 && (!q || !out)) return fail(CA_EINVAL, "null q/out");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!h->host_only && h->set_device() != CA_OK) return CA_ECUDA;
+  const bool same = h->attend_epoch == h->tree.epoch() && (int64_t)h->attend_ids.size() == n &&
+                    (n == 0 || std::memcmp(h->attend_ids.data(), seq_ids, n * sizeof(int64_t)) == 0);
+  std::vector<int32_t> perm;
+  if (!same) {  // validate before touching any state
+    for (int64_t i = 0; i < n; ++i)
+      if (!h->tree.find(seq_ids[i])) return fail(CA_ENOSEQ, "unknown seq id " + std::to_string(seq_ids[i]));
+  }
+  chunkattn_status s = h->ensure_context(st);
+  if (s != CA_OK) return s;
+  if (!same) {
+    perm.assign(n, -1);
+    for (int64_t i = 0; i < n; ++i) {
+      const int32_t r = h->ctx.row_of.at(seq_ids[i]);
+      if (perm[r] >= 0) return fail(CA_ESTATE, "duplicate seq id in attend");
+      perm[r] = (int32_t)i;
+    }
+    if (!h->host_only) {
+      s = h->upload(h->wsp + h->ws.attend_perm, perm.data(), n * 4, st);
+      if (s != CA_OK) return s;
+    }
+    h->attend_ids.assign(seq_ids, seq_ids + n);
+    h->attend_epoch = h->ctx.epoch;
+  }
+  if (h->host_only || n == 0) return CA_OK;
+  AttnLaunch a{};
+  a.pool = h->pool;
+  a.layer = layer;
+  a.q = q;
+  a.out = out;
+  a.out_dtype = h->cfg.out_dtype;
+  a.pO = reinterpret_cast<float*>(h->wsp + h->ws.pO);
+  a.pMN = reinterpret_cast<float2*>(h->wsp + h->ws.pMN);
+  a.scale_log2 = h->scale() * 1.4426950408889634f;
+  a.cf_tensor_cores = h->tma_ok && !h->cf_simt;
+  a.tmap_k = &h->tmk;
+  a.tmap_v = &h->tmv;
+  a.use_pdl = h->use_pdl;
+  const DevTables t = h->dev_tables();
+  cudaError_t e = launch_chunk_first(a, t, st);
+  if (e != cudaSuccess) return h->cuda_fail(e, "chunk_first");
+  if (t.n_cf_tiles > 0) ++h->n_launches;
+  e = launch_seq_first(a, t, st);
+  if (e != cudaSuccess) return h->cuda_fail(e, "seq_first");
+  ++h->n_launches;
+  return CA_OK;
+  CA_GUARD_END
+}
+
+chunkattn_status chunkattn_batch_order(chunkattn_t h, int64_t* ids, int64_t cap, int64_t* n) {
+  CA_GUARD_BEGIN
+  if (!h || !n || (cap > 0 && !ids)) return fail(CA_EINVAL, "bad argument");
+  std::vector<int64_t> order;
+  std::vector<ChunkRec> recs;
+  h->tree.dfs(&order, &recs);
+  *n = (int64_t)order.size();
+  if (cap < *n) return fail(CA_ERANGE, "buffer too small");
+  std::copy(order.begin(), order.end(), ids);
+  return CA_OK;
+  CA_GUARD_END
+}
+
+chunkattn_status chunkattn_export_context(chunkattn_t h, char* buf, size_t cap, size_t* len) {
+  CA_GUARD_BEGIN
+  if (!h || !len) return fail(CA_EINVAL, "bad argument");
+  Context x;
+  h->tree.dfs(&x.order, &x.recs);
+  const std::string s = export_text(h->tree, x, h->cfg.share_threshold);
+  *len = s.size();
+  if (!buf || cap <= s.size()) return fail(CA_ERANGE, "buffer too small");
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return CA_OK;
+  CA_GUARD_END
+}
+
+chunkattn_status chunkattn_memory_stats(chunkattn_t h, int64_t out[6]) {
+  if (!h || !out) return fail(CA_EINVAL, "bad argument");
+  const ChunkPool& p = h->tree.pool();
+  out[0] = p.used();
+  out[1] = p.free_count();
+  out[2] = p.created();
+  out[3] = p.hwm();
+  out[4] = p.used() * 2 * h->cfg.num_layers * h->cfg.num_heads * (int64_t)h->cfg.chunk_size * h->cfg.head_dim *
+           dtype_bytes(h->cfg.dtype);
+  out[5] = h->tree.waste_slots();
+  return CA_OK;
+}
+
+chunkattn_status chunkattn_counters(chunkattn_t h, int64_t out[6]) {
+  if (!h || !out) return fail(CA_EINVAL, "bad argument");
+  out[0] = h->n_builds;
+  out[1] = h->n_uploads;
+  out[2] = h->upload_bytes;
+  out[3] = h->n_launches;
+  out[4] = h->tree.epoch();
+  out[5] = h->ctx.n_slots;
+  return CA_OK;
+}
+
+chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t value) {
+  if (!h || !key) return fail(CA_EINVAL, "bad argument");
+  const std::string k(key);
+  if (k == "cf_splits") {
+    h->cf_cpt_forced = value < 0 ? 0 : value;
+  } else if (k == "cf_target_ctas") {
+    h->sopt.cf_target_ctas = value < 1 ? 1 : value;
+  } else if (k == "cf_simt") {
+    h->cf_simt = value != 0;
+  } else if (k == "pdl") {
+    h->use_pdl = value != 0;
+  } else {
+    return fail(CA_EINVAL, "unknown option " + k);
+  }
+  h->ctx.epoch = -1;  // force a rebuild with the new schedule
+  h->attend_epoch = h->append_epoch = -1;
+  return CA_OK;
+}
+
+chunkattn_status chunkattn_download_tables(chunkattn_t h, void* dst, size_t cap, size_t* len, void* stream) {
+  CA_GUARD_BEGIN
+  if (!h || !len) return fail(CA_EINVAL, "bad argument");
+  if (h->host_only) return fail(CA_EINVAL, "host-only handle");
+  if (h->failed) return fail(CA_ECUDA, "handle failed on an earlier CUDA error");
+  const size_t bytes = h->ctx.blob.size() * 4;
+  *len = bytes;
+  if (!dst || cap < bytes) return fail(CA_ERANGE, "buffer too small");
+  if (h->set_device() != CA_OK) return CA_ECUDA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(dst, h->wsp + h->ws.tables, bytes, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return h->cuda_fail(e, "download");
+  return CA_OK;
+  CA_GUARD_END
+}
+
+}  // extern "C"

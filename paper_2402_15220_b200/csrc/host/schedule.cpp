@@ -1,0 +1,233 @@
+// Context builder.  See schedule.h.
+#include "schedule.h"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace pakv {
+
+namespace {
+
+struct Run {
+  std::vector<int32_t> chunks;  // path order (root -> leaf)
+  int32_t i, j;                 // inclusive rows (PAPER.md:162 tuple convention)
+};
+
+// Tiles of one run for a chunks-per-tile value: (splits, row tiles, rows per tile).
+struct RunTiling {
+  int64_t splits, row_tiles, rows_per_tile;
+};
+
+RunTiling tile_run(const Run& r, int64_t cpt) {
+  const int64_t rows = r.j - r.i + 1;
+  const int64_t n = (int64_t)r.chunks.size();
+  RunTiling t;
+  t.splits = (n + cpt - 1) / cpt;
+  t.row_tiles = (rows + kMaxCfTileRows - 1) / kMaxCfTileRows;
+  // balanced row tiles, multiples of 16 rows (one MMA row group) where possible
+  int64_t per = (rows + t.row_tiles - 1) / t.row_tiles;
+  per = std::min<int64_t>(kMaxCfTileRows, (per + 15) / 16 * 16);
+  t.rows_per_tile = per;
+  t.row_tiles = (rows + per - 1) / per;
+  return t;
+}
+
+}  // namespace
+
+bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* ctx, std::string* err) {
+  const int32_t c = tree.c();
+  const int32_t thr = opt.share_threshold;
+  Context& X = *ctx;
+  tree.dfs(&X.order, &X.recs);
+  const int32_t b = (int32_t)X.order.size();
+  X.b = b;
+  X.row_of.clear();
+  X.row_of.reserve(b * 2 + 1);
+  for (int32_t r = 0; r < b; ++r) X.row_of[X.order[r]] = r;
+
+  // ---- runs: maximal chains of shared chunks with one row range (pre-order)
+  std::vector<Run> runs;
+  std::unordered_map<int32_t, int32_t> run_of;  // chunk id -> run index
+  for (const ChunkRec& rec : X.recs) {
+    const Node& nd = tree.node(rec.id);
+    if (nd.ref < thr) continue;
+    int32_t ri = -1;
+    if (nd.parent >= 0) {
+      auto it = run_of.find(nd.parent);
+      if (it != run_of.end() && runs[it->second].i == rec.i && runs[it->second].j == rec.j) ri = it->second;
+    }
+    if (ri < 0) {
+      ri = (int32_t)runs.size();
+      runs.push_back(Run{{}, rec.i, rec.j});
+    }
+    runs[ri].chunks.push_back(rec.id);
+    run_of[rec.id] = ri;
+  }
+  X.n_runs = (int32_t)runs.size();
+
+  // ---- seq-first lists: path suffix with ref < threshold (Alg 2 "chunks in T
+  // with respect to q only")
+  std::vector<int32_t> sf_ptr(b + 1, 0), sf_first(b), last_chunk(b), last_start(b), seq_len(b);
+  std::vector<int32_t> sf_chunk;
+  for (int32_t r = 0; r < b; ++r) {
+    const Sequence* s = tree.find(X.order[r]);
+    const auto& p = s->path;
+    size_t k = p.size();
+    while (k > 0 && tree.node(p[k - 1]).ref < thr) --k;
+    sf_first[r] = (int32_t)k * c;
+    for (size_t q = k; q < p.size(); ++q) sf_chunk.push_back(p[q]);
+    sf_ptr[r + 1] = (int32_t)sf_chunk.size();
+    last_chunk[r] = p.back();
+    last_start[r] = tree.node(p.back()).start_pos;
+    seq_len[r] = (int32_t)s->len;
+  }
+
+  // ---- split rule: chunks per tile so that heads * tiles >= target CTAs
+  int64_t max_n = 1;
+  for (const Run& r : runs) max_n = std::max<int64_t>(max_n, (int64_t)r.chunks.size());
+  auto count = [&](int64_t cpt, int64_t* tiles, int64_t* slots) {
+    *tiles = 0;
+    *slots = 0;
+    for (const Run& r : runs) {
+      RunTiling t = tile_run(r, cpt);
+      *tiles += t.splits * t.row_tiles;
+      *slots += t.splits * (r.j - r.i + 1);
+    }
+  };
+  int64_t cpt = max_n, tiles = 0, slots = 0;
+  if (opt.cf_chunks_per_tile > 0) {
+    cpt = std::min<int64_t>(opt.cf_chunks_per_tile, max_n);
+  } else if (!runs.empty()) {
+    // cost = waves x chunks per tile (the per-CTA stream length); ties go to the
+    // larger tile (fewer partials).  One wave = cf_target_ctas CTAs.
+    int64_t best = -1;
+    for (int64_t t = max_n; t >= 1; --t) {
+      count(t, &tiles, &slots);
+      const int64_t waves = (tiles * opt.num_heads + opt.cf_target_ctas - 1) / opt.cf_target_ctas;
+      const int64_t cost = waves * t;
+      if (best < 0 || cost < best) {
+        best = cost;
+        cpt = t;
+      }
+    }
+  }
+  count(cpt, &tiles, &slots);
+  while (slots > opt.slot_capacity && cpt < max_n) count(++cpt, &tiles, &slots);
+  if (slots > opt.slot_capacity) {
+    *err = "partial slots exceed workspace capacity";
+    return false;
+  }
+  X.cf_chunks_per_tile = cpt;
+  X.n_slots = slots;
+
+  // ---- tiles, cf chunk lists, merge lists (fixed order: runs root->leaf,
+  // splits ascending: reading A12)
+  std::vector<int32_t> cf_chunk, cf_tile;
+  std::vector<int32_t> mg_cnt(b + 1, 0);
+  for (const Run& r : runs) {
+    RunTiling t = tile_run(r, cpt);
+    for (int32_t row = r.i; row <= r.j; ++row) mg_cnt[row + 1] += (int32_t)t.splits;
+  }
+  std::vector<int32_t> mg_ptr(b + 1, 0);
+  for (int32_t r = 0; r < b; ++r) mg_ptr[r + 1] = mg_ptr[r] + mg_cnt[r + 1];
+  std::vector<int32_t> mg_slot(mg_ptr[b]);
+  std::vector<int32_t> mg_fill(mg_ptr.begin(), mg_ptr.end() - 1);
+  int64_t slot = 0;
+  int32_t max_rows = 0;
+  for (size_t ri = 0; ri < runs.size(); ++ri) {
+    const Run& r = runs[ri];
+    RunTiling t = tile_run(r, cpt);
+    const int64_t n = (int64_t)r.chunks.size();
+    for (int64_t s = 0; s < t.splits; ++s) {
+      const int64_t k0 = s * n / t.splits, k1 = (s + 1) * n / t.splits;  // balanced split
+      const int32_t off = (int32_t)cf_chunk.size();
+      for (int64_t k = k0; k < k1; ++k) cf_chunk.push_back(r.chunks[k]);
+      for (int64_t rt = 0; rt < t.row_tiles; ++rt) {
+        const int32_t r0 = r.i + (int32_t)(rt * t.rows_per_tile);
+        const int32_t r1 = std::min<int32_t>(r.j + 1, r0 + (int32_t)t.rows_per_tile);
+        cf_tile.insert(cf_tile.end(), {off, (int32_t)(k1 - k0), r0, r1, (int32_t)slot, (int32_t)ri, 0, 0});
+        for (int32_t row = r0; row < r1; ++row) mg_slot[mg_fill[row]++] = (int32_t)(slot + (row - r0));
+        slot += r1 - r0;
+        max_rows = std::max(max_rows, r1 - r0);
+      }
+    }
+  }
+  X.n_cf_tiles = (int32_t)(cf_tile.size() / kCfTileInts);
+  X.max_tile_rows = max_rows;
+
+  // ---- pack the blob (seq_len first: the device copy is authoritative between
+  // structural changes and is bumped by the append kernel)
+  BlobLayout& L = X.lay;
+  int64_t o = 0;
+  auto place = [&](int64_t n) {
+    int64_t at = o;
+    o += (n + 3) / 4 * 4;  // 16-byte aligned sub-arrays
+    return at;
+  };
+  L.seq_len = place(b);
+  L.sf_first = place(b);
+  L.last_chunk = place(b);
+  L.last_start = place(b);
+  L.sf_ptr = place(b + 1);
+  L.mg_ptr = place(b + 1);
+  L.sf_chunk = place((int64_t)sf_chunk.size());
+  L.mg_slot = place((int64_t)mg_slot.size());
+  L.cf_chunk = place((int64_t)cf_chunk.size());
+  L.cf_tile = place((int64_t)cf_tile.size());
+  L.total = o;
+  if (o > opt.table_capacity) {
+    *err = "context tables exceed workspace capacity";
+    return false;
+  }
+  X.blob.assign(o, 0);
+  auto put = [&](int64_t at, const std::vector<int32_t>& v) {
+    std::copy(v.begin(), v.end(), X.blob.begin() + at);
+  };
+  put(L.seq_len, seq_len);
+  put(L.sf_first, sf_first);
+  put(L.last_chunk, last_chunk);
+  put(L.last_start, last_start);
+  put(L.sf_ptr, sf_ptr);
+  put(L.mg_ptr, mg_ptr);
+  put(L.sf_chunk, sf_chunk);
+  put(L.mg_slot, mg_slot);
+  put(L.cf_chunk, cf_chunk);
+  put(L.cf_tile, cf_tile);
+  X.epoch = tree.epoch();
+  return true;
+}
+
+std::string export_text(const PrefixTree& tree, const Context& X, int32_t thr) {
+  std::string out = "chunks:\n";
+  char buf[160];
+  for (const ChunkRec& rec : X.recs) {
+    const Node& nd = tree.node(rec.id);
+    const int32_t* t = tree.tokens(rec.id);
+    std::snprintf(buf, sizeof buf, "%d %d %d %d %d %d %d\n", rec.id, nd.parent, nd.start_pos, nd.len,
+                  nd.ref, t[0], t[nd.len - 1]);
+    out += buf;
+  }
+  out += "order:";
+  for (int64_t s : X.order) out += " " + std::to_string(s);
+  out += "\nshared:";
+  for (const ChunkRec& rec : X.recs)
+    if (tree.node(rec.id).ref >= thr)
+      out += " (" + std::to_string(rec.id) + "," + std::to_string(rec.i) + "," + std::to_string(rec.j) + ")";
+  out += "\n";
+  for (size_t r = 0; r < X.order.size(); ++r) {
+    out += "private[" + std::to_string(r) + "]:";
+    for (int32_t id : tree.find(X.order[r])->path)
+      if (tree.node(id).ref < thr) out += " " + std::to_string(id);
+    out += "\n";
+  }
+  out += "tuples:";
+  for (const ChunkRec& rec : X.recs)
+    out += " (" + std::to_string(rec.id) + "," + std::to_string(rec.i) + "," + std::to_string(rec.j) + ")";
+  const ChunkPool& p = tree.pool();
+  std::snprintf(buf, sizeof buf, "\nalloc: %lld %lld %lld %lld\n", (long long)p.used(),
+                (long long)p.free_count(), (long long)p.created(), (long long)p.hwm());
+  out += buf;
+  return out;
+}
+
+}  // namespace pakv

@@ -1,0 +1,60 @@
+// Context generation for the two-phase partition (§3.3): from the
+// prefix tree build, on the host, the chunk-first work list (C, i, j) and the
+// per-sequence private chunk lists, plus the scheduling tables the kernels use
+// (runs split into tiles sized for 148 SMs, merge lists fixing the Eqn 2
+// reduction order).  The result is one packed int32 blob copied to the GPU in a
+// single cudaMemcpyAsync when the tree structure changed (lazy context copy).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "tree.h"
+
+namespace pakv {
+
+// Chunk-first tile record in the blob (kCfTileInts int32 each).
+enum CfTileField { CF_CHUNK_OFF = 0, CF_NCHUNK, CF_ROW0, CF_ROW1, CF_SLOT, CF_RUN, CF_PAD0, CF_PAD1 };
+constexpr int kCfTileInts = 8;
+constexpr int kMaxCfTileRows = 128;  // rows of one chunk-first tile (8 warps x 16 rows)
+
+struct ScheduleOptions {
+  int32_t share_threshold = 2;
+  int32_t num_heads = 1;
+  int64_t cf_chunks_per_tile = 0;  // 0 = auto
+  int64_t cf_target_ctas = 296;    // auto rule: heads * tiles >= this
+  int64_t slot_capacity = 0;       // partial slots available in the workspace
+  int64_t table_capacity = 0;      // int32 entries available for the blob
+};
+
+// Offsets (int32 units) of the arrays inside the blob.
+struct BlobLayout {
+  int64_t seq_len = 0, sf_first = 0, last_chunk = 0, last_start = 0, sf_ptr = 0, mg_ptr = 0,
+          sf_chunk = 0, mg_slot = 0, cf_chunk = 0, cf_tile = 0, total = 0;
+};
+
+struct Context {
+  int64_t epoch = -1;
+  std::vector<int64_t> order;                  // seq ids by row
+  std::unordered_map<int64_t, int32_t> row_of;  // seq id -> row
+  std::vector<ChunkRec> recs;                   // DFS pre-order chunk records
+  std::vector<int32_t> blob;                    // packed tables
+  BlobLayout lay;
+  int32_t b = 0;
+  int32_t n_cf_tiles = 0;
+  int32_t n_runs = 0;
+  int32_t max_tile_rows = 0;
+  int64_t n_slots = 0;
+  int64_t cf_chunks_per_tile = 0;
+};
+
+// Build the context of the current tree.  Returns false (and sets *err) when
+// the tables or the partial slots do not fit the capacities.
+bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* ctx, std::string* err);
+
+// Canonical export text (T5) from a built context.
+std::string export_text(const PrefixTree& tree, const Context& ctx, int32_t share_threshold);
+
+}  // namespace pakv

@@ -1,0 +1,108 @@
+// K1 append_kv: "At each decoding iteration, we append new tokens
+// into leaf chunks" — scatter each sequence's new K/V row into slot
+// seq_len - start_pos of its leaf chunk and bump the device-resident seq_len
+// (so steps that do not change the tree upload nothing: lazy context copy,
+// PAPER.md:162).  Plus the prefill copy of a new sequence's private chunks.
+// Pure data movement: 16-byte vector loads/stores, one CTA per appended row.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pakv {
+
+namespace {
+
+constexpr int kThreads = 128;
+
+__global__ void __launch_bounds__(kThreads) append_kv_kernel(uint4* __restrict__ kpool, uint4* __restrict__ vpool,
+                                                             const uint4* __restrict__ knew,
+                                                             const uint4* __restrict__ vnew, DevTables t,
+                                                             int64_t layer_stride_v, int32_t L, int32_t h,
+                                                             int32_t c, int32_t dv) {
+  const int i = blockIdx.x;
+  const int row = t.append_row[i];
+  const int chunk = t.last_chunk[row];
+  const int slot = t.seq_len[row] - t.last_start[row];
+  const int per_layer = h * dv;  // 16-byte vectors per layer of one token
+  const int total = L * per_layer;
+  for (int e = threadIdx.x; e < total; e += kThreads) {
+    const int l = e / per_layer;
+    const int r = e - l * per_layer;
+    const int hh = r / dv;
+    const int x = r - hh * dv;
+    const int64_t dst = l * layer_stride_v + ((int64_t)(chunk * h + hh) * c + slot) * dv + x;
+    const int64_t src = (int64_t)i * total + e;
+    kpool[dst] = knew[src];
+    vpool[dst] = vnew[src];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) t.seq_len[row] = slot + t.last_start[row] + 1;
+}
+
+struct ChunkList {
+  int32_t ids[256];
+};
+
+__global__ void __launch_bounds__(kThreads) copy_rows_kernel(uint4* __restrict__ kpool, uint4* __restrict__ vpool,
+                                                             const uint4* __restrict__ ksrc,
+                                                             const uint4* __restrict__ vsrc, ChunkList list,
+                                                             int64_t first_pos, int64_t layer_stride_v, int32_t L,
+                                                             int32_t h, int32_t c, int32_t dv) {
+  const int64_t i = blockIdx.x;  // source row
+  const int64_t pos = first_pos + i;
+  const int chunk = list.ids[pos / c - first_pos / c];
+  const int slot = (int)(pos % c);
+  const int per_layer = h * dv;
+  const int total = L * per_layer;
+  for (int e = threadIdx.x; e < total; e += kThreads) {
+    const int l = e / per_layer;
+    const int r = e - l * per_layer;
+    const int hh = r / dv;
+    const int x = r - hh * dv;
+    const int64_t dst = l * layer_stride_v + ((int64_t)(chunk * h + hh) * c + slot) * dv + x;
+    const int64_t src = i * total + e;
+    kpool[dst] = ksrc[src];
+    vpool[dst] = vsrc[src];
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_append_kv(const PoolGeom& p, const DevTables& t, int32_t n, const void* k, const void* v,
+                             cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int E = dtype_bytes(p.dtype);
+  const int dv = p.d * E / 16;
+  append_kv_kernel<<<n, kThreads, 0, st>>>((uint4*)p.k, (uint4*)p.v, (const uint4*)k, (const uint4*)v, t,
+                                           p.layer_stride * E / 16, p.num_layers, p.h, p.c, dv);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_rows(const PoolGeom& p, const int32_t* chunks, int32_t n_chunks, int64_t first_pos,
+                             int64_t m, const void* k, const void* v, cudaStream_t st) {
+  const int E = dtype_bytes(p.dtype);
+  const int dv = p.d * E / 16;
+  const int64_t row_vecs = (int64_t)p.num_layers * p.h * dv;
+  // launch in pieces of <= 256 chunks (the chunk list travels as a kernel parameter)
+  int64_t done = 0;
+  int32_t ci = 0;
+  while (done < m) {
+    const int64_t pos = first_pos + done;
+    const int64_t chunk_end_pos = (pos / p.c + 256) * (int64_t)p.c;  // exclusive
+    const int64_t rows = std::min<int64_t>(m - done, chunk_end_pos - pos);
+    ChunkList list;
+    const int32_t cnt = (int32_t)std::min<int64_t>(256, n_chunks - ci);
+    for (int32_t q = 0; q < cnt; ++q) list.ids[q] = chunks[ci + q];
+    copy_rows_kernel<<<(unsigned)rows, kThreads, 0, st>>>(
+        (uint4*)p.k, (uint4*)p.v, (const uint4*)k + done * row_vecs, (const uint4*)v + done * row_vecs, list, pos,
+        p.layer_stride * E / 16, p.num_layers, p.h, p.c, dv);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    done += rows;
+    ci += 256;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace pakv

@@ -1,0 +1,74 @@
+// Host-side launch interface of the CUDA kernels (internal; not part of the C ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pakv {
+
+enum DType : int32_t { DT_F32 = 0, DT_F16 = 1, DT_BF16 = 2 };
+
+inline int dtype_bytes(int32_t dt) { return dt == DT_F32 ? 4 : 2; }
+
+// Device views of the context tables of one epoch (pointers into the workspace).
+struct DevTables {
+  const int32_t* row_caller;  // row -> index in the caller's attend order
+  int32_t* seq_len;           // [b] tokens per row (bumped by the append kernel)
+  const int32_t* sf_first;    // [b] position of the first seq-first chunk
+  const int32_t* sf_ptr;      // [b+1] CSR into sf_chunk
+  const int32_t* sf_chunk;    // seq-first (private) chunk ids, path order
+  const int32_t* mg_ptr;      // [b+1] CSR into mg_slot
+  const int32_t* mg_slot;     // partial slots merged into each row, fixed order
+  const int32_t* cf_chunk;    // chunk-first chunk ids (runs, path order)
+  const int32_t* cf_tile;     // [n_cf_tiles][8] tile records (schedule.h)
+  const int32_t* last_chunk;  // [b] append target chunk
+  const int32_t* last_start;  // [b] its start position
+  const int32_t* append_row;  // [n] append caller index -> row
+  int32_t b, n_cf_tiles, max_tile_rows;
+};
+
+struct PoolGeom {
+  void* k;  // base of layer 0
+  void* v;
+  int64_t layer_stride;  // elements per layer = max_chunks*h*c*d
+  int64_t max_chunks;
+  int32_t h, c, d, num_layers;
+  int32_t dtype;
+};
+
+struct AttnLaunch {
+  PoolGeom pool;
+  int32_t layer;
+  const void* q;   // [n][h][d] dtype, caller order
+  void* out;       // [n][h][d] out_dtype, caller order
+  int32_t out_dtype;
+  float* pO;       // [slots][h][d]
+  float2* pMN;     // [slots][h]   (m in log2 units, n)
+  float scale_log2;
+  bool cf_tensor_cores;  // use the mma chunk-first kernel
+  const CUtensorMap* tmap_k;  // host copies (passed by value to kernels)
+  const CUtensorMap* tmap_v;
+  bool use_pdl;
+};
+
+// K1: scatter one decode step's K/V into the leaf chunks and bump seq_len.
+cudaError_t launch_append_kv(const PoolGeom& pool, const DevTables& t, int32_t n, const void* k,
+                             const void* v, cudaStream_t st);
+
+// Copy rows [first_pos, first_pos+m) of one sequence into its chunks
+// (chunk of position p = chunks[p/c - first_pos/c]); src [m][L][h][d].
+cudaError_t launch_copy_rows(const PoolGeom& pool, const int32_t* chunks, int32_t n_chunks, int64_t first_pos,
+                             int64_t m, const void* k, const void* v, cudaStream_t st);
+
+// K3: chunk-first phase (Alg 1) -> partial slots.
+cudaError_t launch_chunk_first(const AttnLaunch& a, const DevTables& t, cudaStream_t st);
+// K4: seq-first phase (Alg 2) -> merged, normalised output.
+cudaError_t launch_seq_first(const AttnLaunch& a, const DevTables& t, cudaStream_t st);
+
+// Build the TMA descriptors of a 16-bit pool viewed as 2-D [rows][d], box
+// {64, c} with 128-byte swizzle.  Returns false if unsupported.
+bool make_pool_tmaps(const PoolGeom& pool, CUtensorMap* tk, CUtensorMap* tv);
+bool cf_mma_supported(const PoolGeom& pool);
+
+}  // namespace pakv
