@@ -165,8 +165,17 @@ chunkattn_status chunkattn_counters(chunkattn_t h, int64_t out[6]);
  *   "cf_splits"        0 = auto, else force chunks-per-split of chunk-first tiles
  *   "cf_target_ctas"   chunk-first CTA target for the auto split rule
  *   "cf_simt"          1 = force the SIMT chunk-first kernel (no tensor cores)
- *   "sf_seg_chunks"    0 = auto, else max private chunks per seq-first tile  */
+ *   "pdl"              1 (default) = programmatic dependent launch of seq-first
+ *   "kernel_events"    1 = time every kernel launch (chunkattn_kernel_times) */
 chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t value);
+
+/* Per-kernel device time, measured with CUDA events recorded on the launch
+ * stream around every kernel launch while the option "kernel_events" is 1
+ * (PDL is not used between the two phases in that mode).  Synchronises on the
+ * recorded events, accumulates, and resets the accumulators.
+ *   ms[4]       total milliseconds of {append, chunk_first, seq_first, copy}
+ *   launches[4] launches of each kind that were timed */
+chunkattn_status chunkattn_kernel_times(chunkattn_t h, double ms[4], int64_t launches[4]);
 
 /* Copy the device-resident context tables (int32) to host memory `dst` (for
  * tests: they must equal the host-built tables).  *len = bytes. */

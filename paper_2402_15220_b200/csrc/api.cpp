@@ -106,6 +106,67 @@ struct chunkattn {
   // counters
   int64_t n_builds = 0, n_uploads = 0, upload_bytes = 0, n_launches = 0;
   bool failed = false;
+  // per-kernel CUDA-event timing ("kernel_events" option)
+  enum { K_APPEND = 0, K_CF = 1, K_SF = 2, K_COPY = 3 };
+  struct Timed {
+    cudaEvent_t a, b;
+    int kind;
+  };
+  bool kernel_events = false;
+  std::vector<Timed> timed;
+  std::vector<cudaEvent_t> ev_pool;
+  double acc_ms[4] = {0, 0, 0, 0};
+  int64_t acc_n[4] = {0, 0, 0, 0};
+
+  cudaError_t get_event(cudaEvent_t* e) {
+    if (!ev_pool.empty()) {
+      *e = ev_pool.back();
+      ev_pool.pop_back();
+      return cudaSuccess;
+    }
+    return cudaEventCreate(e);
+  }
+  cudaError_t flush_times() {
+    for (const Timed& t : timed) {
+      cudaError_t e = cudaEventSynchronize(t.b);
+      if (e != cudaSuccess) return e;
+      float ms = 0.f;
+      e = cudaEventElapsedTime(&ms, t.a, t.b);
+      if (e != cudaSuccess) return e;
+      acc_ms[t.kind] += ms;
+      acc_n[t.kind] += 1;
+      ev_pool.push_back(t.a);
+      ev_pool.push_back(t.b);
+    }
+    timed.clear();
+    return cudaSuccess;
+  }
+  // Launch through f(); when timing, bracket it with events on the same stream.
+  template <class F>
+  cudaError_t timed_launch(int kind, cudaStream_t st, F f) {
+    if (!kernel_events) return f();
+    if (timed.size() >= 4096) {
+      cudaError_t e = flush_times();
+      if (e != cudaSuccess) return e;
+    }
+    Timed t{nullptr, nullptr, kind};
+    cudaError_t e = get_event(&t.a);
+    if (e == cudaSuccess) e = get_event(&t.b);
+    if (e == cudaSuccess) e = cudaEventRecord(t.a, st);
+    if (e != cudaSuccess) return e;
+    e = f();
+    if (e != cudaSuccess) return e;
+    e = cudaEventRecord(t.b, st);
+    if (e == cudaSuccess) timed.push_back(t);
+    return e;
+  }
+  ~chunkattn() {
+    for (const Timed& t : timed) {
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+  }
 
   explicit chunkattn(const chunkattn_config& c)
       : cfg(c), tree(c.chunk_size, c.max_chunks, c.prefix_match != 0) {}
