@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""Decode-attention benchmark of the B200 ChunkAttention path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--mode chunk|b0|b1] [--workload cfg2]
+
+Workload (BASELINE.json configs[1], the metric's configuration): Llama-2-7B
+attention shape, 32 heads x 128 dim, fp16, chunk 64, batch 32, a shared system
+prompt of 2048 tokens (n_p = n_s = 2048, fully shared), then
+iterative decoding: a STEP is one decode iteration = append one token's K/V
+per sequence (a4, host tree a1-a3) + two-phase attention (a5 chunk-first, a6
+seq-first) for all 32 sequences.  Timed steps are completion tokens 1..K of a
+fresh cache (the warm-up runs on a cache that is then drained and refilled),
+so K = 512 reproduces the token-rate point (n_s = 2048, n_c = 512) of
+fig:cuda_attn_tps.  Token rate = b * K / t.
+
+Timing: CUDA events on the launch stream around each step; the L2 (126 MB on
+B200) is flushed by writing a 2x-L2 buffer between timed steps (outside the
+events).  Multi-GPU (torchrun): every rank decodes its own batch of 32
+sequences (independent problems, weak scaling, no data-path collective);
+value = all ranks' tokens / max-over-ranks time.
+
+The JSON line adds: roofline (dominant kernel, algorithmic bytes / its CUDA
+event time, against MEASURED_PEAKS.json), cpu_baseline (the fp64 oracle on the
+host, bounded sample), e2e (same metric through the C ABI with pinned host
+buffers, H2D of q/k/v and D2H of the output inside the timed region),
+gpu_launches, clocks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "decode attention tokens/s and kernel µs vs shared-prompt len; % HBM roofline"
+
+
+# ------------------------------------------------------------------ helpers --
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return j.get("hbm_gbs", 6650.0), "measured", j
+    return 6650.0, "fallback", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the run."""
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        time.sleep(0.05)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 8:
+                    continue
+                try:
+                    s, m, util = float(parts[1]), float(parts[2]), float(parts[7])
+                except ValueError:
+                    continue
+                mx = m
+                if util > 0:
+                    sm.append(s)
+                for nm, v in zip(names, parts[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- workload --
+class DecodeWorkload:
+    """b sequences sharing a prompt of n_shared tokens (+ optional private
+    question), decoded for `steps` iterations; all inputs generated on the device
+    before timing (synthetic, seeded; DESIGN.md input recipe)."""
+
+    def __init__(self, dev, seed=0, b=32, h=32, d=128, c=64, n_shared=2048, question=0, steps=512,
+                 dtype=torch.float16, mode="chunk"):
+        from paper_2402_15220_b200 import ChunkAttention
+        self.dev, self.seed, self.b, self.h, self.d, self.c = dev, seed, b, h, d, c
+        self.n_shared, self.question, self.steps, self.dtype, self.mode = n_shared, question, steps, dtype, mode
+        max_len = n_shared + question + steps + 1
+        per_seq = (max_len + c - 1) // c
+        max_chunks = per_seq * b + 8 if mode == "b0" else (n_shared // c + 1) + b * ((question + steps) // c + 2)
+        thr = (1 << 30) if mode == "b1" else 2
+        self.ca = ChunkAttention(h, d, c, max_chunks, b, max_len, dtype=dtype, out_dtype=dtype,
+                                 share_threshold=thr, prefix_match=(mode != "b0"), device=dev)
+        self.prompt = synth.token_ids(seed, synth.TAG_SYS, 0, n_shared, device=dev)
+        self.questions = [synth.token_ids(seed, synth.TAG_PRIV, r, question, device=dev) for r in range(b)]
+        pos = torch.arange(n_shared, device=dev)
+        self.k_prompt = synth.kv_values(seed, synth.TID_K, self.prompt, pos, 1, h, d, device=dev).to(dtype)
+        self.v_prompt = synth.kv_values(seed, synth.TID_V, self.prompt, pos, 1, h, d, device=dev).to(dtype)
+        # per-step decode inputs, resident in HBM: tokens, k/v [S][b][1][h][d], q [S][b][h][d]
+        S = steps
+        rows = torch.arange(b, device=dev, dtype=torch.int64)
+        st = torch.arange(S, device=dev, dtype=torch.int64)
+        tok = 1 + synth.hash_keys(seed, synth.TAG_DECODE, rows[None, :], st[:, None], device=dev) % 31999
+        self.tokens = tok.to(torch.int32).cpu().numpy()                        # [S][b]
+        self.kn = torch.empty((S, b, 1, h, d), dtype=dtype, device=dev)
+        self.vn = torch.empty_like(self.kn)
+        self.q = torch.empty((S, b, h, d), dtype=dtype, device=dev)
+        base = n_shared + question
+        for s in range(S):
+            p = torch.full((b,), base + s, dtype=torch.int64, device=dev)
+            t = tok[s]
+            self.kn[s] = synth.kv_values(seed, synth.TID_K, t, p, 1, h, d, device=dev).to(dtype)
+            self.vn[s] = synth.kv_values(seed, synth.TID_V, t, p, 1, h, d, device=dev).to(dtype)
+        for s0 in range(0, S, 64):
+            s1 = min(S, s0 + 64)
+            for s in range(s0, s1):
+                self.q[s] = synth.q_values(seed, rows, s + 1, 1, h, d, alpha=8.0, device=dev)[:, 0].to(dtype)
+        self.out = torch.empty((b, h, d), dtype=dtype, device=dev)
+        self.ids = None
+
+    def fill(self):
+        """Drain the cache and insert the b sequences (prefill with prefix lookup)."""
+        if self.ids is not None:
+            for s in self.ids.tolist():
+                self.ca.remove_sequence(s)
+        ids = []
+        for r in range(self.b):
+            toks = torch.cat([self.prompt, self.questions[r]]).tolist()
+            m = self.ca.match_prefix(toks)
+            pos = torch.arange(m, len(toks), device=self.dev)
+            if m < self.n_shared:
+                k = torch.cat([self.k_prompt[m:], self._qkv(synth.TID_K, r)])
+                v = torch.cat([self.v_prompt[m:], self._qkv(synth.TID_V, r)])
+            else:
+                k = self._qkv(synth.TID_K, r, m - self.n_shared)
+                v = self._qkv(synth.TID_V, r, m - self.n_shared)
+            assert k.shape[0] == len(pos)
+            sid, _ = self.ca.add_sequence(toks, k.contiguous(), v.contiguous(), kv_first_pos=m)
+            ids.append(sid)
+        self.ids = np.asarray(ids, dtype=np.int64)
+        torch.cuda.synchronize(self.dev)
+
+    def _qkv(self, which, r, skip=0):
+        t = self.questions[r][skip:]
+        pos = torch.arange(self.n_shared + skip, self.n_shared + self.question, device=self.dev)
+        return synth.kv_values(self.seed, which, t, pos, 1, self.h, self.d, device=self.dev).to(self.dtype)
+
+    def step(self, s: int, stream: int):
+        self.ca.append_raw(self.ids, self.tokens[s], self.kn[s].data_ptr(), self.vn[s].data_ptr(), stream)
+        self.ca.attend_raw(0, self.ids, self.q[s].data_ptr(), self.out.data_ptr(), stream)
+
+    def shape_at(self, s: int):
+        """StepShape of decode step s (0-based): private tokens per row = question + s + 1."""
+        from paper_2402_15220_b200.roofline import StepShape
+        p = self.question + s + 1
+        if self.mode == "chunk":
+            shared = self.n_shared // self.c
+            priv = self.b * (p + self.n_shared % self.c)
+            return StepShape(self.b, self.h, self.d, self.c, 2, 2, shared, shared * self.b,
+                             self.b if shared else 0, priv)
+        # baselines: no chunk-first phase; every row walks its whole context
+        return StepShape(self.b, self.h, self.d, self.c, 2, 2, 0, 0, 0, self.b * (self.n_shared + p))
+
+
+# -------------------------------------------------------------------- arms --
+def flush_l2(buf):
+    buf.zero_()
+
+
+def time_steps(wl: DecodeWorkload, K: int, flush_buf, stream) -> list[float]:
+    sp = stream.cuda_stream
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with torch.cuda.stream(stream):
+        for s in range(K):
+            flush_l2(flush_buf)
+            evs[s][0].record(stream)
+            wl.step(s, sp)
+            evs[s][1].record(stream)
+    stream.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def time_e2e(wl: DecodeWorkload, K: int, flush_buf, stream):
+    """Same steps through the public C ABI with pinned host inputs/outputs:
+    H2D of q, k_new, v_new and D2H of the output inside the timed region."""
+    sp = stream.cuda_stream
+    hq = wl.q[:K].cpu().pin_memory()
+    hk = wl.kn[:K].cpu().pin_memory()
+    hv = wl.vn[:K].cpu().pin_memory()
+    hout = torch.empty((K,) + tuple(wl.out.shape), dtype=wl.out.dtype).pin_memory()
+    dq = torch.empty_like(wl.q[0])
+    dk = torch.empty_like(wl.kn[0])
+    dv = torch.empty_like(wl.vn[0])
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with torch.cuda.stream(stream):
+        for s in range(K):
+            flush_l2(flush_buf)
+            evs[s][0].record(stream)
+            dq.copy_(hq[s], non_blocking=True)
+            dk.copy_(hk[s], non_blocking=True)
+            dv.copy_(hv[s], non_blocking=True)
+            wl.ca.append_raw(wl.ids, wl.tokens[s], dk.data_ptr(), dv.data_ptr(), sp)
+            wl.ca.attend_raw(0, wl.ids, dq.data_ptr(), wl.out.data_ptr(), sp)
+            hout[s].copy_(wl.out, non_blocking=True)
+            evs[s][1].record(stream)
+    stream.synchronize()
+    h2d = dq.numel() * dq.element_size() + 2 * dk.numel() * dk.element_size()
+    d2h = wl.out.numel() * wl.out.element_size()
+    return [a.elapsed_time(b) for a, b in evs], h2d, d2h
+
+
+def cpu_baseline(seed, n_shared, question, h, d, budget_s, max_steps):
+    """fp64 oracle on the host: row 0's decode step at completion tokens 1..n
+    until the budget is spent (materialisation untimed)."""
+    from oracle.reference import OracleSequence, timed_attend
+    prompt = synth.token_ids(seed, synth.TAG_SYS, 0, n_shared).tolist()
+    q0 = synth.token_ids(seed, synth.TAG_PRIV, 0, question).tolist()
+    seq = OracleSequence(seed, prompt + q0, h, d, n_shared + question + max_steps + 1)
+    wall = cpu = 0.0
+    n = 0
+    t_start = time.perf_counter()
+    while n < max_steps and time.perf_counter() - t_start < budget_s:
+        tok = int(synth.hash_py(seed, synth.TAG_DECODE, 0, n) % 31999 + 1)
+        seq.extend([tok])
+        q = synth.q_values(seed, torch.tensor([0]), n + 1, 1, h, d, alpha=8.0)[0, 0].numpy()
+        _, w, c = timed_attend(seq, q)
+        wall += w
+        cpu += c
+        n += 1
+    return {"value": n / wall, "unit": "tokens/s", "cores": max(1, round(cpu / wall)), "kind": "oracle",
+            "sample": f"fp64 numpy oracle (C1), row 0 of the cfg2 batch at completion tokens 1..{n} "
+                      f"(context {n_shared + question + 1}..{n_shared + question + n}); attention math only, "
+                      f"KV materialisation untimed; {wall:.1f} s of CPU work"}
+
+
+def run_reference(args):
+    """`--impl reference`: the oracle as it stands, timed on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.reference import OracleSequence, timed_attend
+    h, d, n_shared, seed = 32, 128, 2048, 0
+    K, W = args.steps, args.warmup
+    prompt = synth.token_ids(seed, synth.TAG_SYS, 0, n_shared).tolist()
+    seq = OracleSequence(seed, prompt, h, d, n_shared + W + K + 1)
+    times = []
+    cpu = 0.0
+    for s in range(W + K):
+        tok = int(synth.hash_py(seed, synth.TAG_DECODE, 0, s) % 31999 + 1)
+        seq.extend([tok])
+        q = synth.q_values(seed, torch.tensor([0]), s + 1, 1, h, d, alpha=8.0)[0, 0].numpy()
+        _, w, c = timed_attend(seq, q)
+        if s >= W:
+            times.append(w)
+            cpu += c
+    tot = sum(times)
+    value = K / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": K, "warmup": W, "ms_per_step": 1e3 * tot / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg2_llama2_7b_b32_s2048 (oracle: 1 sequence per step)", "b": 32, "h": h,
+                       "d": d, "c": 64, "n_shared": n_shared, "l2": "n/a (CPU)"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": max(1, round(cpu / tot)), "kind": "oracle",
+                             "sample": f"each step = one sequence's decode attention (fp64 numpy, C1) at context "
+                                       f"{n_shared + W + 1}..{n_shared + W + K}; KV materialisation untimed"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    K, W = args.steps, args.warmup
+    hbm_peak, peak_src, _ = load_peaks()
+    sampler = ClockSampler(local)
+    props = torch.cuda.get_device_properties(dev)
+    l2 = getattr(props, "L2_cache_size", 126 * 2 ** 20) or 126 * 2 ** 20
+    flush_buf = torch.empty(2 * l2 // 4 + 1024, dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(dev)
+    wl = DecodeWorkload(dev, seed=rank, steps=max(K, W), mode=args.mode, question=args.question,
+                        n_shared=args.n_shared, b=args.batch)
+    # warm-up on the same cache, then drain and refill: timed steps are tokens 1..K
+    wl.fill()
+    time_steps(wl, W, flush_buf, stream)
+    # spin the clocks up (~0.3 s of memsets) so the timed region runs at boost
+    t0 = time.time()
+    while time.time() - t0 < 0.3:
+        flush_l2(flush_buf)
+    torch.cuda.synchronize(dev)
+    # ---- pass A: the headline number (PDL on, no per-kernel events)
+    wl.fill()
+    c0 = wl.ca.counters()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    ms = time_steps(wl, K, flush_buf, stream)
+    torch.cuda.synchronize(dev)
+    c1 = wl.ca.counters()
+    total_ms = sum(ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+        torch.distributed.barrier()
+    launches = c1["launches"] - c0["launches"]
+    uploads = c1["uploads"] - c0["uploads"]
+    # ---- pass B: per-kernel CUDA events (roofline of the dominant kernel)
+    wl.fill()
+    wl.ca.set_option("kernel_events", 1)
+    wl.ca.kernel_times()
+    ms_b = time_steps(wl, K, flush_buf, stream)
+    kt = wl.ca.kernel_times()
+    wl.ca.set_option("kernel_events", 0)
+    shapes = [wl.shape_at(s) for s in range(K)]
+    kbytes = {"append": sum(x.append_bytes() for x in shapes),
+              "chunk_first": sum(x.chunk_first_bytes() for x in shapes),
+              "seq_first": sum(x.seq_first_bytes() for x in shapes)}
+    dom = max(("append", "chunk_first", "seq_first"), key=lambda k: kt[k][0])
+    dom_ms, dom_n = kt[dom]
+    achieved = kbytes[dom] / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(f"{args.mode}:{dom}")
+    kernels = {k: {"ms_total": kt[k][0], "launches": kt[k][1],
+                   "us_avg": 1e3 * kt[k][0] / kt[k][1] if kt[k][1] else None,
+                   "alg_bytes_per_launch": kbytes[k] / kt[k][1] if kt[k][1] and k in kbytes else None,
+                   "gbs": kbytes[k] / (kt[k][0] * 1e-3) / 1e9 if kt[k][0] and k in kbytes else None}
+               for k in ("append", "chunk_first", "seq_first")}
+    step_bytes = sum(x.unique_bytes() for x in shapes)
+    # ---- pass C: end to end through the C ABI with host buffers
+    wl.fill()
+    e2e_ms, h2d, d2h = time_e2e(wl, K, flush_buf, stream)
+    clocks = sampler.stop()
+    e2e_total = sum(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_total], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    value = world * wl.b * K / (total_ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16", "data": "synthetic",
+        "config": {"workload": f"cfg2_llama2_7b_b{wl.b}_s{wl.n_shared}" + ("" if args.mode == "chunk" else f"_{args.mode}"),
+                   "b_per_gpu": wl.b, "h": wl.h, "d": wl.d, "c": wl.c, "n_shared": wl.n_shared,
+                   "question": wl.question, "completion_tokens_timed": f"1..{K}", "mode": args.mode,
+                   "l2": "flushed between timed steps (2x L2 memset, outside the events)",
+                   "parallelism": f"independent batch per GPU x{world}"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
+                     "peak_source": peak_src, "avg_launch_us": 1e3 * dom_ms / dom_n if dom_n else None},
+        "kernels": kernels,
+        "step_unique_bytes_avg": step_bytes / K,
+        "step_gbs_vs_unique_bytes": step_bytes / (total_ms * 1e-3) / 1e9,
+        "passB_ms_per_step": sum(ms_b) / K,
+        "uploads_in_timed_region": uploads,
+        "e2e": {"value": world * wl.b * K / (e2e_total * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / K},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(0, wl.n_shared, wl.question, wl.h, wl.d, args.cpu_budget, 4096)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=512)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="chunk", choices=["chunk", "b0", "b1"])
+    ap.add_argument("--n-shared", dest="n_shared", type=int, default=2048)
+    ap.add_argument("--question", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--cpu-budget", dest="cpu_budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -72,6 +72,7 @@ _SIGS = {
     "chunkattn_memory_stats": (ctypes.c_int, [_P, _I64P]),
     "chunkattn_counters": (ctypes.c_int, [_P, _I64P]),
     "chunkattn_set_option": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.c_int64]),
+    "chunkattn_kernel_times": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double), _I64P]),
     "chunkattn_download_tables": (ctypes.c_int, [_P, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), _P]),
     "chunkattn_last_error": (ctypes.c_char_p, []),
 }

@@ -188,6 +188,13 @@ class ChunkAttention:
     def set_option(self, key: str, value: int) -> None:
         C.check(self.lib.chunkattn_set_option(self._h, key.encode(), int(value)))
 
+    def kernel_times(self) -> dict:
+        """{kind: (total ms, launches)} since the last call (option "kernel_events")."""
+        ms = (ctypes.c_double * 4)()
+        n = (ctypes.c_int64 * 4)()
+        C.check(self.lib.chunkattn_kernel_times(self._h, ms, n))
+        return {k: (ms[i], n[i]) for i, k in enumerate(["append", "chunk_first", "seq_first", "copy"])}
+
     def download_tables(self) -> np.ndarray:
         ln = ctypes.c_size_t()
         self.lib.chunkattn_download_tables(self._h, None, 0, ctypes.byref(ln), self._stream())

@@ -372,9 +372,11 @@ chunkattn_status chunkattn_add_sequence(chunkattn_t h, const int32_t* tokens, in
     if (h->set_device() != CA_OK) return CA_ECUDA;
     const size_t row_bytes = (size_t)h->cfg.num_layers * h->cfg.num_heads * h->cfg.head_dim * dtype_bytes(h->cfg.dtype);
     const size_t skip = (size_t)(mm - kv_first_pos) * row_bytes;
-    cudaError_t e = launch_copy_rows(h->pool, fresh.data(), (int32_t)fresh.size(), mm, n - mm,
-                                     static_cast<const char*>(k) + skip, static_cast<const char*>(v) + skip,
-                                     static_cast<cudaStream_t>(stream));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = h->timed_launch(chunkattn::K_COPY, st, [&] {
+      return launch_copy_rows(h->pool, fresh.data(), (int32_t)fresh.size(), mm, n - mm,
+                              static_cast<const char*>(k) + skip, static_cast<const char*>(v) + skip, st);
+    });
     if (e != cudaSuccess) return h->cuda_fail(e, "copy_rows");
     h->n_launches += (n - mm + 256LL * h->cfg.chunk_size - 1) / (256LL * h->cfg.chunk_size);
   }
@@ -419,7 +421,9 @@ chunkattn_status chunkattn_append_kv(chunkattn_t h, int64_t n, const int64_t* se
       h->append_ids.assign(seq_ids, seq_ids + n);
       h->append_epoch = h->ctx.epoch;
     }
-    cudaError_t e = launch_append_kv(h->pool, h->dev_tables(), (int32_t)n, k, v, st);
+    const DevTables t = h->dev_tables();
+    cudaError_t e = h->timed_launch(chunkattn::K_APPEND, st,
+                                    [&] { return launch_append_kv(h->pool, t, (int32_t)n, k, v, st); });
     if (e != cudaSuccess) return h->cuda_fail(e, "append_kv");
     ++h->n_launches;
   }
@@ -485,12 +489,15 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   a.cf_tensor_cores = h->tma_ok && !h->cf_simt;
   a.tmap_k = &h->tmk;
   a.tmap_v = &h->tmv;
-  a.use_pdl = h->use_pdl;
+  a.use_pdl = h->use_pdl && !h->kernel_events;
   const DevTables t = h->dev_tables();
-  cudaError_t e = launch_chunk_first(a, t, st);
-  if (e != cudaSuccess) return h->cuda_fail(e, "chunk_first");
-  if (t.n_cf_tiles > 0) ++h->n_launches;
-  e = launch_seq_first(a, t, st);
+  cudaError_t e = cudaSuccess;
+  if (t.n_cf_tiles > 0) {
+    e = h->timed_launch(chunkattn::K_CF, st, [&] { return launch_chunk_first(a, t, st); });
+    if (e != cudaSuccess) return h->cuda_fail(e, "chunk_first");
+    ++h->n_launches;
+  }
+  e = h->timed_launch(chunkattn::K_SF, st, [&] { return launch_seq_first(a, t, st); });
   if (e != cudaSuccess) return h->cuda_fail(e, "seq_first");
   ++h->n_launches;
   return CA_OK;
@@ -558,11 +565,30 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->cf_simt = value != 0;
   } else if (k == "pdl") {
     h->use_pdl = value != 0;
+  } else if (k == "kernel_events") {
+    if (h->host_only) return fail(CA_EINVAL, "host-only handle");
+    h->kernel_events = value != 0;
+    return CA_OK;
   } else {
     return fail(CA_EINVAL, "unknown option " + k);
   }
   h->ctx.epoch = -1;  // force a rebuild with the new schedule
   h->attend_epoch = h->append_epoch = -1;
+  return CA_OK;
+}
+
+chunkattn_status chunkattn_kernel_times(chunkattn_t h, double ms[4], int64_t launches[4]) {
+  if (!h || !ms || !launches) return fail(CA_EINVAL, "bad argument");
+  if (h->host_only) return fail(CA_EINVAL, "host-only handle");
+  if (h->set_device() != CA_OK) return CA_ECUDA;
+  cudaError_t e = h->flush_times();
+  if (e != cudaSuccess) return h->cuda_fail(e, "kernel_times");
+  for (int k = 0; k < 4; ++k) {
+    ms[k] = h->acc_ms[k];
+    launches[k] = h->acc_n[k];
+    h->acc_ms[k] = 0;
+    h->acc_n[k] = 0;
+  }
   return CA_OK;
 }
 
