@@ -88,8 +88,10 @@ typedef struct {
   void* k_pool;            /* device [L][max_chunks][h][c][d] dtype; chunk id = index  */
   void* v_pool;            /* device, same layout as k_pool                            */
   void* workspace;         /* device, >= chunkattn_workspace_bytes(config) bytes,
-                              16-byte aligned; holds the context tables and the
-                              fp32 partials [slot][h][d] + (m, n)[slot][h]            */
+                              16-byte aligned, ZERO-INITIALISED by the caller; holds
+                              the context tables, the fp32 chunk-first partials
+                              [slot][h][d + 4] (o, then m in log2 units, n) and the
+                              seq-first split-item counters (kept zero between calls) */
   size_t workspace_bytes;
 } chunkattn_buffers;
 

@@ -32,7 +32,7 @@ chunkattn_status fail(chunkattn_status s, const std::string& msg) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t attend_perm, append_row, tables, pO, pMN, total;
+  size_t attend_perm, append_row, tables, pO, pMN, segO, segMN, counters, total;
   int64_t table_cap, slot_cap;
 };
 
@@ -58,7 +58,9 @@ WsLayout ws_layout(const chunkattn_config* c) {
   w.slot_cap = B * msc;
   const int64_t sfcap = B * msc;
   w.table_cap = 4 * (B + 4) + 2 * (B + 5) + (sfcap + 4) + (w.slot_cap + 4) + (c->max_chunks + 4) +
-                kCfTileInts * (w.slot_cap + 1);
+                kCfTileInts * (w.slot_cap + 1) + kSfCtaInts * kMaxSfCtas + 4 +
+                (int64_t)kSfItemInts * B * c->num_heads + 4 +
+                (int64_t)kSfUnitInts * c->num_heads * B * (msc + 1) + 4;
   size_t o = 0;
   w.attend_perm = o;
   o = align_up(o + 4 * B, 256);
@@ -66,10 +68,16 @@ WsLayout ws_layout(const chunkattn_config* c) {
   o = align_up(o + 4 * B, 256);
   w.tables = o;
   o = align_up(o + 4 * w.table_cap, 256);
+  // chunk-first partials [slot][h][d + 4] fp32: o[0..d), m (log2 units) at d, n at d+1
   w.pO = o;
-  o = align_up(o + (size_t)4 * w.slot_cap * c->num_heads * c->head_dim, 256);
+  o = align_up(o + (size_t)4 * w.slot_cap * c->num_heads * (c->head_dim + 4), 256);
   w.pMN = o;
-  o = align_up(o + (size_t)8 * w.slot_cap * c->num_heads, 256);
+  // segment partials of seq-first items split across CTAs (<= 2 per CTA), same row format
+  w.segO = o;
+  o = align_up(o + (size_t)4 * 2 * kMaxSfCtas * (c->head_dim + 4), 256);
+  w.segMN = o;
+  w.counters = o;  // arrival counters of split items, [B][h] int32, zero between launches
+  o = align_up(o + (size_t)4 * B * c->num_heads, 256);
   w.total = o;
   return w;
 }
@@ -102,6 +110,8 @@ struct chunkattn {
   std::vector<int64_t> attend_ids;
   int64_t attend_epoch = -1;
   std::vector<int64_t> append_ids;
+  std::vector<int32_t> append_rows;
+  std::vector<AppendItem> append_items;
   int64_t append_epoch = -1;
   // counters
   int64_t n_builds = 0, n_uploads = 0, upload_bytes = 0, n_launches = 0;
@@ -227,7 +237,6 @@ struct chunkattn {
     const int32_t* base = reinterpret_cast<const int32_t*>(wsp + ws.tables);
     const BlobLayout& L = ctx.lay;
     t.row_caller = reinterpret_cast<const int32_t*>(wsp + ws.attend_perm);
-    t.append_row = reinterpret_cast<const int32_t*>(wsp + ws.append_row);
     t.seq_len = const_cast<int32_t*>(base + L.seq_len);
     t.sf_first = base + L.sf_first;
     t.last_chunk = base + L.last_chunk;
@@ -241,6 +250,10 @@ struct chunkattn {
     t.b = ctx.b;
     t.n_cf_tiles = ctx.n_cf_tiles;
     t.max_tile_rows = ctx.max_tile_rows;
+    t.sf_cta = base + L.sf_cta;
+    t.sf_item = base + L.sf_item;
+    t.sf_unit = base + L.sf_unit;
+    t.n_sf_ctas = ctx.n_sf_ctas;
     return t;
   }
 };
@@ -317,6 +330,7 @@ chunkattn_status chunkattn_create(const chunkattn_config* cfg, const chunkattn_b
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device) == cudaSuccess && sms > 0)
       h->num_sms = sms;
     h->sopt.cf_target_ctas = h->num_sms;
+    h->sopt.sf_ctas = 2 * h->num_sms;
     h->tma_ok = make_pool_tmaps(h->pool, &h->tmk, &h->tmv);
     const size_t pin_bytes = (size_t)4 * (h->ws.table_cap + 2 * cfg->max_batch + 64);
     for (int k = 0; k < 2; ++k) {
@@ -411,21 +425,29 @@ chunkattn_status chunkattn_append_kv(chunkattn_t h, int64_t n, const int64_t* se
   chunkattn_status s = h->ensure_context(st);       // tables with pre-step lengths
   if (s != CA_OK) return s;
   if (!h->host_only) {
+    // scatter list (row, chunk, slot, new length) travels with the launch
+    // parameters: steps that do not change the tree upload no table.
     const bool same = h->append_epoch == h->ctx.epoch && (int64_t)h->append_ids.size() == n &&
                       std::memcmp(h->append_ids.data(), seq_ids, n * sizeof(int64_t)) == 0;
     if (!same) {
-      std::vector<int32_t> rows(n);
-      for (int64_t i = 0; i < n; ++i) rows[i] = h->ctx.row_of.at(seq_ids[i]);
-      s = h->upload(h->wsp + h->ws.append_row, rows.data(), n * 4, st);
-      if (s != CA_OK) return s;
+      h->append_rows.resize(n);
+      for (int64_t i = 0; i < n; ++i) h->append_rows[i] = h->ctx.row_of.at(seq_ids[i]);
       h->append_ids.assign(seq_ids, seq_ids + n);
       h->append_epoch = h->ctx.epoch;
     }
+    h->append_items.resize(n);
+    for (int64_t i = 0; i < n; ++i) {
+      const Sequence* sq = h->tree.find(seq_ids[i]);
+      const int32_t chunk = sq->path.back();
+      h->append_items[i] = AppendItem{h->append_rows[i], chunk,
+                                      (int32_t)(sq->len - h->tree.node(chunk).start_pos), (int32_t)(sq->len + 1)};
+    }
     const DevTables t = h->dev_tables();
-    cudaError_t e = h->timed_launch(chunkattn::K_APPEND, st,
-                                    [&] { return launch_append_kv(h->pool, t, (int32_t)n, k, v, st); });
+    cudaError_t e = h->timed_launch(chunkattn::K_APPEND, st, [&] {
+      return launch_append_kv(h->pool, t, h->append_items.data(), (int32_t)n, k, v, st);
+    });
     if (e != cudaSuccess) return h->cuda_fail(e, "append_kv");
-    ++h->n_launches;
+    h->n_launches += (n + kMaxAppendItems - 1) / kMaxAppendItems;
   }
   h->tree.append_tokens(seq_ids, tokens, n);
   return CA_OK;
@@ -485,6 +507,9 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   a.out_dtype = h->cfg.out_dtype;
   a.pO = reinterpret_cast<float*>(h->wsp + h->ws.pO);
   a.pMN = reinterpret_cast<float2*>(h->wsp + h->ws.pMN);
+  a.segO = reinterpret_cast<float*>(h->wsp + h->ws.segO);
+  a.segMN = reinterpret_cast<float2*>(h->wsp + h->ws.segMN);
+  a.counters = reinterpret_cast<int32_t*>(h->wsp + h->ws.counters);
   a.scale_log2 = h->scale() * 1.4426950408889634f;
   a.cf_tensor_cores = h->tma_ok && !h->cf_simt;
   a.tmap_k = &h->tmk;
@@ -561,6 +586,8 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->cf_cpt_forced = value < 0 ? 0 : value;
   } else if (k == "cf_target_ctas") {
     h->sopt.cf_target_ctas = value < 1 ? 1 : value;
+  } else if (k == "sf_ctas") {
+    h->sopt.sf_ctas = value < 1 ? 1 : std::min<int64_t>(value, kMaxSfCtas);
   } else if (k == "cf_simt") {
     h->cf_simt = value != 0;
   } else if (k == "pdl") {

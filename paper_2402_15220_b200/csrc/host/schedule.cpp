@@ -98,13 +98,16 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   if (opt.cf_chunks_per_tile > 0) {
     cpt = std::min<int64_t>(opt.cf_chunks_per_tile, max_n);
   } else if (!runs.empty()) {
-    // cost = waves x chunks per tile (the per-CTA stream length); ties go to the
-    // larger tile (fewer partials).  One wave = cf_target_ctas CTAs.
+    // cost = waves x (chunks per tile + fixed per-CTA overhead, in chunk
+    // loads: prologue/epilogue latency and the partial written here and read
+    // back by the seq-first phase); ties go to the larger tile (fewer
+    // partials).  One wave = cf_target_ctas CTAs (1 CTA per SM).
+    constexpr int64_t kTileOverhead = 3;
     int64_t best = -1;
     for (int64_t t = max_n; t >= 1; --t) {
       count(t, &tiles, &slots);
       const int64_t waves = (tiles * opt.num_heads + opt.cf_target_ctas - 1) / opt.cf_target_ctas;
-      const int64_t cost = waves * t;
+      const int64_t cost = waves * (t + kTileOverhead);
       if (best < 0 || cost < best) {
         best = cost;
         cpt = t;
@@ -155,6 +158,58 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   X.n_cf_tiles = (int32_t)(cf_tile.size() / kCfTileInts);
   X.max_tile_rows = max_rows;
 
+  // ---- persistent seq-first schedule: items (row, head) in row-major order,
+  // each worth max(1, private chunks) units; CTA g takes units
+  // [U g / G, U (g+1) / G) (balanced, contiguous; stream-K style).  Items cut
+  // by a CTA boundary are finished by the last-arriving segment, which merges
+  // the segments in CTA order (deterministic).
+  const int32_t H = opt.num_heads;
+  std::vector<int64_t> row_u0(b + 1, 0);  // first unit of row r (all heads)
+  for (int32_t r = 0; r < b; ++r)
+    row_u0[r + 1] = row_u0[r] + (int64_t)H * std::max<int32_t>(1, sf_ptr[r + 1] - sf_ptr[r]);
+  const int64_t U = row_u0[b];
+  const int64_t G = b == 0 ? 0 : std::max<int64_t>(1, std::min<int64_t>({U, opt.sf_ctas, kMaxSfCtas}));
+  std::vector<int32_t> sf_cta(kSfCtaInts * G), sf_item((size_t)kSfItemInts * b * H, 0);
+  // per-unit descriptors {chunk id or -1, item, k, units of the item}
+  std::vector<int32_t> sf_unit((size_t)kSfUnitInts * U);
+  for (int32_t r = 0; r < b; ++r) {
+    const int32_t n = sf_ptr[r + 1] - sf_ptr[r], per = std::max<int32_t>(1, n);
+    for (int32_t hh = 0; hh < H; ++hh) {
+      const int64_t base = row_u0[r] + (int64_t)hh * per;
+      for (int32_t k = 0; k < per; ++k) {
+        int32_t* d = &sf_unit[(size_t)kSfUnitInts * (base + k)];
+        d[0] = n > 0 ? sf_chunk[sf_ptr[r] + k] : -1;
+        d[1] = r * H + hh;
+        d[2] = k;
+        d[3] = per;
+      }
+    }
+  }
+  int32_t seg_slots = 0;
+  for (int64_t g = 0; g < G; ++g) {
+    const int64_t u0 = U * g / G, u1 = U * (g + 1) / G;
+    sf_cta[kSfCtaInts * g + 0] = (int32_t)u0;
+    sf_cta[kSfCtaInts * g + 1] = (int32_t)u1;
+    // one segment for every item this CTA touches
+    int64_t u = u0;
+    while (u < u1) {
+      const int32_t* d = &sf_unit[(size_t)kSfUnitInts * u];
+      int32_t* rec = &sf_item[kSfItemInts * d[1]];
+      if (rec[1] == 0) rec[2] = (int32_t)g;  // first CTA of the item
+      rec[1] += 1;
+      u += d[3] - d[2];
+    }
+  }
+  for (int64_t i = 0; i < (int64_t)b * H; ++i) {
+    int32_t* rec = &sf_item[kSfItemInts * i];
+    if (rec[1] > 1) {
+      rec[0] = seg_slots;
+      seg_slots += rec[1];
+    }
+  }
+  X.n_sf_ctas = (int32_t)G;
+  X.n_seg_slots = seg_slots;
+
   // ---- pack the blob (seq_len first: the device copy is authoritative between
   // structural changes and is bumped by the append kernel)
   BlobLayout& L = X.lay;
@@ -174,6 +229,9 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   L.mg_slot = place((int64_t)mg_slot.size());
   L.cf_chunk = place((int64_t)cf_chunk.size());
   L.cf_tile = place((int64_t)cf_tile.size());
+  L.sf_cta = place((int64_t)sf_cta.size());
+  L.sf_item = place((int64_t)sf_item.size());
+  L.sf_unit = place((int64_t)sf_unit.size());
   L.total = o;
   if (o > opt.table_capacity) {
     *err = "context tables exceed workspace capacity";
@@ -193,6 +251,9 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   put(L.mg_slot, mg_slot);
   put(L.cf_chunk, cf_chunk);
   put(L.cf_tile, cf_tile);
+  put(L.sf_cta, sf_cta);
+  put(L.sf_item, sf_item);
+  put(L.sf_unit, sf_unit);
   X.epoch = tree.epoch();
   return true;
 }

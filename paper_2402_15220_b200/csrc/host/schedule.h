@@ -20,11 +20,23 @@ enum CfTileField { CF_CHUNK_OFF = 0, CF_NCHUNK, CF_ROW0, CF_ROW1, CF_SLOT, CF_RU
 constexpr int kCfTileInts = 8;
 constexpr int kMaxCfTileRows = 128;  // rows of one chunk-first tile (8 warps x 16 rows)
 
+// Seq-first CTA record (kSfCtaInts int32 each): a contiguous range of
+// (row, head, chunk) units [u0, u1) starting inside item `item0` at unit `off0`.
+constexpr int kSfCtaInts = 4;
+// Seq-first item record (kSfItemInts int32 each), item = row * h + head:
+// segment-partial slot base, number of CTA segments, first CTA.
+constexpr int kSfItemInts = 4;
+constexpr int kMaxSfCtas = 2048;
+// Seq-first unit descriptor (kSfUnitInts int32 each): {chunk id or -1 (row
+// without private chunks), item, chunk index k in the item, units of the item}.
+constexpr int kSfUnitInts = 4;
+
 struct ScheduleOptions {
   int32_t share_threshold = 2;
   int32_t num_heads = 1;
   int64_t cf_chunks_per_tile = 0;  // 0 = auto
   int64_t cf_target_ctas = 296;    // auto rule: heads * tiles >= this
+  int64_t sf_ctas = 296;           // persistent seq-first grid (<= kMaxSfCtas)
   int64_t slot_capacity = 0;       // partial slots available in the workspace
   int64_t table_capacity = 0;      // int32 entries available for the blob
 };
@@ -32,7 +44,7 @@ struct ScheduleOptions {
 // Offsets (int32 units) of the arrays inside the blob.
 struct BlobLayout {
   int64_t seq_len = 0, sf_first = 0, last_chunk = 0, last_start = 0, sf_ptr = 0, mg_ptr = 0,
-          sf_chunk = 0, mg_slot = 0, cf_chunk = 0, cf_tile = 0, total = 0;
+          sf_chunk = 0, mg_slot = 0, cf_chunk = 0, cf_tile = 0, sf_cta = 0, sf_item = 0, sf_unit = 0, total = 0;
 };
 
 struct Context {
@@ -48,6 +60,8 @@ struct Context {
   int32_t max_tile_rows = 0;
   int64_t n_slots = 0;
   int64_t cf_chunks_per_tile = 0;
+  int32_t n_sf_ctas = 0;
+  int32_t n_seg_slots = 0;  // segment partials of items split across CTAs
 };
 
 // Build the context of the current tree.  Returns false (and sets *err) when

@@ -15,29 +15,33 @@ namespace {
 
 constexpr int kThreads = 128;
 
+struct AppendList {
+  AppendItem it[kMaxAppendItems];
+};
+
+// One thread per 16-byte vector of the step's new K (and V): fully parallel,
+// no dependent loads (the scatter list arrives as kernel parameters).
 __global__ void __launch_bounds__(kThreads) append_kv_kernel(uint4* __restrict__ kpool, uint4* __restrict__ vpool,
                                                              const uint4* __restrict__ knew,
-                                                             const uint4* __restrict__ vnew, DevTables t,
-                                                             int64_t layer_stride_v, int32_t L, int32_t h,
-                                                             int32_t c, int32_t dv) {
-  const int i = blockIdx.x;
-  const int row = t.append_row[i];
-  const int chunk = t.last_chunk[row];
-  const int slot = t.seq_len[row] - t.last_start[row];
+                                                             const uint4* __restrict__ vnew,
+                                                             const __grid_constant__ AppendList list, int32_t n,
+                                                             int32_t* __restrict__ seq_len, int64_t layer_stride_v,
+                                                             int32_t L, int32_t h, int32_t c, int32_t dv) {
   const int per_layer = h * dv;  // 16-byte vectors per layer of one token
   const int total = L * per_layer;
-  for (int e = threadIdx.x; e < total; e += kThreads) {
-    const int l = e / per_layer;
-    const int r = e - l * per_layer;
-    const int hh = r / dv;
-    const int x = r - hh * dv;
-    const int64_t dst = l * layer_stride_v + ((int64_t)(chunk * h + hh) * c + slot) * dv + x;
-    const int64_t src = (int64_t)i * total + e;
-    kpool[dst] = knew[src];
-    vpool[dst] = vnew[src];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) t.seq_len[row] = slot + t.last_start[row] + 1;
+  const int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (e >= (int64_t)n * total) return;
+  const int i = (int)(e / total);
+  const int r0 = (int)(e - (int64_t)i * total);
+  const int l = r0 / per_layer;
+  const int r = r0 - l * per_layer;
+  const int hh = r / dv;
+  const int x = r - hh * dv;
+  const AppendItem it = list.it[i];
+  const int64_t dst = l * layer_stride_v + ((int64_t)(it.chunk * h + hh) * c + it.slot) * dv + x;
+  kpool[dst] = knew[e];
+  vpool[dst] = vnew[e];
+  if (r0 == 0) seq_len[it.row] = it.new_len;
 }
 
 struct ChunkList {
@@ -69,14 +73,23 @@ __global__ void __launch_bounds__(kThreads) copy_rows_kernel(uint4* __restrict__
 
 }  // namespace
 
-cudaError_t launch_append_kv(const PoolGeom& p, const DevTables& t, int32_t n, const void* k, const void* v,
-                             cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
+cudaError_t launch_append_kv(const PoolGeom& p, const DevTables& t, const AppendItem* items, int32_t n,
+                             const void* k, const void* v, cudaStream_t st) {
   const int E = dtype_bytes(p.dtype);
   const int dv = p.d * E / 16;
-  append_kv_kernel<<<n, kThreads, 0, st>>>((uint4*)p.k, (uint4*)p.v, (const uint4*)k, (const uint4*)v, t,
-                                           p.layer_stride * E / 16, p.num_layers, p.h, p.c, dv);
-  return cudaGetLastError();
+  const int64_t total = (int64_t)p.num_layers * p.h * dv;
+  static AppendList list;  // host staging of the parameter block (handle is single-writer)
+  for (int32_t i0 = 0; i0 < n; i0 += kMaxAppendItems) {
+    const int32_t m = std::min<int32_t>(kMaxAppendItems, n - i0);
+    std::copy(items + i0, items + i0 + m, list.it);
+    const int64_t vecs = (int64_t)m * total;
+    append_kv_kernel<<<(unsigned)((vecs + kThreads - 1) / kThreads), kThreads, 0, st>>>(
+        (uint4*)p.k, (uint4*)p.v, (const uint4*)k + i0 * total, (const uint4*)v + i0 * total, list, m, t.seq_len,
+        p.layer_stride * E / 16, p.num_layers, p.h, p.c, dv);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_copy_rows(const PoolGeom& p, const int32_t* chunks, int32_t n_chunks, int64_t first_pos,

@@ -225,9 +225,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       an = xa * nc + ya * an;
       am = mx;
     }
-    const size_t sl = (size_t)(slot0 + rloc) * h + head;
-    pO[sl * D + x] = ao;
-    if (x == 0) pMN[sl] = make_float2(am, an);
+    float* prow = pO + ((size_t)(slot0 + rloc) * h + head) * (D + 4);  // [o | m n pad pad]
+    prow[x] = ao;
+    if (x == 0) *reinterpret_cast<float4*>(prow + D) = make_float4(am, an, 0.f, 0.f);
   }
 }
 

@@ -24,8 +24,10 @@ struct DevTables {
   const int32_t* cf_tile;     // [n_cf_tiles][8] tile records (schedule.h)
   const int32_t* last_chunk;  // [b] append target chunk
   const int32_t* last_start;  // [b] its start position
-  const int32_t* append_row;  // [n] append caller index -> row
-  int32_t b, n_cf_tiles, max_tile_rows;
+  const int32_t* sf_cta;      // [n_sf_ctas][4] persistent seq-first ranges
+  const int32_t* sf_item;     // [b*h][4] split-item records
+  const int32_t* sf_unit;     // [units][4] unit descriptors
+  int32_t b, n_cf_tiles, max_tile_rows, n_sf_ctas;
 };
 
 struct PoolGeom {
@@ -43,8 +45,11 @@ struct AttnLaunch {
   const void* q;   // [n][h][d] dtype, caller order
   void* out;       // [n][h][d] out_dtype, caller order
   int32_t out_dtype;
-  float* pO;       // [slots][h][d]
-  float2* pMN;     // [slots][h]   (m in log2 units, n)
+  float* pO;       // [slots][h][d+4]: o, then m (log2 units), n
+  float2* pMN;     // unused (m, n live inside pO rows)
+  float* segO;     // [seg slots][d+4] seq-first segment partials, same format
+  float2* segMN;   // unused
+  int32_t* counters;  // [b*h] arrival counters (zero between launches)
   float scale_log2;
   bool cf_tensor_cores;  // use the mma chunk-first kernel
   const CUtensorMap* tmap_k;  // host copies (passed by value to kernels)
@@ -52,9 +57,13 @@ struct AttnLaunch {
   bool use_pdl;
 };
 
-// K1: scatter one decode step's K/V into the leaf chunks and bump seq_len.
-cudaError_t launch_append_kv(const PoolGeom& pool, const DevTables& t, int32_t n, const void* k,
-                             const void* v, cudaStream_t st);
+// K1: scatter one decode step's K/V into the leaf chunks and set seq_len.
+struct AppendItem {
+  int32_t row, chunk, slot, new_len;
+};
+constexpr int kMaxAppendItems = 1024;  // per launch (items travel as kernel parameters)
+cudaError_t launch_append_kv(const PoolGeom& pool, const DevTables& t, const AppendItem* items, int32_t n,
+                             const void* k, const void* v, cudaStream_t st);
 
 // Copy rows [first_pos, first_pos+m) of one sequence into its chunks
 // (chunk of position p = chunks[p/c - first_pos/c]); src [m][L][h][d].

@@ -1,21 +1,29 @@
-// K4 seq-first phase (Alg 2) and the SIMT chunk-first
-// fallback (Alg 1 for fp32 / shapes the tensor-core kernel does not take).
+// K4 seq-first phase (Alg 2) as a persistent, warp-
+// specialised kernel, and the SIMT chunk-first fallback (Alg 1) for fp32 and
+// shapes the tensor-core kernel does not take.
 //
-// One CTA per (row, head) [seq-first] or (tile row, head) [chunk-first SIMT].
-// The row's chunks are streamed (K and V tile of one (chunk, head): c x d,
-// contiguous in the pool) with 1-D bulk async copies into an NST-stage shared
-// memory ring; only the valid tokens of the last, partial chunk are copied and
-// the rest are masked by select (stale slots never enter the arithmetic).
-// 128 threads = G groups of d/VEC threads; a group owns every G-th token of a
-// chunk, computes its logits with 16-byte shared loads + FMA + shfl_xor
-// reduction and keeps its own online-softmax state (o, m, n) in registers
-// (Eqn 1 partial_attn fused with Eqn 2 attn_reduce, PAPER.md:95-108, 145-158;
-// m in log2 units, exp2 with log2(e) folded into the scale).  At the end the
-// groups merge in a fixed order through shared memory; the seq-first CTA then
-// merges the chunk-first partials listed for its row (fixed order, reading A12)
-// and writes O / n in the output dtype.
+// Seq-first work = items (row, head); an item's units are its private chunks
+// (max(1, n) units so rows without private chunks still merge their partials).
+// The host cuts the flattened unit list into one balanced contiguous range per
+// CTA (2 per SM).  Warp 0 is the producer: it reads the unit descriptors 32 at
+// a time (one lane each), and for every unit waits for a free stage of an
+// NST-deep shared-memory ring, publishes the unit's metadata in the stage and
+// issues 1-D bulk async copies (cp.async.bulk -> UBLKCP) of the K and V tile
+// of that (chunk, head) -- only the valid tokens of a partial last chunk --
+// plus the query row at a segment start and the chunk-first partial rows of
+// the item at its end, all completing on the stage's mbarrier.  Warps 1-4
+// consume: 8 groups of 16 threads (d = 128, fp16) each own every 8th token of
+// the chunk, computing logits with 16-byte shared loads + FMA + shfl_xor and
+// keeping an online-softmax state (Eqn 1 fused with Eqn 2, PAPER.md:95-108,
+// 145-158; m in log2 units).  At the end of an item the groups and the
+// chunk-first partials merge in a fixed order (n-ary Eqn 2: rebase to the
+// common max, sum in list order) and O / n is written.  An item
+// cut by a CTA boundary writes a segment partial; the last-arriving segment
+// (atomic counter) merges all segments in CTA order -- deterministic.
+// Stale slots past a partial chunk are never read (select, not multiply).
 #include <algorithm>
 
+#include "../host/schedule.h"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -25,29 +33,18 @@ using namespace dev;
 
 namespace {
 
-constexpr int kThreads = 128;
 constexpr int kMaxStages = 4;
-
-CA_DEV void merge_state(float& o, float& m, float& n, float oc, float mc, float nc) {
-  // Eqn 2 in log2 units; empty partials (m = -inf) skipped (reading A2).
-  const float mx = fmaxf(m, mc);
-  if (mx == -INFINITY) return;
-  const float x = fast_exp2(mc - mx);
-  const float y = fast_exp2(m - mx);
-  o = x * oc + y * o;
-  n = x * nc + y * n;
-  m = mx;
-}
 
 template <typename T, int D>
 struct Geo {
   static constexpr int kVec = Elem<T>::kVec;
-  static constexpr int kTpt = D / kVec;            // threads per token row
-  static constexpr int kGroups = kThreads / kTpt;  // token groups per CTA
+  static constexpr int kTpt = D / kVec;     // threads per token row
+  static constexpr int kGroups = 128 / kTpt;  // token groups per 128 consumer threads
   static_assert(kTpt <= 32 && (32 % kTpt) == 0, "group must sit inside a warp");
 };
 
-// One chunk tile in shared memory: nt valid tokens.
+// One chunk tile in shared memory with nt valid tokens, consumed by 128
+// threads (tid in [0,128)): group g owns tokens g, g + G, ...
 template <typename T, int D>
 CA_DEV void consume_chunk(const T* __restrict__ Ks, const T* __restrict__ Vs, int nt, const float* qf, float& m,
                           float& n, float* o, int g, int j) {
@@ -102,43 +99,270 @@ CA_DEV void consume_chunk(const T* __restrict__ Ks, const T* __restrict__ Vs, in
   }
 }
 
-// MODE 0: seq-first (grid b x h).  MODE 1: chunk-first SIMT (grid tiles x h x rows).
-template <typename T, typename TO, int D, int MODE>
-__global__ void __launch_bounds__(kThreads) attend_simt_kernel(const T* __restrict__ kpool,
-                                                               const T* __restrict__ vpool,
-                                                               const T* __restrict__ q, TO* __restrict__ out,
-                                                               float* __restrict__ pO, float2* __restrict__ pMN,
-                                                               DevTables t, int32_t h, int32_t c, float scale_log2,
-                                                               int32_t nst) {
+// ============================================================ seq-first ===
+constexpr int kProducerWarps = 1;
+constexpr int kConsumerWarps = 4;
+constexpr int kSfThreads = (kProducerWarps + kConsumerWarps) * 32;
+constexpr int kMaxPrefetchSlots = 4;  // chunk-first partial rows staged per item
+
+enum : int { F_FIRST = 1, F_LAST = 2, F_FULL = 4 };
+
+struct StageMeta {
+  int item, nt, flags, caller;
+  int mg0, mg1, seg, nsegs;
+};
+
+CA_DEV void named_sync_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory"); }
+
+CA_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <typename T, typename TO, int D>
+__global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
+    const T* __restrict__ kpool, const T* __restrict__ vpool, const T* __restrict__ q, TO* __restrict__ out,
+    const float* __restrict__ pO, float* __restrict__ segO, int32_t* __restrict__ counters, DevTables t,
+    int32_t h, int32_t c, float scale_log2, int32_t nst, uint32_t stage_bytes) {
   using G = Geo<T, D>;
+  constexpr int PR = D + 4;  // partial row floats
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
+  __shared__ StageMeta meta[kMaxStages];
+  __shared__ float sm_m[G::kGroups], sm_n[G::kGroups];
+  __shared__ float sm_o[G::kGroups][D];
+  __shared__ int sm_last;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int u0 = t.sf_cta[blockIdx.x * kSfCtaInts + 0], u1 = t.sf_cta[blockIdx.x * kSfCtaInts + 1];
+  const size_t tile_bytes = (size_t)c * D * sizeof(T);
+  // stage layout: K tile | V tile | q row | partial rows
+  auto stage_ptr = [&](int s) { return smem_raw + (size_t)s * stage_bytes; };
+
+  if (tid == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    int jj = 0;
+    for (int base = u0; base < u1; base += 32) {
+      const int u = base + lane;
+      int chunk = -1, item = 0, k = 0, per = 1, nt = 0, caller = 0, mg0 = 0, mg1 = 0, seg = -1, nsegs = 1;
+      int flags = 0;
+      if (u < u1) {
+        const int4 d = *reinterpret_cast<const int4*>(t.sf_unit + (size_t)u * kSfUnitInts);
+        chunk = d.x;
+        item = d.y;
+        k = d.z;
+        per = d.w;
+        const int row = item / h;
+        caller = t.row_caller[row];
+        mg0 = t.mg_ptr[row];
+        mg1 = t.mg_ptr[row + 1];
+        if (chunk >= 0) nt = min(c, t.seq_len[row] - (t.sf_first[row] + k * c));
+        const bool first = (u == u0) || k == 0;
+        const bool last = (u == u1 - 1) || k == per - 1;
+        const bool full = (u - k >= u0) && (u - k + per <= u1);
+        flags = (first ? F_FIRST : 0) | (last ? F_LAST : 0) | (full ? F_FULL : 0);
+        if (last && !full) {
+          const int4 rec = *reinterpret_cast<const int4*>(t.sf_item + (size_t)item * kSfItemInts);
+          nsegs = rec.y;
+          seg = rec.x + ((int)blockIdx.x - rec.z);
+        }
+      }
+      const int cnt = min(32, u1 - base);
+      for (int i = 0; i < cnt; ++i) {
+        const int i_chunk = __shfl_sync(0xffffffffu, chunk, i);
+        const int i_item = __shfl_sync(0xffffffffu, item, i);
+        const int i_nt = __shfl_sync(0xffffffffu, nt, i);
+        const int i_flags = __shfl_sync(0xffffffffu, flags, i);
+        const int i_caller = __shfl_sync(0xffffffffu, caller, i);
+        const int i_mg0 = __shfl_sync(0xffffffffu, mg0, i);
+        const int i_mg1 = __shfl_sync(0xffffffffu, mg1, i);
+        const int i_seg = __shfl_sync(0xffffffffu, seg, i);
+        const int i_nsegs = __shfl_sync(0xffffffffu, nsegs, i);
+        const int s = jj % nst;
+        const bool want_q = (i_flags & F_FIRST) && i_chunk >= 0;
+        const bool want_p = (i_flags & F_LAST) && (i_flags & F_FULL);
+        const int np = want_p ? min(i_mg1 - i_mg0, kMaxPrefetchSlots) : 0;
+        // partial slot ids for the prefetch (lanes 0..np-1)
+        int slot = 0;
+        if (lane < np) slot = t.mg_slot[i_mg0 + lane];
+        if (jj >= nst) mbar_wait(&empty_bar[s], (uint32_t)(((jj / nst) - 1) & 1));
+        unsigned char* st = stage_ptr(s);
+        const uint32_t kv_bytes = (uint32_t)(i_nt * D * (int)sizeof(T));
+        const uint32_t q_bytes = want_q ? (uint32_t)(D * sizeof(T)) : 0u;
+        const uint32_t p_bytes = (uint32_t)(np * PR * 4);
+        if (lane == 0) {
+          meta[s] = StageMeta{i_item, i_nt, i_flags, i_caller, i_mg0, i_mg1, i_seg, i_nsegs};
+          mbar_arrive_expect_tx(&full_bar[s], 2 * kv_bytes + q_bytes + p_bytes);
+          if (kv_bytes) {
+            const size_t off = ((size_t)i_chunk * h + (i_item % h)) * c * D;
+            bulk_g2s(st, kpool + off, kv_bytes, &full_bar[s]);
+            bulk_g2s(st + tile_bytes, vpool + off, kv_bytes, &full_bar[s]);
+          }
+          if (q_bytes) bulk_g2s(st + 2 * tile_bytes, q + ((size_t)i_caller * h + (i_item % h)) * D, q_bytes, &full_bar[s]);
+        }
+        __syncwarp();
+        if (lane < np) {
+          unsigned char* pdst = st + 2 * tile_bytes + D * sizeof(T) + (size_t)lane * PR * 4;
+          pdst = reinterpret_cast<unsigned char*>(((uintptr_t)pdst + 15) & ~(uintptr_t)15);
+          bulk_g2s(pdst, pO + ((size_t)slot * h + (i_item % h)) * PR, PR * 4, &full_bar[s]);
+        }
+        ++jj;
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int ct = tid - 32;  // 0..127
+  const int g = ct / G::kTpt, j = ct % G::kTpt;
+  float qf[G::kVec];
+  float m = -INFINITY, n = 0.f, o[G::kVec];
+  int jj = 0;
+  for (int u = u0; u < u1; ++u, ++jj) {
+    const int s = jj % nst;
+    mbar_wait(&full_bar[s], (uint32_t)((jj / nst) & 1));
+    const StageMeta md = meta[s];
+    const unsigned char* st = stage_ptr(s);
+    const T* Ks = reinterpret_cast<const T*>(st);
+    const T* Vs = reinterpret_cast<const T*>(st + tile_bytes);
+    if (md.flags & F_FIRST) {
+      m = -INFINITY;
+      n = 0.f;
+#pragma unroll
+      for (int v = 0; v < G::kVec; ++v) o[v] = 0.f;
+      if (md.nt > 0) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(st + 2 * tile_bytes + j * 16);
+        Elem<T>::to_float(raw, qf);
+#pragma unroll
+        for (int v = 0; v < G::kVec; ++v) qf[v] *= scale_log2;
+      }
+    }
+    if (md.nt > 0) consume_chunk<T, D>(Ks, Vs, md.nt, qf, m, n, o, g, j);
+    if (md.flags & F_LAST) {
+      // groups -> shared memory
+      if (j == 0) {
+        sm_m[g] = m;
+        sm_n[g] = n;
+      }
+#pragma unroll
+      for (int v = 0; v < G::kVec; ++v) sm_o[g][j * G::kVec + v] = o[v];
+      named_sync_consumers();
+      const int head = md.item % h;
+      const float* pst = reinterpret_cast<const float*>(
+          ((uintptr_t)(st + 2 * tile_bytes + D * sizeof(T)) + 15) & ~(uintptr_t)15);
+      if (md.flags & F_FULL) {
+        // whole item in this CTA: partials (staged, then global beyond the staging) + groups
+        const int np = min(md.mg1 - md.mg0, kMaxPrefetchSlots);
+        for (int x = ct; x < D; x += 128) {
+          float M = -INFINITY;
+          for (int e = 0; e < np; ++e) M = fmaxf(M, pst[e * PR + D]);
+          for (int e = md.mg0 + np; e < md.mg1; ++e) M = fmaxf(M, pO[((size_t)t.mg_slot[e] * h + head) * PR + D]);
+          for (int gg = 0; gg < G::kGroups; ++gg) M = fmaxf(M, sm_m[gg]);
+          float ao = 0.f, an = 0.f;
+          for (int e = 0; e < np; ++e) {
+            const float w = fast_exp2(pst[e * PR + D] - M);
+            ao = fmaf(w, pst[e * PR + x], ao);
+            an = fmaf(w, pst[e * PR + D + 1], an);
+          }
+          for (int e = md.mg0 + np; e < md.mg1; ++e) {
+            const float* pr = pO + ((size_t)t.mg_slot[e] * h + head) * PR;
+            const float w = fast_exp2(pr[D] - M);
+            ao = fmaf(w, pr[x], ao);
+            an = fmaf(w, pr[D + 1], an);
+          }
+          for (int gg = 0; gg < G::kGroups; ++gg) {
+            const float w = fast_exp2(sm_m[gg] - M);
+            ao = fmaf(w, sm_o[gg][x], ao);
+            an = fmaf(w, sm_n[gg], an);
+          }
+          Elem<TO>::store1(out + ((size_t)md.caller * h + head) * D + x, ao / an);
+        }
+      } else {
+        // segment of a split item: write the segment partial, count arrivals
+        for (int x = ct; x < D; x += 128) {
+          float M = -INFINITY;
+          for (int gg = 0; gg < G::kGroups; ++gg) M = fmaxf(M, sm_m[gg]);
+          float ao = 0.f, an = 0.f;
+          for (int gg = 0; gg < G::kGroups; ++gg) {
+            const float w = M == -INFINITY ? 0.f : fast_exp2(sm_m[gg] - M);
+            ao = fmaf(w, sm_o[gg][x], ao);
+            an = fmaf(w, sm_n[gg], an);
+          }
+          float* srow = segO + (size_t)md.seg * PR;
+          srow[x] = ao;
+          if (x == 0) {
+            srow[D] = M;
+            srow[D + 1] = an;
+          }
+        }
+        __threadfence();
+        named_sync_consumers();
+        if (ct == 0) sm_last = (atomicAdd(&counters[md.item], 1) == md.nsegs - 1);
+        named_sync_consumers();
+        if (sm_last) {
+          __threadfence();
+          const int4 rec = *reinterpret_cast<const int4*>(t.sf_item + (size_t)md.item * kSfItemInts);
+          for (int x = ct; x < D; x += 128) {
+            float M = -INFINITY;
+            for (int e = md.mg0; e < md.mg1; ++e) M = fmaxf(M, __ldcg(pO + ((size_t)t.mg_slot[e] * h + head) * PR + D));
+            for (int sgi = 0; sgi < md.nsegs; ++sgi) M = fmaxf(M, __ldcg(segO + (size_t)(rec.x + sgi) * PR + D));
+            float ao = 0.f, an = 0.f;
+            for (int e = md.mg0; e < md.mg1; ++e) {
+              const float* pr = pO + ((size_t)t.mg_slot[e] * h + head) * PR;
+              const float w = fast_exp2(__ldcg(pr + D) - M);
+              ao = fmaf(w, __ldcg(pr + x), ao);
+              an = fmaf(w, __ldcg(pr + D + 1), an);
+            }
+            for (int sgi = 0; sgi < md.nsegs; ++sgi) {
+              const float* sr = segO + (size_t)(rec.x + sgi) * PR;
+              const float w = fast_exp2(__ldcg(sr + D) - M);
+              ao = fmaf(w, __ldcg(sr + x), ao);
+              an = fmaf(w, __ldcg(sr + D + 1), an);
+            }
+            Elem<TO>::store1(out + ((size_t)md.caller * h + head) * D + x, ao / an);
+          }
+          if (ct == 0) counters[md.item] = 0;  // every segment has arrived: reset for the next launch
+        }
+      }
+      named_sync_consumers();  // sm_o / stage reuse
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
+  }
+}
+
+// ========================================================= chunk-first ====
+// SIMT chunk-first (grid tiles x h x rows): one CTA per (tile row, head)
+// streams the tile's chunks (full, reading T1) and writes the partial row.
+template <typename T, int D>
+__global__ void __launch_bounds__(128) cf_simt_kernel(const T* __restrict__ kpool, const T* __restrict__ vpool,
+                                                      const T* __restrict__ q, float* __restrict__ pO, DevTables t,
+                                                      int32_t h, int32_t c, float scale_log2, int32_t nst) {
+  using G = Geo<T, D>;
+  constexpr int PR = D + 4;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t bars[kMaxStages];
   __shared__ float sm_m[G::kGroups], sm_n[G::kGroups];
   __shared__ float sm_o[G::kGroups][D];
 
   const int head = blockIdx.y;
-  int row, n_chunks, first_pos, len, slot = -1;
-  const int32_t* chunks;
-  if (MODE == 0) {
-    row = blockIdx.x;
-    chunks = t.sf_chunk + t.sf_ptr[row];
-    n_chunks = t.sf_ptr[row + 1] - t.sf_ptr[row];
-    first_pos = t.sf_first[row];
-    len = t.seq_len[row];
-  } else {
-    const int32_t* tile = t.cf_tile + blockIdx.x * 8;
-    row = tile[2] + blockIdx.z;
-    if (row >= tile[3]) return;
-    chunks = t.cf_chunk + tile[0];
-    n_chunks = tile[1];
-    first_pos = 0;
-    len = 0x7fffffff;  // shared chunks are always full (reading T1)
-    slot = tile[4] + (int)blockIdx.z;
-  }
+  const int32_t* tile = t.cf_tile + blockIdx.x * kCfTileInts;
+  const int row = tile[CF_ROW0] + blockIdx.z;
+  if (row >= tile[CF_ROW1]) return;
+  const int32_t* chunks = t.cf_chunk + tile[CF_CHUNK_OFF];
+  const int n_chunks = tile[CF_NCHUNK];
+  const int slot = tile[CF_SLOT] + (int)blockIdx.z;
   const int caller = t.row_caller[row];
   const int tid = threadIdx.x;
   const int g = tid / G::kTpt, j = tid % G::kTpt;
-
   const size_t tile_elems = (size_t)c * D;
   T* Ks = reinterpret_cast<T*>(smem_raw);
   T* Vs = Ks + (size_t)nst * tile_elems;
@@ -148,20 +372,16 @@ __global__ void __launch_bounds__(kThreads) attend_simt_kernel(const T* __restri
     fence_barrier_init();
   }
   __syncthreads();
-
   auto issue = [&](int k) {
     const int s = k % nst;
-    const int cid = chunks[k];
-    const int nt = min(c, len - (first_pos + k * c));
-    const uint32_t bytes = (uint32_t)(nt * D * (int)sizeof(T));
-    const size_t off = ((size_t)cid * h + head) * tile_elems;
+    const uint32_t bytes = (uint32_t)(tile_elems * sizeof(T));
+    const size_t off = ((size_t)chunks[k] * h + head) * tile_elems;
     mbar_arrive_expect_tx(&bars[s], 2 * bytes);
     bulk_g2s(Ks + s * tile_elems, kpool + off, bytes, &bars[s]);
     bulk_g2s(Vs + s * tile_elems, vpool + off, bytes, &bars[s]);
   };
   if (tid == 0)
     for (int k = 0; k < min(nst, n_chunks); ++k) issue(k);
-
   float qf[G::kVec];
   {
     const uint4 raw = *reinterpret_cast<const uint4*>(q + ((size_t)caller * h + head) * D + j * G::kVec);
@@ -172,16 +392,13 @@ __global__ void __launch_bounds__(kThreads) attend_simt_kernel(const T* __restri
   float m = -INFINITY, n = 0.f, o[G::kVec];
 #pragma unroll
   for (int v = 0; v < G::kVec; ++v) o[v] = 0.f;
-
   for (int k = 0; k < n_chunks; ++k) {
     const int s = k % nst;
     mbar_wait(&bars[s], (uint32_t)((k / nst) & 1));
-    const int nt = min(c, len - (first_pos + k * c));
-    consume_chunk<T, D>(Ks + s * tile_elems, Vs + s * tile_elems, nt, qf, m, n, o, g, j);
-    __syncthreads();  // every group is done with stage s
+    consume_chunk<T, D>(Ks + s * tile_elems, Vs + s * tile_elems, c, qf, m, n, o, g, j);
+    __syncthreads();
     if (tid == 0 && k + nst < n_chunks) issue(k + nst);
   }
-
   if (j == 0) {
     sm_m[g] = m;
     sm_n[g] = n;
@@ -189,61 +406,66 @@ __global__ void __launch_bounds__(kThreads) attend_simt_kernel(const T* __restri
 #pragma unroll
   for (int v = 0; v < G::kVec; ++v) sm_o[g][j * G::kVec + v] = o[v];
   __syncthreads();
-
-  for (int x = tid; x < D; x += kThreads) {
-    float ao = 0.f, am = -INFINITY, an = 0.f;
-    if (MODE == 0) {
-      pdl_wait();  // chunk-first partials are complete (no-op without PDL)
-      for (int e = t.mg_ptr[row]; e < t.mg_ptr[row + 1]; ++e) {
-        const int sl = t.mg_slot[e];
-        const float2 mn = pMN[(size_t)sl * h + head];
-        merge_state(ao, am, an, pO[((size_t)sl * h + head) * D + x], mn.x, mn.y);
-      }
+  for (int x = tid; x < D; x += 128) {
+    float M = -INFINITY;
+    for (int gg = 0; gg < G::kGroups; ++gg) M = fmaxf(M, sm_m[gg]);
+    float ao = 0.f, an = 0.f;
+    for (int gg = 0; gg < G::kGroups; ++gg) {
+      const float w = fast_exp2(sm_m[gg] - M);
+      ao = fmaf(w, sm_o[gg][x], ao);
+      an = fmaf(w, sm_n[gg], an);
     }
-    for (int gg = 0; gg < G::kGroups; ++gg) merge_state(ao, am, an, sm_o[gg][x], sm_m[gg], sm_n[gg]);
-    if (MODE == 0) {
-      Elem<TO>::store1(out + ((size_t)caller * h + head) * D + x, ao / an);
-    } else {
-      pO[((size_t)slot * h + head) * D + x] = ao;
-      if (x == 0) pMN[(size_t)slot * h + head] = make_float2(am, an);
-    }
+    float* prow = pO + ((size_t)slot * h + head) * PR;
+    prow[x] = ao;
+    if (x == 0) *reinterpret_cast<float4*>(prow + D) = make_float4(M, an, 0.f, 0.f);
   }
 }
 
-template <typename T, typename TO, int D, int MODE>
-cudaError_t launch_simt(const AttnLaunch& a, const DevTables& t, dim3 grid, cudaStream_t st, bool pdl) {
+cudaError_t set_smem(const void* kern, size_t smem) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <typename T, typename TO, int D>
+cudaError_t launch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
+  const PoolGeom& p = a.pool;
+  const size_t kv = (size_t)2 * p.c * D * sizeof(T);
+  const size_t stage = (kv + D * sizeof(T) + 16 + (size_t)kMaxPrefetchSlots * (D + 4) * 4 + 127) / 128 * 128;
+  int nst = (int)std::min<size_t>(kMaxStages, (size_t)(108 * 1024) / stage);  // 2 CTAs / SM
+  nst = std::max(2, nst);
+  const size_t smem = nst * stage;
+  auto kern = sf_persistent_kernel<T, TO, D>;
+  cudaError_t e = set_smem((const void*)kern, smem);
+  if (e != cudaSuccess) return e;
+  const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
+  const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;
+  kern<<<t.n_sf_ctas, kSfThreads, smem, st>>>(kp, vp, (const T*)a.q, (TO*)a.out, a.pO, a.segO, a.counters, t, p.h,
+                                              p.c, a.scale_log2, nst, (uint32_t)stage);
+  return cudaGetLastError();
+}
+
+template <typename T, int D>
+cudaError_t launch_cf_simt(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   const PoolGeom& p = a.pool;
   const size_t stage = (size_t)2 * p.c * D * sizeof(T);
   int nst = (int)std::min<size_t>(3, (size_t)(160 * 1024) / stage);
   nst = std::max(1, nst);
   const size_t smem = nst * stage;
-  auto kern = attend_simt_kernel<T, TO, D, MODE>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = cf_simt_kernel<T, D>;
+  cudaError_t e = set_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  if (pdl) {
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-  }
-  return cudaLaunchKernelEx(&cfg, kern, kp, vp, (const T*)a.q, (TO*)a.out, a.pO, a.pMN, t, p.h, p.c, a.scale_log2,
-                            nst);
+  kern<<<dim3(t.n_cf_tiles, p.h, t.max_tile_rows), 128, smem, st>>>(kp, vp, (const T*)a.q, a.pO, t, p.h, p.c,
+                                                                     a.scale_log2, nst);
+  return cudaGetLastError();
 }
 
-template <typename T, int MODE>
-cudaError_t dispatch_d_out(const AttnLaunch& a, const DevTables& t, dim3 grid, cudaStream_t st, bool pdl) {
+template <typename T>
+cudaError_t dispatch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   const int d = a.pool.d;
-  const int od = MODE == 1 ? DT_F32 : a.out_dtype;
-#define CA_CASE(DD, TO)                                                           \
-  if (d == DD) return launch_simt<T, TO, DD, MODE>(a, t, grid, st, pdl);
+  const int od = a.out_dtype;
+#define CA_CASE(DD, TO) \
+  if (d == DD) return launch_sf<T, TO, DD>(a, t, st);
   if (od == DT_F32) {
     CA_CASE(64, float) CA_CASE(128, float)
   } else if (od == DT_F16) {
@@ -255,25 +477,31 @@ cudaError_t dispatch_d_out(const AttnLaunch& a, const DevTables& t, dim3 grid, c
   return cudaErrorInvalidValue;
 }
 
-template <int MODE>
-cudaError_t dispatch(const AttnLaunch& a, const DevTables& t, dim3 grid, cudaStream_t st, bool pdl) {
-  switch (a.pool.dtype) {
-    case DT_F32: return dispatch_d_out<float, MODE>(a, t, grid, st, pdl);
-    case DT_F16: return dispatch_d_out<__half, MODE>(a, t, grid, st, pdl);
-    default: return dispatch_d_out<__nv_bfloat16, MODE>(a, t, grid, st, pdl);
-  }
+template <typename T>
+cudaError_t dispatch_cf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
+  if (a.pool.d == 64) return launch_cf_simt<T, 64>(a, t, st);
+  if (a.pool.d == 128) return launch_cf_simt<T, 128>(a, t, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
 cudaError_t launch_seq_first(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   if (t.b == 0) return cudaSuccess;
-  return dispatch<0>(a, t, dim3(t.b, a.pool.h), st, a.use_pdl && t.n_cf_tiles > 0);
+  switch (a.pool.dtype) {
+    case DT_F32: return dispatch_sf<float>(a, t, st);
+    case DT_F16: return dispatch_sf<__half>(a, t, st);
+    default: return dispatch_sf<__nv_bfloat16>(a, t, st);
+  }
 }
 
 cudaError_t launch_chunk_first_simt(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   if (t.n_cf_tiles == 0) return cudaSuccess;
-  return dispatch<1>(a, t, dim3(t.n_cf_tiles, a.pool.h, t.max_tile_rows), st, false);
+  switch (a.pool.dtype) {
+    case DT_F32: return dispatch_cf<float>(a, t, st);
+    case DT_F16: return dispatch_cf<__half>(a, t, st);
+    default: return dispatch_cf<__nv_bfloat16>(a, t, st);
+  }
 }
 
 }  // namespace pakv
