@@ -85,7 +85,12 @@ typedef struct {
 
 /* Caller-owned device memory (the library never calls cudaMalloc). */
 typedef struct {
-  void* k_pool;            /* device [L][max_chunks][h][c][d] dtype; chunk id = index  */
+  void* k_pool;            /* device [L][max_chunks][h][c][d] dtype; chunk id = index.
+                              Within a token row the 16-byte groups are stored
+                              XOR-permuted by (slot % 8): logical group g of slot s
+                              lives at group g ^ (s & 7) -- a (chunk, head) tile is
+                              then bank-conflict free for ldmatrix after one 1-D
+                              bulk copy                    */
   void* v_pool;            /* device, same layout as k_pool                            */
   void* workspace;         /* device, >= chunkattn_workspace_bytes(config) bytes,
                               16-byte aligned, ZERO-INITIALISED by the caller; holds

@@ -95,9 +95,9 @@ struct chunkattn {
   // device
   PoolGeom pool{};
   char* wsp = nullptr;
-  CUtensorMap tmk{}, tmv{};
   bool tma_ok = false;
   bool cf_simt = false;
+  bool sf_simt = false;
   bool use_pdl = true;
   int num_sms = 148;
   int64_t cf_cpt_forced = 0;
@@ -331,7 +331,7 @@ chunkattn_status chunkattn_create(const chunkattn_config* cfg, const chunkattn_b
       h->num_sms = sms;
     h->sopt.cf_target_ctas = h->num_sms;
     h->sopt.sf_ctas = 2 * h->num_sms;
-    h->tma_ok = make_pool_tmaps(h->pool, &h->tmk, &h->tmv);
+    h->tma_ok = cf_mma_supported(h->pool);
     const size_t pin_bytes = (size_t)4 * (h->ws.table_cap + 2 * cfg->max_batch + 64);
     for (int k = 0; k < 2; ++k) {
       cudaError_t e = cudaHostAlloc((void**)&h->pinned[k], pin_bytes, cudaHostAllocDefault);
@@ -512,8 +512,7 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   a.counters = reinterpret_cast<int32_t*>(h->wsp + h->ws.counters);
   a.scale_log2 = h->scale() * 1.4426950408889634f;
   a.cf_tensor_cores = h->tma_ok && !h->cf_simt;
-  a.tmap_k = &h->tmk;
-  a.tmap_v = &h->tmv;
+  a.sf_tensor_cores = !h->sf_simt;
   a.use_pdl = h->use_pdl && !h->kernel_events;
   const DevTables t = h->dev_tables();
   cudaError_t e = cudaSuccess;
@@ -590,6 +589,8 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->sopt.sf_ctas = value < 1 ? 1 : std::min<int64_t>(value, kMaxSfCtas);
   } else if (k == "cf_simt") {
     h->cf_simt = value != 0;
+  } else if (k == "sf_simt") {
+    h->sf_simt = value != 0;
   } else if (k == "pdl") {
     h->use_pdl = value != 0;
   } else if (k == "kernel_events") {

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kThreads) append_kv_kernel(uint4* __restrict__
   const int hh = r / dv;
   const int x = r - hh * dv;
   const AppendItem it = list.it[i];
-  const int64_t dst = l * layer_stride_v + ((int64_t)(it.chunk * h + hh) * c + it.slot) * dv + x;
+  const int64_t dst = l * layer_stride_v + ((int64_t)(it.chunk * h + hh) * c + it.slot) * dv + dev::swz_chunk(it.slot, x);
   kpool[dst] = knew[e];
   vpool[dst] = vnew[e];
   if (r0 == 0) seq_len[it.row] = it.new_len;
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kThreads) copy_rows_kernel(uint4* __restrict__
     const int r = e - l * per_layer;
     const int hh = r / dv;
     const int x = r - hh * dv;
-    const int64_t dst = l * layer_stride_v + ((int64_t)(chunk * h + hh) * c + slot) * dv + x;
+    const int64_t dst = l * layer_stride_v + ((int64_t)(chunk * h + hh) * c + slot) * dv + dev::swz_chunk(slot, x);
     const int64_t src = i * total + e;
     kpool[dst] = ksrc[src];
     vpool[dst] = vsrc[src];

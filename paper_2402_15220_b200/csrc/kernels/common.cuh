@@ -22,6 +22,13 @@ CA_DEV float fast_exp2(float x) {  // ex2.approx: exp2(-inf) = +0
 
 CA_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// Pool layout: a (chunk, head) tile is c rows (tokens) x d elements, row-major,
+// with the 16-byte chunk index of every row XOR-ed by (token % 8).  A 1-D bulk
+// copy of the tile therefore lands in shared memory already bank-conflict free
+// for ldmatrix (8 consecutive tokens at one logical column hit 8 distinct
+// 16-byte bank groups).  Physical 16-byte chunk of logical chunk j of token t:
+CA_DEV int swz_chunk(int t, int j) { return j ^ (t & 7); }
+
 // ------------------------------------------------------------- mbarrier ---
 CA_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

@@ -52,8 +52,7 @@ struct AttnLaunch {
   int32_t* counters;  // [b*h] arrival counters (zero between launches)
   float scale_log2;
   bool cf_tensor_cores;  // use the mma chunk-first kernel
-  const CUtensorMap* tmap_k;  // host copies (passed by value to kernels)
-  const CUtensorMap* tmap_v;
+  bool sf_tensor_cores;  // use the mma consumers in the seq-first kernel (16-bit types)
   bool use_pdl;
 };
 
@@ -75,9 +74,6 @@ cudaError_t launch_chunk_first(const AttnLaunch& a, const DevTables& t, cudaStre
 // K4: seq-first phase (Alg 2) -> merged, normalised output.
 cudaError_t launch_seq_first(const AttnLaunch& a, const DevTables& t, cudaStream_t st);
 
-// Build the TMA descriptors of a 16-bit pool viewed as 2-D [rows][d], box
-// {64, c} with 128-byte swizzle.  Returns false if unsupported.
-bool make_pool_tmaps(const PoolGeom& pool, CUtensorMap* tk, CUtensorMap* tv);
 bool cf_mma_supported(const PoolGeom& pool);
 
 }  // namespace pakv

@@ -26,6 +26,7 @@
 #include "../host/schedule.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "mma_attn.cuh"
 
 namespace pakv {
 
@@ -58,7 +59,7 @@ CA_DEV void consume_chunk(const T* __restrict__ Ks, const T* __restrict__ Vs, in
       const int t = (it * U + u) * G::kGroups + g;
       float acc = 0.f;
       if (t < nt) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(Ks + (size_t)t * D + j * G::kVec);
+        const uint4 raw = *reinterpret_cast<const uint4*>(Ks + (size_t)t * D + swz_chunk(t, j) * G::kVec);
         float kf[G::kVec];
         Elem<T>::to_float(raw, kf);
 #pragma unroll
@@ -88,7 +89,7 @@ CA_DEV void consume_chunk(const T* __restrict__ Ks, const T* __restrict__ Vs, in
     for (int u = 0; u < U; ++u) {
       const int t = (it * U + u) * G::kGroups + g;
       if (t < nt) {  // select, not multiply: stale slots never enter the sum
-        const uint4 raw = *reinterpret_cast<const uint4*>(Vs + (size_t)t * D + j * G::kVec);
+        const uint4 raw = *reinterpret_cast<const uint4*>(Vs + (size_t)t * D + swz_chunk(t, j) * G::kVec);
         float vf[G::kVec];
         Elem<T>::to_float(raw, vf);
 #pragma unroll
@@ -118,230 +119,319 @@ CA_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <typename T, typename TO, int D>
+// Shared-memory state of one seq-first CTA.
+template <int D, int NG>
+struct SfShared {
+  uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
+  StageMeta meta[kMaxStages];
+  float m[NG], n[NG];
+  float o[NG][D];
+  int last;
+};
+
+// Stage layout: K tile | V tile | q row | chunk-first partial rows.
+template <typename T, int D>
+CA_DEV const float* stage_partials(const unsigned char* st, size_t tile_bytes) {
+  return reinterpret_cast<const float*>(st + 2 * tile_bytes + D * sizeof(T));
+}
+
+// Producer warp: walk the CTA's units 32 at a time (one descriptor per lane),
+// then for every unit wait for a free stage, publish its metadata and issue
+// the bulk copies (K, V valid rows; q at a segment start; partial rows at the
+// end of an item finished here), all completing on the stage's full barrier.
+template <typename T, int D, int NG>
+CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __restrict__ kpool,
+                       const T* __restrict__ vpool, const T* __restrict__ q, const float* __restrict__ pO,
+                       const DevTables& t, int h, int c, int nst, uint32_t stage_bytes, int u0, int u1, int lane) {
+  constexpr int PR = D + 4;
+  const size_t tile_bytes = (size_t)c * D * sizeof(T);
+  int jj = 0;
+  for (int base = u0; base < u1; base += 32) {
+    const int u = base + lane;
+    int chunk = -1, item = 0, k = 0, per = 1, nt = 0, caller = 0, mg0 = 0, mg1 = 0, seg = -1, nsegs = 1;
+    int flags = 0, slot4[kMaxPrefetchSlots] = {0, 0, 0, 0};
+    if (u < u1) {
+      const int4 d = *reinterpret_cast<const int4*>(t.sf_unit + (size_t)u * kSfUnitInts);
+      chunk = d.x;
+      item = d.y;
+      k = d.z;
+      per = d.w;
+      const int row = item / h;
+      caller = t.row_caller[row];
+      mg0 = t.mg_ptr[row];
+      mg1 = t.mg_ptr[row + 1];
+      if (chunk >= 0) nt = min(c, t.seq_len[row] - (t.sf_first[row] + k * c));
+      const bool first = (u == u0) || k == 0;
+      const bool last = (u == u1 - 1) || k == per - 1;
+      const bool full = (u - k >= u0) && (u - k + per <= u1);
+      flags = (first ? F_FIRST : 0) | (last ? F_LAST : 0) | (full ? F_FULL : 0);
+      if (last && !full) {
+        const int4 rec = *reinterpret_cast<const int4*>(t.sf_item + (size_t)item * kSfItemInts);
+        nsegs = rec.y;
+        seg = rec.x + ((int)blockIdx.x - rec.z);
+      }
+      if (last && full) {
+#pragma unroll
+        for (int e = 0; e < kMaxPrefetchSlots; ++e)
+          if (mg0 + e < mg1) slot4[e] = t.mg_slot[mg0 + e];
+      }
+    }
+    const int cnt = min(32, u1 - base);
+    for (int i = 0; i < cnt; ++i) {
+      const int i_chunk = __shfl_sync(0xffffffffu, chunk, i);
+      const int i_item = __shfl_sync(0xffffffffu, item, i);
+      const int i_nt = __shfl_sync(0xffffffffu, nt, i);
+      const int i_flags = __shfl_sync(0xffffffffu, flags, i);
+      const int i_caller = __shfl_sync(0xffffffffu, caller, i);
+      const int i_mg0 = __shfl_sync(0xffffffffu, mg0, i);
+      const int i_mg1 = __shfl_sync(0xffffffffu, mg1, i);
+      const int i_seg = __shfl_sync(0xffffffffu, seg, i);
+      const int i_nsegs = __shfl_sync(0xffffffffu, nsegs, i);
+      int my_slot = 0;
+#pragma unroll
+      for (int e = 0; e < kMaxPrefetchSlots; ++e) {
+        const int v = __shfl_sync(0xffffffffu, slot4[e], i);
+        if (lane == e) my_slot = v;
+      }
+      const int s = jj % nst;
+      const int head = i_item % h;
+      const bool want_q = (i_flags & F_FIRST) && i_chunk >= 0;
+      const bool want_p = (i_flags & F_LAST) && (i_flags & F_FULL);
+      const int np = want_p ? min(i_mg1 - i_mg0, kMaxPrefetchSlots) : 0;
+      if (jj >= nst) mbar_wait(&S.empty_bar[s], (uint32_t)(((jj / nst) - 1) & 1));
+      unsigned char* st = smem_raw + (size_t)s * stage_bytes;
+      const uint32_t kv_bytes = (uint32_t)(i_nt * D * (int)sizeof(T));
+      const uint32_t q_bytes = want_q ? (uint32_t)(D * sizeof(T)) : 0u;
+      const uint32_t p_bytes = (uint32_t)(np * PR * 4);
+      if (lane == 0) {
+        S.meta[s] = StageMeta{i_item, i_nt, i_flags, i_caller, i_mg0, i_mg1, i_seg, i_nsegs};
+        mbar_arrive_expect_tx(&S.full_bar[s], 2 * kv_bytes + q_bytes + p_bytes);
+        if (kv_bytes) {
+          const size_t off = ((size_t)i_chunk * h + head) * c * D;
+          bulk_g2s(st, kpool + off, kv_bytes, &S.full_bar[s]);
+          bulk_g2s(st + tile_bytes, vpool + off, kv_bytes, &S.full_bar[s]);
+        }
+        if (q_bytes) bulk_g2s(st + 2 * tile_bytes, q + ((size_t)i_caller * h + head) * D, q_bytes, &S.full_bar[s]);
+      }
+      __syncwarp();
+      if (lane < np) {
+        float* pdst = const_cast<float*>(stage_partials<T, D>(st, tile_bytes)) + lane * PR;
+        bulk_g2s(pdst, pO + ((size_t)my_slot * h + head) * PR, PR * 4, &S.full_bar[s]);
+      }
+      ++jj;
+    }
+  }
+}
+
+// End of an item segment: the NG consumer states sit in S.m/S.n/S.o.  A whole
+// item merges the chunk-first partials (staged rows first, the rest from
+// global) with the states and writes O / n; a segment of a split item writes
+// its partial and the last-arriving segment merges all of them in CTA order.
+// n-ary Eqn 2: rebase to the common max, sum in the fixed list order.
+template <typename TO, int D, int NG>
+CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* pst, const float* __restrict__ pO,
+                        float* __restrict__ segO, int32_t* __restrict__ counters, TO* __restrict__ out,
+                        const DevTables& t, int h, int ct) {
+  constexpr int PR = D + 4;
+  const int head = md.item % h;
+  if (md.flags & F_FULL) {
+    const int np = min(md.mg1 - md.mg0, kMaxPrefetchSlots);
+    for (int x = ct; x < D; x += kConsumerWarps * 32) {
+      float M = -INFINITY;
+      for (int e = 0; e < np; ++e) M = fmaxf(M, pst[e * PR + D]);
+      for (int e = md.mg0 + np; e < md.mg1; ++e) M = fmaxf(M, pO[((size_t)t.mg_slot[e] * h + head) * PR + D]);
+      for (int gg = 0; gg < NG; ++gg) M = fmaxf(M, S.m[gg]);
+      float ao = 0.f, an = 0.f;
+      for (int e = 0; e < np; ++e) {
+        const float w = fast_exp2(pst[e * PR + D] - M);
+        ao = fmaf(w, pst[e * PR + x], ao);
+        an = fmaf(w, pst[e * PR + D + 1], an);
+      }
+      for (int e = md.mg0 + np; e < md.mg1; ++e) {
+        const float* pr = pO + ((size_t)t.mg_slot[e] * h + head) * PR;
+        const float w = fast_exp2(pr[D] - M);
+        ao = fmaf(w, pr[x], ao);
+        an = fmaf(w, pr[D + 1], an);
+      }
+      for (int gg = 0; gg < NG; ++gg) {
+        const float w = fast_exp2(S.m[gg] - M);
+        ao = fmaf(w, S.o[gg][x], ao);
+        an = fmaf(w, S.n[gg], an);
+      }
+      Elem<TO>::store1(out + ((size_t)md.caller * h + head) * D + x, ao / an);
+    }
+    return;
+  }
+  for (int x = ct; x < D; x += kConsumerWarps * 32) {
+    float M = -INFINITY;
+    for (int gg = 0; gg < NG; ++gg) M = fmaxf(M, S.m[gg]);
+    float ao = 0.f, an = 0.f;
+    for (int gg = 0; gg < NG; ++gg) {
+      const float w = M == -INFINITY ? 0.f : fast_exp2(S.m[gg] - M);
+      ao = fmaf(w, S.o[gg][x], ao);
+      an = fmaf(w, S.n[gg], an);
+    }
+    float* srow = segO + (size_t)md.seg * PR;
+    srow[x] = ao;
+    if (x == 0) {
+      srow[D] = M;
+      srow[D + 1] = an;
+    }
+  }
+  __threadfence();
+  named_sync_consumers();
+  if (ct == 0) S.last = (atomicAdd(&counters[md.item], 1) == md.nsegs - 1);
+  named_sync_consumers();
+  if (!S.last) return;
+  __threadfence();
+  const int4 rec = *reinterpret_cast<const int4*>(t.sf_item + (size_t)md.item * kSfItemInts);
+  for (int x = ct; x < D; x += kConsumerWarps * 32) {
+    float M = -INFINITY;
+    for (int e = md.mg0; e < md.mg1; ++e) M = fmaxf(M, __ldcg(pO + ((size_t)t.mg_slot[e] * h + head) * PR + D));
+    for (int sg = 0; sg < md.nsegs; ++sg) M = fmaxf(M, __ldcg(segO + (size_t)(rec.x + sg) * PR + D));
+    float ao = 0.f, an = 0.f;
+    for (int e = md.mg0; e < md.mg1; ++e) {
+      const float* pr = pO + ((size_t)t.mg_slot[e] * h + head) * PR;
+      const float w = fast_exp2(__ldcg(pr + D) - M);
+      ao = fmaf(w, __ldcg(pr + x), ao);
+      an = fmaf(w, __ldcg(pr + D + 1), an);
+    }
+    for (int sg = 0; sg < md.nsegs; ++sg) {
+      const float* sr = segO + (size_t)(rec.x + sg) * PR;
+      const float w = fast_exp2(__ldcg(sr + D) - M);
+      ao = fmaf(w, __ldcg(sr + x), ao);
+      an = fmaf(w, __ldcg(sr + D + 1), an);
+    }
+    Elem<TO>::store1(out + ((size_t)md.caller * h + head) * D + x, ao / an);
+  }
+  if (ct == 0) counters[md.item] = 0;  // every segment has arrived: reset for the next launch
+}
+
+// MMA: consumers run WarpAttn with the row's query in row 0 of the 16-row
+// tile (warp cw owns the token slice [cw TPW, (cw+1) TPW) of each chunk).
+// SIMT (fp32 and fallback): 8 groups x 16 threads own every 8th token.
+template <typename T, typename TO, int D, bool MMA, int TPW>
 __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     const T* __restrict__ kpool, const T* __restrict__ vpool, const T* __restrict__ q, TO* __restrict__ out,
     const float* __restrict__ pO, float* __restrict__ segO, int32_t* __restrict__ counters, DevTables t,
     int32_t h, int32_t c, float scale_log2, int32_t nst, uint32_t stage_bytes) {
   using G = Geo<T, D>;
-  constexpr int PR = D + 4;  // partial row floats
+  constexpr int NG = MMA ? kConsumerWarps : G::kGroups;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
-  __shared__ StageMeta meta[kMaxStages];
-  __shared__ float sm_m[G::kGroups], sm_n[G::kGroups];
-  __shared__ float sm_o[G::kGroups][D];
-  __shared__ int sm_last;
+  __shared__ SfShared<D, NG> S;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int u0 = t.sf_cta[blockIdx.x * kSfCtaInts + 0], u1 = t.sf_cta[blockIdx.x * kSfCtaInts + 1];
   const size_t tile_bytes = (size_t)c * D * sizeof(T);
-  // stage layout: K tile | V tile | q row | partial rows
-  auto stage_ptr = [&](int s) { return smem_raw + (size_t)s * stage_bytes; };
 
+  // stale shared memory must be finite: masked MMA columns multiply P = 0 by it
+  for (size_t i = tid * 16; i < (size_t)nst * stage_bytes; i += kSfThreads * 16)
+    *reinterpret_cast<uint4*>(smem_raw + i) = make_uint4(0, 0, 0, 0);
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], kConsumerWarps);
+      mbar_init(&S.full_bar[s], 1);
+      mbar_init(&S.empty_bar[s], kConsumerWarps);
     }
     fence_barrier_init();
   }
+  fence_proxy_async();  // generic-proxy zero fill before async-proxy bulk writes
   __syncthreads();
 
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    int jj = 0;
-    for (int base = u0; base < u1; base += 32) {
-      const int u = base + lane;
-      int chunk = -1, item = 0, k = 0, per = 1, nt = 0, caller = 0, mg0 = 0, mg1 = 0, seg = -1, nsegs = 1;
-      int flags = 0;
-      if (u < u1) {
-        const int4 d = *reinterpret_cast<const int4*>(t.sf_unit + (size_t)u * kSfUnitInts);
-        chunk = d.x;
-        item = d.y;
-        k = d.z;
-        per = d.w;
-        const int row = item / h;
-        caller = t.row_caller[row];
-        mg0 = t.mg_ptr[row];
-        mg1 = t.mg_ptr[row + 1];
-        if (chunk >= 0) nt = min(c, t.seq_len[row] - (t.sf_first[row] + k * c));
-        const bool first = (u == u0) || k == 0;
-        const bool last = (u == u1 - 1) || k == per - 1;
-        const bool full = (u - k >= u0) && (u - k + per <= u1);
-        flags = (first ? F_FIRST : 0) | (last ? F_LAST : 0) | (full ? F_FULL : 0);
-        if (last && !full) {
-          const int4 rec = *reinterpret_cast<const int4*>(t.sf_item + (size_t)item * kSfItemInts);
-          nsegs = rec.y;
-          seg = rec.x + ((int)blockIdx.x - rec.z);
-        }
-      }
-      const int cnt = min(32, u1 - base);
-      for (int i = 0; i < cnt; ++i) {
-        const int i_chunk = __shfl_sync(0xffffffffu, chunk, i);
-        const int i_item = __shfl_sync(0xffffffffu, item, i);
-        const int i_nt = __shfl_sync(0xffffffffu, nt, i);
-        const int i_flags = __shfl_sync(0xffffffffu, flags, i);
-        const int i_caller = __shfl_sync(0xffffffffu, caller, i);
-        const int i_mg0 = __shfl_sync(0xffffffffu, mg0, i);
-        const int i_mg1 = __shfl_sync(0xffffffffu, mg1, i);
-        const int i_seg = __shfl_sync(0xffffffffu, seg, i);
-        const int i_nsegs = __shfl_sync(0xffffffffu, nsegs, i);
-        const int s = jj % nst;
-        const bool want_q = (i_flags & F_FIRST) && i_chunk >= 0;
-        const bool want_p = (i_flags & F_LAST) && (i_flags & F_FULL);
-        const int np = want_p ? min(i_mg1 - i_mg0, kMaxPrefetchSlots) : 0;
-        // partial slot ids for the prefetch (lanes 0..np-1)
-        int slot = 0;
-        if (lane < np) slot = t.mg_slot[i_mg0 + lane];
-        if (jj >= nst) mbar_wait(&empty_bar[s], (uint32_t)(((jj / nst) - 1) & 1));
-        unsigned char* st = stage_ptr(s);
-        const uint32_t kv_bytes = (uint32_t)(i_nt * D * (int)sizeof(T));
-        const uint32_t q_bytes = want_q ? (uint32_t)(D * sizeof(T)) : 0u;
-        const uint32_t p_bytes = (uint32_t)(np * PR * 4);
-        if (lane == 0) {
-          meta[s] = StageMeta{i_item, i_nt, i_flags, i_caller, i_mg0, i_mg1, i_seg, i_nsegs};
-          mbar_arrive_expect_tx(&full_bar[s], 2 * kv_bytes + q_bytes + p_bytes);
-          if (kv_bytes) {
-            const size_t off = ((size_t)i_chunk * h + (i_item % h)) * c * D;
-            bulk_g2s(st, kpool + off, kv_bytes, &full_bar[s]);
-            bulk_g2s(st + tile_bytes, vpool + off, kv_bytes, &full_bar[s]);
-          }
-          if (q_bytes) bulk_g2s(st + 2 * tile_bytes, q + ((size_t)i_caller * h + (i_item % h)) * D, q_bytes, &full_bar[s]);
-        }
-        __syncwarp();
-        if (lane < np) {
-          unsigned char* pdst = st + 2 * tile_bytes + D * sizeof(T) + (size_t)lane * PR * 4;
-          pdst = reinterpret_cast<unsigned char*>(((uintptr_t)pdst + 15) & ~(uintptr_t)15);
-          bulk_g2s(pdst, pO + ((size_t)slot * h + (i_item % h)) * PR, PR * 4, &full_bar[s]);
-        }
-        ++jj;
-      }
-    }
+    sf_produce<T, D, NG>(S, smem_raw, kpool, vpool, q, pO, t, h, c, nst, stage_bytes, u0, u1, lane);
     return;
   }
 
-  // -------------------------------------------------------------- consumers
   const int ct = tid - 32;  // 0..127
-  const int g = ct / G::kTpt, j = ct % G::kTpt;
-  float qf[G::kVec];
-  float m = -INFINITY, n = 0.f, o[G::kVec];
+  const int cw = warp - 1;  // consumer warp 0..3
   int jj = 0;
-  for (int u = u0; u < u1; ++u, ++jj) {
-    const int s = jj % nst;
-    mbar_wait(&full_bar[s], (uint32_t)((jj / nst) & 1));
-    const StageMeta md = meta[s];
-    const unsigned char* st = stage_ptr(s);
-    const T* Ks = reinterpret_cast<const T*>(st);
-    const T* Vs = reinterpret_cast<const T*>(st + tile_bytes);
-    if (md.flags & F_FIRST) {
-      m = -INFINITY;
-      n = 0.f;
+  if constexpr (MMA) {
+    using WA = WarpAttn<T, D, TPW>;
+    const int L = c / TPW;  // token slices per chunk (<= 4)
+    uint32_t qa[WA::KS][4];
+    WA wa;
+    wa.reset();
+    for (int u = u0; u < u1; ++u, ++jj) {
+      const int s = jj % nst;
+      mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
+      const StageMeta md = S.meta[s];
+      const unsigned char* st = smem_raw + (size_t)s * stage_bytes;
+      if (md.flags & F_FIRST) {
+        wa.reset();
+        if (md.nt > 0) {
+          const uint32_t* q32 = reinterpret_cast<const uint32_t*>(st + 2 * tile_bytes);
 #pragma unroll
-      for (int v = 0; v < G::kVec; ++v) o[v] = 0.f;
-      if (md.nt > 0) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(st + 2 * tile_bytes + j * 16);
-        Elem<T>::to_float(raw, qf);
-#pragma unroll
-        for (int v = 0; v < G::kVec; ++v) qf[v] *= scale_log2;
-      }
-    }
-    if (md.nt > 0) consume_chunk<T, D>(Ks, Vs, md.nt, qf, m, n, o, g, j);
-    if (md.flags & F_LAST) {
-      // groups -> shared memory
-      if (j == 0) {
-        sm_m[g] = m;
-        sm_n[g] = n;
-      }
-#pragma unroll
-      for (int v = 0; v < G::kVec; ++v) sm_o[g][j * G::kVec + v] = o[v];
-      named_sync_consumers();
-      const int head = md.item % h;
-      const float* pst = reinterpret_cast<const float*>(
-          ((uintptr_t)(st + 2 * tile_bytes + D * sizeof(T)) + 15) & ~(uintptr_t)15);
-      if (md.flags & F_FULL) {
-        // whole item in this CTA: partials (staged, then global beyond the staging) + groups
-        const int np = min(md.mg1 - md.mg0, kMaxPrefetchSlots);
-        for (int x = ct; x < D; x += 128) {
-          float M = -INFINITY;
-          for (int e = 0; e < np; ++e) M = fmaxf(M, pst[e * PR + D]);
-          for (int e = md.mg0 + np; e < md.mg1; ++e) M = fmaxf(M, pO[((size_t)t.mg_slot[e] * h + head) * PR + D]);
-          for (int gg = 0; gg < G::kGroups; ++gg) M = fmaxf(M, sm_m[gg]);
-          float ao = 0.f, an = 0.f;
-          for (int e = 0; e < np; ++e) {
-            const float w = fast_exp2(pst[e * PR + D] - M);
-            ao = fmaf(w, pst[e * PR + x], ao);
-            an = fmaf(w, pst[e * PR + D + 1], an);
-          }
-          for (int e = md.mg0 + np; e < md.mg1; ++e) {
-            const float* pr = pO + ((size_t)t.mg_slot[e] * h + head) * PR;
-            const float w = fast_exp2(pr[D] - M);
-            ao = fmaf(w, pr[x], ao);
-            an = fmaf(w, pr[D + 1], an);
-          }
-          for (int gg = 0; gg < G::kGroups; ++gg) {
-            const float w = fast_exp2(sm_m[gg] - M);
-            ao = fmaf(w, sm_o[gg][x], ao);
-            an = fmaf(w, sm_n[gg], an);
-          }
-          Elem<TO>::store1(out + ((size_t)md.caller * h + head) * D + x, ao / an);
-        }
-      } else {
-        // segment of a split item: write the segment partial, count arrivals
-        for (int x = ct; x < D; x += 128) {
-          float M = -INFINITY;
-          for (int gg = 0; gg < G::kGroups; ++gg) M = fmaxf(M, sm_m[gg]);
-          float ao = 0.f, an = 0.f;
-          for (int gg = 0; gg < G::kGroups; ++gg) {
-            const float w = M == -INFINITY ? 0.f : fast_exp2(sm_m[gg] - M);
-            ao = fmaf(w, sm_o[gg][x], ao);
-            an = fmaf(w, sm_n[gg], an);
-          }
-          float* srow = segO + (size_t)md.seg * PR;
-          srow[x] = ao;
-          if (x == 0) {
-            srow[D] = M;
-            srow[D + 1] = an;
+          for (int ks = 0; ks < WA::KS; ++ks) {
+            qa[ks][0] = lane < 4 ? q32[ks * 8 + lane] : 0u;
+            qa[ks][2] = lane < 4 ? q32[ks * 8 + 4 + lane] : 0u;
+            qa[ks][1] = qa[ks][3] = 0u;
           }
         }
-        __threadfence();
+      }
+      if (cw < L && cw * TPW < md.nt) {
+        const uint32_t k_u32 = smem_u32(st);
+        wa.template chunk<true>(qa, k_u32, k_u32 + (uint32_t)tile_bytes, cw * TPW, md.nt, scale_log2, lane);
+      }
+      if (md.flags & F_LAST) {
+        wa.finish();
+        if (lane < 4) {  // row 0 lives in lanes 0..3 (c0, c1 of every n-tile)
+          if (lane == 0) {
+            S.m[cw] = wa.m_lo;
+            S.n[cw] = wa.n_lo;
+          }
+#pragma unroll
+          for (int i = 0; i < WA::DT; ++i)
+            *reinterpret_cast<float2*>(&S.o[cw][i * 8 + lane * 2]) = make_float2(wa.o[i][0], wa.o[i][1]);
+        }
         named_sync_consumers();
-        if (ct == 0) sm_last = (atomicAdd(&counters[md.item], 1) == md.nsegs - 1);
-        named_sync_consumers();
-        if (sm_last) {
-          __threadfence();
-          const int4 rec = *reinterpret_cast<const int4*>(t.sf_item + (size_t)md.item * kSfItemInts);
-          for (int x = ct; x < D; x += 128) {
-            float M = -INFINITY;
-            for (int e = md.mg0; e < md.mg1; ++e) M = fmaxf(M, __ldcg(pO + ((size_t)t.mg_slot[e] * h + head) * PR + D));
-            for (int sgi = 0; sgi < md.nsegs; ++sgi) M = fmaxf(M, __ldcg(segO + (size_t)(rec.x + sgi) * PR + D));
-            float ao = 0.f, an = 0.f;
-            for (int e = md.mg0; e < md.mg1; ++e) {
-              const float* pr = pO + ((size_t)t.mg_slot[e] * h + head) * PR;
-              const float w = fast_exp2(__ldcg(pr + D) - M);
-              ao = fmaf(w, __ldcg(pr + x), ao);
-              an = fmaf(w, __ldcg(pr + D + 1), an);
-            }
-            for (int sgi = 0; sgi < md.nsegs; ++sgi) {
-              const float* sr = segO + (size_t)(rec.x + sgi) * PR;
-              const float w = fast_exp2(__ldcg(sr + D) - M);
-              ao = fmaf(w, __ldcg(sr + x), ao);
-              an = fmaf(w, __ldcg(sr + D + 1), an);
-            }
-            Elem<TO>::store1(out + ((size_t)md.caller * h + head) * D + x, ao / an);
-          }
-          if (ct == 0) counters[md.item] = 0;  // every segment has arrived: reset for the next launch
+        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, counters, out, t, h, ct);
+        named_sync_consumers();  // S.o / stage reuse
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty_bar[s]);
+    }
+  } else {
+    const int g = ct / G::kTpt, j = ct % G::kTpt;
+    float qf[G::kVec];
+    float m = -INFINITY, n = 0.f, o[G::kVec];
+    for (int u = u0; u < u1; ++u, ++jj) {
+      const int s = jj % nst;
+      mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
+      const StageMeta md = S.meta[s];
+      const unsigned char* st = smem_raw + (size_t)s * stage_bytes;
+      if (md.flags & F_FIRST) {
+        m = -INFINITY;
+        n = 0.f;
+#pragma unroll
+        for (int v = 0; v < G::kVec; ++v) o[v] = 0.f;
+        if (md.nt > 0) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(st + 2 * tile_bytes + j * 16);
+          Elem<T>::to_float(raw, qf);
+#pragma unroll
+          for (int v = 0; v < G::kVec; ++v) qf[v] *= scale_log2;
         }
       }
-      named_sync_consumers();  // sm_o / stage reuse
+      if (md.nt > 0)
+        consume_chunk<T, D>(reinterpret_cast<const T*>(st), reinterpret_cast<const T*>(st + tile_bytes), md.nt, qf,
+                            m, n, o, g, j);
+      if (md.flags & F_LAST) {
+        if (j == 0) {
+          S.m[g] = m;
+          S.n[g] = n;
+        }
+#pragma unroll
+        for (int v = 0; v < G::kVec; ++v) S.o[g][j * G::kVec + v] = o[v];
+        named_sync_consumers();
+        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, counters, out, t, h, ct);
+        named_sync_consumers();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty_bar[s]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[s]);
   }
+  (void)cw;
 }
 
-// ========================================================= chunk-first ====
-// SIMT chunk-first (grid tiles x h x rows): one CTA per (tile row, head)
-// streams the tile's chunks (full, reading T1) and writes the partial row.
 template <typename T, int D>
 __global__ void __launch_bounds__(128) cf_simt_kernel(const T* __restrict__ kpool, const T* __restrict__ vpool,
                                                       const T* __restrict__ q, float* __restrict__ pO, DevTables t,
@@ -425,15 +515,15 @@ cudaError_t set_smem(const void* kern, size_t smem) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-template <typename T, typename TO, int D>
+template <typename T, typename TO, int D, bool MMA, int TPW>
 cudaError_t launch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   const PoolGeom& p = a.pool;
   const size_t kv = (size_t)2 * p.c * D * sizeof(T);
-  const size_t stage = (kv + D * sizeof(T) + 16 + (size_t)kMaxPrefetchSlots * (D + 4) * 4 + 127) / 128 * 128;
+  const size_t stage = (kv + D * sizeof(T) + (size_t)kMaxPrefetchSlots * (D + 4) * 4 + 127) / 128 * 128;
   int nst = (int)std::min<size_t>(kMaxStages, (size_t)(108 * 1024) / stage);  // 2 CTAs / SM
   nst = std::max(2, nst);
   const size_t smem = nst * stage;
-  auto kern = sf_persistent_kernel<T, TO, D>;
+  auto kern = sf_persistent_kernel<T, TO, D, MMA, TPW>;
   cudaError_t e = set_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
@@ -460,12 +550,34 @@ cudaError_t launch_cf_simt(const AttnLaunch& a, const DevTables& t, cudaStream_t
   return cudaGetLastError();
 }
 
+// tokens per consumer warp of the MMA seq-first kernel (0 = use SIMT)
+int sf_tpw(const AttnLaunch& a) {
+  if (a.pool.dtype == DT_F32 || !a.sf_tensor_cores) return 0;
+  for (int tpw : {16, 32, 64})
+    if (a.pool.c % tpw == 0 && a.pool.c / tpw <= kConsumerWarps) return tpw;
+  return 0;
+}
+
+template <typename T, typename TO, int D>
+cudaError_t dispatch_sf_tpw(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
+  if constexpr (std::is_same<T, float>::value) {
+    return launch_sf<T, TO, D, false, 16>(a, t, st);
+  } else {
+    switch (sf_tpw(a)) {
+      case 16: return launch_sf<T, TO, D, true, 16>(a, t, st);
+      case 32: return launch_sf<T, TO, D, true, 32>(a, t, st);
+      case 64: return launch_sf<T, TO, D, true, 64>(a, t, st);
+      default: return launch_sf<T, TO, D, false, 16>(a, t, st);
+    }
+  }
+}
+
 template <typename T>
 cudaError_t dispatch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   const int d = a.pool.d;
   const int od = a.out_dtype;
 #define CA_CASE(DD, TO) \
-  if (d == DD) return launch_sf<T, TO, DD>(a, t, st);
+  if (d == DD) return dispatch_sf_tpw<T, TO, DD>(a, t, st);
   if (od == DT_F32) {
     CA_CASE(64, float) CA_CASE(128, float)
   } else if (od == DT_F16) {

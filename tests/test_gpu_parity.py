@@ -180,15 +180,16 @@ def test_split_invariance_and_simt_chunk_first(dt, odt):
     ref = hs.oracle(ids, q64)
     q = q64.to(hs.dev, hs.dt)
     for opt, val in [("cf_splits", 1), ("cf_splits", 2), ("cf_splits", 4), ("cf_splits", 32), ("cf_splits", 0),
-                     ("cf_simt", 1)]:
+                     ("cf_simt", 1), ("sf_simt", 1), ("sf_ctas", 1), ("sf_ctas", 7), ("sf_ctas", 333),
+                     ("sf_ctas", 2048)]:
         hs.ca.set_option(opt, val)
         o1 = hs.ca.attend(ids, q).clone()
         o2 = hs.ca.attend(ids, q).clone()
-        assert torch.equal(o1, o2)
+        assert torch.equal(o1, o2)                   # each fixed schedule is bitwise reproducible
         err = float(np.abs(o1.double().cpu().numpy() - ref).max())
         assert err <= 2e-3, (opt, val, err)
-        if opt == "cf_simt":
-            hs.ca.set_option("cf_simt", 0)
+        if opt in ("cf_simt", "sf_simt"):
+            hs.ca.set_option(opt, 0)
 
 
 def test_layers_independent():
@@ -213,11 +214,15 @@ def test_pool_contents_match_supplied_kv():
     torch.cuda.synchronize()
     kp = hs.ca.k_pool.cpu()
     vp = hs.ca.v_pool.cpu()
+    idx = torch.arange(64)
+
+    def unswz(row, s):  # 16-byte groups (8 x 16-bit) of slot s are XOR-permuted by s % 8
+        return row[:, ((idx // 8) ^ (s & 7)) * 8 + idx % 8]
     for sid in ids:
         k, v = hs.kv(hs.seqs[sid], list(range(len(hs.seqs[sid]))))
         slots = tm.token_slots(sid)
-        gk = torch.stack([kp[0, c, :, s, :] for c, s in slots]).double()
-        gv = torch.stack([vp[0, c, :, s, :] for c, s in slots]).double()
+        gk = torch.stack([unswz(kp[0, c, :, s, :], s) for c, s in slots]).double()
+        gv = torch.stack([unswz(vp[0, c, :, s, :], s) for c, s in slots]).double()
         assert torch.equal(gk, k[:, 0].cpu()) and torch.equal(gv, v[:, 0].cpu())
 
 
