@@ -32,7 +32,7 @@ chunkattn_status fail(chunkattn_status s, const std::string& msg) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t attend_perm, append_row, tables, pO, pMN, segO, segMN, counters, total;
+  size_t attend_perm, append_row, tables, pO, pMN, segO, segMN, counters, trace, total;
   int64_t table_cap, slot_cap;
 };
 
@@ -78,6 +78,8 @@ WsLayout ws_layout(const chunkattn_config* c) {
   w.segMN = o;
   w.counters = o;  // arrival counters of split items, [B][h] int32, zero between launches
   o = align_up(o + (size_t)4 * B * c->num_heads, 256);
+  w.trace = o;  // debug timeline (option "trace"): the last kTraceCtas*kTraceStride u64 words
+  o = align_up(o + (size_t)8 * kTraceCtas * kTraceStride, 256);
   w.total = o;
   return w;
 }
@@ -98,6 +100,8 @@ struct chunkattn {
   bool tma_ok = false;
   bool cf_simt = false;
   bool sf_simt = false;
+  int trace_kernel = 0;    // 1: trace seq-first, 2: trace chunk-first
+  int sf_ctas_per_sm = 2;  // persistent seq-first residency (smem budget per CTA)
   bool use_pdl = true;
   int num_sms = 148;
   int64_t cf_cpt_forced = 0;
@@ -513,6 +517,9 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   a.scale_log2 = h->scale() * 1.4426950408889634f;
   a.cf_tensor_cores = h->tma_ok && !h->cf_simt;
   a.sf_tensor_cores = !h->sf_simt;
+  a.trace = h->trace_kernel ? reinterpret_cast<uint64_t*>(h->wsp + h->ws.trace) : nullptr;
+  a.trace_cf = h->trace_kernel == 2;
+  a.sf_ctas_per_sm = h->sf_ctas_per_sm;
   a.use_pdl = h->use_pdl && !h->kernel_events;
   const DevTables t = h->dev_tables();
   cudaError_t e = cudaSuccess;
@@ -591,6 +598,12 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->cf_simt = value != 0;
   } else if (k == "sf_simt") {
     h->sf_simt = value != 0;
+  } else if (k == "trace") {
+    h->trace_kernel = (int)value;
+    return CA_OK;
+  } else if (k == "sf_ctas_per_sm") {
+    h->sf_ctas_per_sm = value <= 1 ? 1 : 2;
+    h->sopt.sf_ctas = (int64_t)h->sf_ctas_per_sm * h->num_sms;
   } else if (k == "pdl") {
     h->use_pdl = value != 0;
   } else if (k == "kernel_events") {

@@ -35,7 +35,7 @@ template <typename T, int D, int TPW>
 __global__ void __launch_bounds__(kThreads, 1)
     cf_mma_kernel(const T* __restrict__ kpool, const T* __restrict__ vpool, const T* __restrict__ q,
                   float* __restrict__ pO, DevTables t, int32_t h, int32_t C, int32_t L, float scale_log2,
-                  int32_t nst) {
+                  int32_t nst, uint64_t* __restrict__ trace) {
   using WA = WarpAttn<T, D, TPW>;
   constexpr int PR = D + 4;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -55,6 +55,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tile_bytes = (uint32_t)C * D * 2;
   const uint32_t stage_bytes = 2 * tile_bytes;
   const uint32_t base_u32 = smem_u32(smem_raw);
+  const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+  uint64_t* tr = trace && cta < kTraceCtas ? trace + (size_t)cta * kTraceStride : nullptr;
+  if (tr && tid == 0) tr[0] = globaltimer_ns();
 
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) mbar_init(&bars[s], 1);
@@ -69,6 +72,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_arrive_expect_tx(&bars[s], stage_bytes);
     bulk_g2s(ks, kpool + off, tile_bytes, &bars[s]);
     bulk_g2s(ks + tile_bytes, vpool + off, tile_bytes, &bars[s]);
+    if (tr && k < kTraceUnits) tr[3 + 2 * k] = globaltimer_ns();
   };
   if (tid == 0)
     for (int k = 0; k < min(nst, n_chunks); ++k) issue(k);
@@ -94,6 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int k = 0; k < n_chunks; ++k) {
     const int s = k % nst;
     mbar_wait(&bars[s], (uint32_t)((k / nst) & 1));
+    if (tr && tid == 0 && k < kTraceUnits) tr[4 + 2 * k] = globaltimer_ns();
     if (active) {
       const uint32_t ks_u32 = base_u32 + s * stage_bytes;
       wa.template chunk<false>(qa, ks_u32, ks_u32 + tile_bytes, lslice * TPW, C, scale_log2, lane);
@@ -149,6 +154,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     *reinterpret_cast<float4*>(pO + ((size_t)(slot0 + rloc) * h + head) * PR + x4) = acc;
   }
+  if (tr && tid == 0) {
+    tr[1] = tr[2] = globaltimer_ns();
+  }
 }
 
 template <typename T, int D, int TPW>
@@ -165,7 +173,7 @@ cudaError_t launch_mma(const AttnLaunch& a, const DevTables& t, int L, cudaStrea
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;
   kern<<<dim3(t.n_cf_tiles, p.h), kThreads, smem, st>>>(kp, vp, (const T*)a.q, a.pO, t, p.h, p.c, L, a.scale_log2,
-                                                          nst);
+                                                          nst, a.trace_cf ? a.trace : nullptr);
   return cudaGetLastError();
 }
 

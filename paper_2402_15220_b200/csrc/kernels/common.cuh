@@ -75,6 +75,12 @@ CA_DEV void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
 
+CA_DEV uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // PDL: let the dependent grid launch / wait for the primary grid.
 CA_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 CA_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

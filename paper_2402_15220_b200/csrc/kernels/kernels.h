@@ -30,6 +30,15 @@ struct DevTables {
   int32_t b, n_cf_tiles, max_tile_rows, n_sf_ctas;
 };
 
+// Trace record per CTA (debug timing, option "trace"): words
+//   [0] kernel entry, [1] producer done, [2] consumers done,
+//   [3 + 2u] producer issue time of unit u, [4 + 2u] consumer data-ready time
+// for the first kTraceUnits units.  Chunk-first uses the same layout per tile.
+constexpr int kTraceUnits = 61;
+constexpr int kTraceWords = 3 + 2 * kTraceUnits;  // 125 -> padded to 128
+constexpr int kTraceStride = 128;
+constexpr int kTraceCtas = 2048;
+
 struct PoolGeom {
   void* k;  // base of layer 0
   void* v;
@@ -51,6 +60,9 @@ struct AttnLaunch {
   float2* segMN;   // unused
   int32_t* counters;  // [b*h] arrival counters (zero between launches)
   float scale_log2;
+  uint64_t* trace;       // optional per-CTA timeline ([cta][kTraceWords] globaltimer ns), or null
+  bool trace_cf;         // trace the chunk-first kernel instead of seq-first
+  int sf_ctas_per_sm;    // 1 or 2: shared-memory budget of the seq-first CTA
   bool cf_tensor_cores;  // use the mma chunk-first kernel
   bool sf_tensor_cores;  // use the mma consumers in the seq-first kernel (16-bit types)
   bool use_pdl;

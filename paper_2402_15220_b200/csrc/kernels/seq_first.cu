@@ -34,7 +34,7 @@ using namespace dev;
 
 namespace {
 
-constexpr int kMaxStages = 4;
+constexpr int kMaxStages = 8;
 
 template <typename T, int D>
 struct Geo {
@@ -142,7 +142,8 @@ CA_DEV const float* stage_partials(const unsigned char* st, size_t tile_bytes) {
 template <typename T, int D, int NG>
 CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __restrict__ kpool,
                        const T* __restrict__ vpool, const T* __restrict__ q, const float* __restrict__ pO,
-                       const DevTables& t, int h, int c, int nst, uint32_t stage_bytes, int u0, int u1, int lane) {
+                       const DevTables& t, int h, int c, int nst, uint32_t stage_bytes, int u0, int u1, int lane,
+                       uint64_t* __restrict__ tr) {
   constexpr int PR = D + 4;
   const size_t tile_bytes = (size_t)c * D * sizeof(T);
   int jj = 0;
@@ -218,6 +219,7 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
         float* pdst = const_cast<float*>(stage_partials<T, D>(st, tile_bytes)) + lane * PR;
         bulk_g2s(pdst, pO + ((size_t)my_slot * h + head) * PR, PR * 4, &S.full_bar[s]);
       }
+      if (tr && lane == 0 && jj < kTraceUnits) tr[3 + 2 * jj] = globaltimer_ns();
       ++jj;
     }
   }
@@ -314,13 +316,16 @@ template <typename T, typename TO, int D, bool MMA, int TPW>
 __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     const T* __restrict__ kpool, const T* __restrict__ vpool, const T* __restrict__ q, TO* __restrict__ out,
     const float* __restrict__ pO, float* __restrict__ segO, int32_t* __restrict__ counters, DevTables t,
-    int32_t h, int32_t c, float scale_log2, int32_t nst, uint32_t stage_bytes) {
+    int32_t h, int32_t c, float scale_log2, int32_t nst, uint32_t stage_bytes,
+    uint64_t* __restrict__ trace) {
   using G = Geo<T, D>;
   constexpr int NG = MMA ? kConsumerWarps : G::kGroups;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ SfShared<D, NG> S;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t* tr = trace && blockIdx.x < kTraceCtas ? trace + (size_t)blockIdx.x * kTraceStride : nullptr;
+  if (tr && tid == 0) tr[0] = globaltimer_ns();
   const int u0 = t.sf_cta[blockIdx.x * kSfCtaInts + 0], u1 = t.sf_cta[blockIdx.x * kSfCtaInts + 1];
   const size_t tile_bytes = (size_t)c * D * sizeof(T);
 
@@ -338,7 +343,8 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
   __syncthreads();
 
   if (warp == 0) {
-    sf_produce<T, D, NG>(S, smem_raw, kpool, vpool, q, pO, t, h, c, nst, stage_bytes, u0, u1, lane);
+    sf_produce<T, D, NG>(S, smem_raw, kpool, vpool, q, pO, t, h, c, nst, stage_bytes, u0, u1, lane, tr);
+    if (tr && lane == 0) tr[1] = globaltimer_ns();
     return;
   }
 
@@ -354,6 +360,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     for (int u = u0; u < u1; ++u, ++jj) {
       const int s = jj % nst;
       mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
+      if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 2 * jj] = globaltimer_ns();
       const StageMeta md = S.meta[s];
       const unsigned char* st = smem_raw + (size_t)s * stage_bytes;
       if (md.flags & F_FIRST) {
@@ -397,6 +404,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     for (int u = u0; u < u1; ++u, ++jj) {
       const int s = jj % nst;
       mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
+      if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 2 * jj] = globaltimer_ns();
       const StageMeta md = S.meta[s];
       const unsigned char* st = smem_raw + (size_t)s * stage_bytes;
       if (md.flags & F_FIRST) {
@@ -430,6 +438,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     }
   }
   (void)cw;
+  if (tr && ct == 0) tr[2] = globaltimer_ns();
 }
 
 template <typename T, int D>
@@ -520,7 +529,8 @@ cudaError_t launch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) 
   const PoolGeom& p = a.pool;
   const size_t kv = (size_t)2 * p.c * D * sizeof(T);
   const size_t stage = (kv + D * sizeof(T) + (size_t)kMaxPrefetchSlots * (D + 4) * 4 + 127) / 128 * 128;
-  int nst = (int)std::min<size_t>(kMaxStages, (size_t)(108 * 1024) / stage);  // 2 CTAs / SM
+  const size_t budget = a.sf_ctas_per_sm == 1 ? (size_t)216 * 1024 : (size_t)108 * 1024;  // per CTA
+  int nst = (int)std::min<size_t>(kMaxStages, budget / stage);
   nst = std::max(2, nst);
   const size_t smem = nst * stage;
   auto kern = sf_persistent_kernel<T, TO, D, MMA, TPW>;
@@ -529,7 +539,7 @@ cudaError_t launch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) 
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;
   kern<<<t.n_sf_ctas, kSfThreads, smem, st>>>(kp, vp, (const T*)a.q, (TO*)a.out, a.pO, a.segO, a.counters, t, p.h,
-                                              p.c, a.scale_log2, nst, (uint32_t)stage);
+                                              p.c, a.scale_log2, nst, (uint32_t)stage, a.trace_cf ? nullptr : a.trace);
   return cudaGetLastError();
 }
 
