@@ -102,6 +102,7 @@ struct chunkattn {
   bool sf_simt = false;
   int trace_kernel = 0;    // 1: trace seq-first, 2: trace chunk-first
   int sf_ctas_per_sm = 2;  // persistent seq-first residency (smem budget per CTA)
+  int sf_prefetch = 0;     // seq-first L2 prefetch distance (units); measured slower on B200
   bool use_pdl = true;
   int num_sms = 148;
   int64_t cf_cpt_forced = 0;
@@ -520,6 +521,7 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   a.trace = h->trace_kernel ? reinterpret_cast<uint64_t*>(h->wsp + h->ws.trace) : nullptr;
   a.trace_cf = h->trace_kernel == 2;
   a.sf_ctas_per_sm = h->sf_ctas_per_sm;
+  a.sf_prefetch = h->sf_prefetch;
   a.use_pdl = h->use_pdl && !h->kernel_events;
   const DevTables t = h->dev_tables();
   cudaError_t e = cudaSuccess;
@@ -598,6 +600,9 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->cf_simt = value != 0;
   } else if (k == "sf_simt") {
     h->sf_simt = value != 0;
+  } else if (k == "sf_prefetch") {
+    h->sf_prefetch = value < 0 ? 0 : (int)std::min<int64_t>(value, 31);
+    return CA_OK;
   } else if (k == "trace") {
     h->trace_kernel = (int)value;
     return CA_OK;

@@ -5,6 +5,7 @@
 // PAPER.md:162).  Plus the prefill copy of a new sequence's private chunks.
 // Pure data movement: 16-byte vector loads/stores, one CTA per appended row.
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -15,16 +16,19 @@ namespace {
 
 constexpr int kThreads = 128;
 
+template <int NI>
 struct AppendList {
-  AppendItem it[kMaxAppendItems];
+  AppendItem it[NI];
 };
 
 // One thread per 16-byte vector of the step's new K (and V): fully parallel,
-// no dependent loads (the scatter list arrives as kernel parameters).
+// no dependent loads (the scatter list arrives as kernel parameters, sized to
+// the batch so small steps do not pay for a large parameter block).
+template <int NI>
 __global__ void __launch_bounds__(kThreads) append_kv_kernel(uint4* __restrict__ kpool, uint4* __restrict__ vpool,
                                                              const uint4* __restrict__ knew,
                                                              const uint4* __restrict__ vnew,
-                                                             const __grid_constant__ AppendList list, int32_t n,
+                                                             const __grid_constant__ AppendList<NI> list, int32_t n,
                                                              int32_t* __restrict__ seq_len, int64_t layer_stride_v,
                                                              int32_t L, int32_t h, int32_t c, int32_t dv) {
   const int per_layer = h * dv;  // 16-byte vectors per layer of one token
@@ -78,15 +82,22 @@ cudaError_t launch_append_kv(const PoolGeom& p, const DevTables& t, const Append
   const int E = dtype_bytes(p.dtype);
   const int dv = p.d * E / 16;
   const int64_t total = (int64_t)p.num_layers * p.h * dv;
-  static AppendList list;  // host staging of the parameter block (handle is single-writer)
-  for (int32_t i0 = 0; i0 < n; i0 += kMaxAppendItems) {
-    const int32_t m = std::min<int32_t>(kMaxAppendItems, n - i0);
+  auto run = [&](auto tag, int32_t i0, int32_t m) {
+    constexpr int NI = decltype(tag)::value;
+    thread_local AppendList<NI> list;  // host staging of the parameter block
     std::copy(items + i0, items + i0 + m, list.it);
     const int64_t vecs = (int64_t)m * total;
-    append_kv_kernel<<<(unsigned)((vecs + kThreads - 1) / kThreads), kThreads, 0, st>>>(
+    append_kv_kernel<NI><<<(unsigned)((vecs + kThreads - 1) / kThreads), kThreads, 0, st>>>(
         (uint4*)p.k, (uint4*)p.v, (const uint4*)k + i0 * total, (const uint4*)v + i0 * total, list, m, t.seq_len,
         p.layer_stride * E / 16, p.num_layers, p.h, p.c, dv);
-    cudaError_t e = cudaGetLastError();
+    return cudaGetLastError();
+  };
+  for (int32_t i0 = 0; i0 < n; i0 += kMaxAppendItems) {
+    const int32_t m = std::min<int32_t>(kMaxAppendItems, n - i0);
+    cudaError_t e;
+    if (m <= 32) e = run(std::integral_constant<int, 32>{}, i0, m);
+    else if (m <= 256) e = run(std::integral_constant<int, 256>{}, i0, m);
+    else e = run(std::integral_constant<int, kMaxAppendItems>{}, i0, m);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -27,10 +27,14 @@ cudaError_t launch_chunk_first_simt(const AttnLaunch& a, const DevTables& t, cud
 
 namespace {
 
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
-constexpr int kMaxStages = 4;
+constexpr int kWarps = 8;                // consumer warps: G row groups x L chunk lanes
+constexpr int kThreads = (kWarps + 1) * 32;  // + 1 producer warp
+constexpr int kMaxStages = 8;
 
+// Warp (g, l) owns query rows [16 g, 16 g + 16) of the tile and the chunks
+// k = l, l + L, ... -- whole chunks, TPW = min(c, 64) tokens per MMA pass --
+// so L chunks are attended concurrently with no CTA-wide sync per chunk.  The
+// producer warp refills a stage as soon as its G consumers release it.
 template <typename T, int D, int TPW>
 __global__ void __launch_bounds__(kThreads, 1)
     cf_mma_kernel(const T* __restrict__ kpool, const T* __restrict__ vpool, const T* __restrict__ q,
@@ -39,10 +43,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   using WA = WarpAttn<T, D, TPW>;
   constexpr int PR = D + 4;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t bars[kMaxStages];
+  __shared__ uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
   __shared__ float sm_m[kWarps][16], sm_n[kWarps][16];
-  __shared__ float sm_w[kWarps * 16][kWarps];  // per-row slice weights (epilogue)
-  __shared__ float sm_ninv[kWarps * 16];
+  __shared__ float sm_w[kWarps * 16][kWarps];  // per-row lane weights (epilogue)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int head = blockIdx.y;
@@ -50,8 +53,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int chunk_off = tile[CF_CHUNK_OFF], n_chunks = tile[CF_NCHUNK], row0 = tile[CF_ROW0], row1 = tile[CF_ROW1];
   const int slot0 = tile[CF_SLOT];
   const int rows = row1 - row0;
+  const int G = kWarps / L;  // row groups
   const int lslice = warp % L, rgroup = warp / L;
-  const bool active = rgroup * 16 < rows;
+  const bool consumer = warp < kWarps;
+  const bool active = consumer && rgroup * 16 < rows;
   const uint32_t tile_bytes = (uint32_t)C * D * 2;
   const uint32_t stage_bytes = 2 * tile_bytes;
   const uint32_t base_u32 = smem_u32(smem_raw);
@@ -60,26 +65,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tr && tid == 0) tr[0] = globaltimer_ns();
 
   if (tid == 0) {
-    for (int s = 0; s < nst; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], G);
+    }
     fence_barrier_init();
   }
   __syncthreads();
 
-  auto issue = [&](int k) {
-    const int s = k % nst;
-    const size_t off = ((size_t)t.cf_chunk[chunk_off + k] * h + head) * C * D;
-    unsigned char* ks = smem_raw + s * stage_bytes;
-    mbar_arrive_expect_tx(&bars[s], stage_bytes);
-    bulk_g2s(ks, kpool + off, tile_bytes, &bars[s]);
-    bulk_g2s(ks + tile_bytes, vpool + off, tile_bytes, &bars[s]);
-    if (tr && k < kTraceUnits) tr[3 + 2 * k] = globaltimer_ns();
-  };
-  if (tid == 0)
-    for (int k = 0; k < min(nst, n_chunks); ++k) issue(k);
+  if (warp == kWarps) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      for (int k = 0; k < n_chunks; ++k) {
+        const int s = k % nst;
+        if (k >= nst) mbar_wait(&empty_bar[s], (uint32_t)(((k / nst) - 1) & 1));
+        const size_t off = ((size_t)t.cf_chunk[chunk_off + k] * h + head) * C * D;
+        unsigned char* ks = smem_raw + s * stage_bytes;
+        mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+        bulk_g2s(ks, kpool + off, tile_bytes, &full_bar[s]);
+        bulk_g2s(ks + tile_bytes, vpool + off, tile_bytes, &full_bar[s]);
+        if (tr && k < kTraceUnits) tr[3 + 2 * k] = globaltimer_ns();
+      }
+    }
+  }
 
   // Q fragments (A operand, row-major 16 x 16 per k-step), rows gathered by caller index
   uint32_t qa[WA::KS][4];
-  {
+  WA wa;
+  wa.reset();
+  if (active) {
     const int rlo = row0 + rgroup * 16 + (lane >> 2), rhi = rlo + 8;
     const T* qlo = (active && rlo < row1) ? q + ((size_t)t.row_caller[rlo] * h + head) * D : nullptr;
     const T* qhi = (active && rhi < row1) ? q + ((size_t)t.row_caller[rhi] * h + head) * D : nullptr;
@@ -92,21 +106,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       qa[ks][3] = qhi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16 + 8 + cq) : 0u;
     }
   }
-
-  WA wa;
-  wa.reset();
-  for (int k = 0; k < n_chunks; ++k) {
-    const int s = k % nst;
-    mbar_wait(&bars[s], (uint32_t)((k / nst) & 1));
-    if (tr && tid == 0 && k < kTraceUnits) tr[4 + 2 * k] = globaltimer_ns();
-    if (active) {
-      const uint32_t ks_u32 = base_u32 + s * stage_bytes;
-      wa.template chunk<false>(qa, ks_u32, ks_u32 + tile_bytes, lslice * TPW, C, scale_log2, lane);
+  if (consumer) {
+    for (int k = lslice; k < n_chunks; k += L) {
+      const int s = k % nst;
+      mbar_wait(&full_bar[s], (uint32_t)((k / nst) & 1));
+      if (tr && lane == 0 && rgroup == 0 && k < kTraceUnits) tr[4 + 2 * k] = globaltimer_ns();
+      if (active) {
+        const uint32_t ks_u32 = base_u32 + s * stage_bytes;
+        for (int t0 = 0; t0 < C; t0 += TPW)
+          wa.template chunk<false>(qa, ks_u32, ks_u32 + tile_bytes, t0, C, scale_log2, lane);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&empty_bar[s]);
     }
-    __syncthreads();  // stage s fully consumed
-    if (tid == 0 && k + nst < n_chunks) issue(k + nst);
   }
   wa.finish();
+  __syncthreads();  // every stage drained (the epilogue reuses the ring)
 
   // ---- merge the L token slices of each row group (fixed order) -> partial
   float* smO = reinterpret_cast<float*>(smem_raw);  // [8 warps][16 rows][D]; stages are drained
@@ -163,7 +178,7 @@ template <typename T, int D, int TPW>
 cudaError_t launch_mma(const AttnLaunch& a, const DevTables& t, int L, cudaStream_t st) {
   const PoolGeom& p = a.pool;
   const size_t stage = (size_t)2 * p.c * D * 2;
-  int nst = (int)std::min<size_t>(kMaxStages, (size_t)(192 * 1024) / stage);
+  int nst = (int)std::min<size_t>(kMaxStages, (size_t)(200 * 1024) / stage);
   nst = std::max(1, nst);
   const size_t epi = (size_t)kWarps * 16 * D * 4;
   const size_t smem = std::max(nst * stage, epi);
@@ -187,15 +202,14 @@ cudaError_t dispatch_mma(const AttnLaunch& a, const DevTables& t, int tpw, int L
   return cudaErrorInvalidValue;
 }
 
-// token slices per chunk L (warps per row group) and tokens per warp TPW
+// chunk lanes L (= warps per row group; G = 8 / L row groups of 16 rows) and
+// tokens per MMA pass TPW (a warp walks its whole chunk in TPW-token passes)
 bool pick_slices(int c, int max_rows, int* L, int* tpw) {
-  const int groups = std::max(1, (max_rows + 15) / 16);  // <= 8
-  int l = std::min(8 / groups, c / 16);
-  while (l > 1 && (8 % l != 0 || c % l != 0 || (c / l) % 16 != 0)) --l;
-  const int tp = c / l;
-  if (tp > 64 || groups * l > 8) return false;
-  *L = l;
-  *tpw = tp;
+  int groups = 1;
+  while (groups * 16 < max_rows) groups *= 2;
+  if (groups > kWarps) return false;
+  *L = kWarps / groups;
+  *tpw = c % 64 == 0 ? 64 : (c % 32 == 0 ? 32 : 16);
   return true;
 }
 
@@ -211,6 +225,7 @@ cudaError_t launch_chunk_first(const AttnLaunch& a, const DevTables& t, cudaStre
   int L = 1, tpw = 16;
   if (!a.cf_tensor_cores || !cf_mma_supported(a.pool) || !pick_slices(a.pool.c, t.max_tile_rows, &L, &tpw))
     return launch_chunk_first_simt(a, t, st);
+  if (a.pool.d == 128 && tpw == 64) tpw = 32;  // keeps the d = 128 warp state under the register cap
   if (a.pool.dtype == DT_F16) return dispatch_mma<__half>(a, t, tpw, L, st);
   return dispatch_mma<__nv_bfloat16>(a, t, tpw, L, st);
 }

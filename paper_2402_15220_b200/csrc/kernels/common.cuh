@@ -41,6 +41,10 @@ CA_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+CA_DEV void mbar_arrive_cta(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 CA_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n"
@@ -61,6 +65,12 @@ CA_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) 
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Bulk prefetch global -> L2 (no shared memory, no completion): lets a kernel
+// keep far more HBM bytes in flight than its shared-memory ring holds.
+CA_DEV void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 // 2-D TMA tile load global -> shared (UTMALDG in SASS).

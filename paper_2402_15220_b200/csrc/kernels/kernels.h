@@ -63,6 +63,7 @@ struct AttnLaunch {
   uint64_t* trace;       // optional per-CTA timeline ([cta][kTraceWords] globaltimer ns), or null
   bool trace_cf;         // trace the chunk-first kernel instead of seq-first
   int sf_ctas_per_sm;    // 1 or 2: shared-memory budget of the seq-first CTA
+  int sf_prefetch;       // seq-first L2 prefetch distance in units (0 = off)
   bool cf_tensor_cores;  // use the mma chunk-first kernel
   bool sf_tensor_cores;  // use the mma consumers in the seq-first kernel (16-bit types)
   bool use_pdl;

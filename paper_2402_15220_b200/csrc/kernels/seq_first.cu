@@ -143,7 +143,7 @@ template <typename T, int D, int NG>
 CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __restrict__ kpool,
                        const T* __restrict__ vpool, const T* __restrict__ q, const float* __restrict__ pO,
                        const DevTables& t, int h, int c, int nst, uint32_t stage_bytes, int u0, int u1, int lane,
-                       uint64_t* __restrict__ tr) {
+                       uint64_t* __restrict__ tr, int pf) {
   constexpr int PR = D + 4;
   const size_t tile_bytes = (size_t)c * D * sizeof(T);
   int jj = 0;
@@ -176,6 +176,23 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
         for (int e = 0; e < kMaxPrefetchSlots; ++e)
           if (mg0 + e < mg1) slot4[e] = t.mg_slot[mg0 + e];
       }
+    }
+    // L2 prefetch descriptor of unit u + pf (issued by this lane when unit u goes out)
+    const T* pf_k = nullptr;
+    uint32_t pf_bytes = 0;
+    if (pf > 0 && u + pf < u1) {
+      const int4 d2 = *reinterpret_cast<const int4*>(t.sf_unit + (size_t)(u + pf) * kSfUnitInts);
+      if (d2.x >= 0) {
+        const int row2 = d2.y / h;
+        const int nt2 = min(c, t.seq_len[row2] - (t.sf_first[row2] + d2.z * c));
+        pf_k = kpool + ((size_t)d2.x * h + (d2.y % h)) * c * D;
+        pf_bytes = (uint32_t)(nt2 * D * (int)sizeof(T));
+      }
+    }
+    if (base == u0 && lane < pf && u < u1 && chunk >= 0) {  // the first pf units of the CTA
+      const size_t off = ((size_t)chunk * h + (item % h)) * c * D;
+      bulk_prefetch_l2(kpool + off, (uint32_t)(nt * D * (int)sizeof(T)));
+      bulk_prefetch_l2(vpool + off, (uint32_t)(nt * D * (int)sizeof(T)));
     }
     const int cnt = min(32, u1 - base);
     for (int i = 0; i < cnt; ++i) {
@@ -218,6 +235,10 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
       if (lane < np) {
         float* pdst = const_cast<float*>(stage_partials<T, D>(st, tile_bytes)) + lane * PR;
         bulk_g2s(pdst, pO + ((size_t)my_slot * h + head) * PR, PR * 4, &S.full_bar[s]);
+      }
+      if (lane == i && pf_bytes) {
+        bulk_prefetch_l2(pf_k, pf_bytes);
+        bulk_prefetch_l2(vpool + (pf_k - kpool), pf_bytes);
       }
       if (tr && lane == 0 && jj < kTraceUnits) tr[3 + 2 * jj] = globaltimer_ns();
       ++jj;
@@ -317,7 +338,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     const T* __restrict__ kpool, const T* __restrict__ vpool, const T* __restrict__ q, TO* __restrict__ out,
     const float* __restrict__ pO, float* __restrict__ segO, int32_t* __restrict__ counters, DevTables t,
     int32_t h, int32_t c, float scale_log2, int32_t nst, uint32_t stage_bytes,
-    uint64_t* __restrict__ trace) {
+    uint64_t* __restrict__ trace, int32_t pf) {
   using G = Geo<T, D>;
   constexpr int NG = MMA ? kConsumerWarps : G::kGroups;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -343,7 +364,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
   __syncthreads();
 
   if (warp == 0) {
-    sf_produce<T, D, NG>(S, smem_raw, kpool, vpool, q, pO, t, h, c, nst, stage_bytes, u0, u1, lane, tr);
+    sf_produce<T, D, NG>(S, smem_raw, kpool, vpool, q, pO, t, h, c, nst, stage_bytes, u0, u1, lane, tr, pf);
     if (tr && lane == 0) tr[1] = globaltimer_ns();
     return;
   }
@@ -539,7 +560,8 @@ cudaError_t launch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) 
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;
   kern<<<t.n_sf_ctas, kSfThreads, smem, st>>>(kp, vp, (const T*)a.q, (TO*)a.out, a.pO, a.segO, a.counters, t, p.h,
-                                              p.c, a.scale_log2, nst, (uint32_t)stage, a.trace_cf ? nullptr : a.trace);
+                                              p.c, a.scale_log2, nst, (uint32_t)stage, a.trace_cf ? nullptr : a.trace,
+                                              std::min(a.sf_prefetch, 31));
   return cudaGetLastError();
 }
 
