@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(kThreads) append_kv_kernel(uint4* __restrict__
                                                              const __grid_constant__ AppendList<NI> list, int32_t n,
                                                              int32_t* __restrict__ seq_len, int64_t layer_stride_v,
                                                              int32_t L, int32_t h, int32_t c, int32_t dv) {
+  dev::pdl_launch_dependents();  // chunk-first reads only shared chunks: it may start now
   const int per_layer = h * dv;  // 16-byte vectors per layer of one token
   const int total = L * per_layer;
   const int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;

@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cta = blockIdx.y * gridDim.x + blockIdx.x;
   uint64_t* tr = trace && cta < kTraceCtas ? trace + (size_t)cta * kTraceStride : nullptr;
   if (tr && tid == 0) tr[0] = globaltimer_ns();
+  pdl_launch_dependents();  // seq-first may start streaming unchanged private chunks
 
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) {
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
         bulk_g2s(ks, kpool + off, tile_bytes, &full_bar[s]);
         bulk_g2s(ks + tile_bytes, vpool + off, tile_bytes, &full_bar[s]);
-        if (tr && k < kTraceUnits) tr[3 + 2 * k] = globaltimer_ns();
+        if (tr && k < kTraceUnits) tr[3 + 3 * k] = globaltimer_ns();
       }
     }
   }
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int k = lslice; k < n_chunks; k += L) {
       const int s = k % nst;
       mbar_wait(&full_bar[s], (uint32_t)((k / nst) & 1));
-      if (tr && lane == 0 && rgroup == 0 && k < kTraceUnits) tr[4 + 2 * k] = globaltimer_ns();
+      if (tr && lane == 0 && rgroup == 0 && k < kTraceUnits) tr[4 + 3 * k] = globaltimer_ns();
       if (active) {
         const uint32_t ks_u32 = base_u32 + s * stage_bytes;
         for (int t0 = 0; t0 < C; t0 += TPW)
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&empty_bar[s]);
+      if (tr && lane == 0 && rgroup == 0 && k < kTraceUnits) tr[5 + 3 * k] = globaltimer_ns();
     }
   }
   wa.finish();
@@ -172,6 +174,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tr && tid == 0) {
     tr[1] = tr[2] = globaltimer_ns();
   }
+  // PDL chain append -> chunk-first -> seq-first: this grid started before the
+  // append finished; do not complete before it, so seq-first's single wait
+  // covers both predecessors.
+  pdl_wait();
 }
 
 template <typename T, int D, int TPW>
@@ -187,9 +193,9 @@ cudaError_t launch_mma(const AttnLaunch& a, const DevTables& t, int L, cudaStrea
   if (e != cudaSuccess) return e;
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;
-  kern<<<dim3(t.n_cf_tiles, p.h), kThreads, smem, st>>>(kp, vp, (const T*)a.q, a.pO, t, p.h, p.c, L, a.scale_log2,
-                                                          nst, a.trace_cf ? a.trace : nullptr);
-  return cudaGetLastError();
+  return launch_ex(kern, dim3(t.n_cf_tiles, p.h), dim3(kThreads), smem, st, a.use_pdl, kp, vp, (const T*)a.q, a.pO,
+                   t, (int32_t)p.h, (int32_t)p.c, (int32_t)L, a.scale_log2, (int32_t)nst,
+                   a.trace_cf ? a.trace : (uint64_t*)nullptr);
 }
 
 template <typename T>

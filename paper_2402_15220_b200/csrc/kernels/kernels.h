@@ -32,10 +32,11 @@ struct DevTables {
 
 // Trace record per CTA (debug timing, option "trace"): words
 //   [0] kernel entry, [1] producer done, [2] consumers done,
-//   [3 + 2u] producer issue time of unit u, [4 + 2u] consumer data-ready time
-// for the first kTraceUnits units.  Chunk-first uses the same layout per tile.
-constexpr int kTraceUnits = 61;
-constexpr int kTraceWords = 3 + 2 * kTraceUnits;  // 125 -> padded to 128
+//   [3 + 3u] producer issue time of unit u, [4 + 3u] consumer data-ready time,
+//   [5 + 3u] consumer done time, for the first kTraceUnits units.
+// Chunk-first uses the same layout per tile.
+constexpr int kTraceUnits = 41;
+constexpr int kTraceWords = 3 + 3 * kTraceUnits;  // 126 -> padded to 128
 constexpr int kTraceStride = 128;
 constexpr int kTraceCtas = 2048;
 

@@ -147,6 +147,7 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
   constexpr int PR = D + 4;
   const size_t tile_bytes = (size_t)c * D * sizeof(T);
   int jj = 0;
+  bool waited = false;  // PDL: append (new token, seq_len) and chunk-first (partials) complete
   for (int base = u0; base < u1; base += 32) {
     const int u = base + lane;
     int chunk = -1, item = 0, k = 0, per = 1, nt = 0, caller = 0, mg0 = 0, mg1 = 0, seg = -1, nsegs = 1;
@@ -161,7 +162,9 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
       caller = t.row_caller[row];
       mg0 = t.mg_ptr[row];
       mg1 = t.mg_ptr[row + 1];
-      if (chunk >= 0) nt = min(c, t.seq_len[row] - (t.sf_first[row] + k * c));
+      // only an item's last chunk can be partial -- and it is the one this
+      // step's append writes: its length is read after the PDL wait
+      if (chunk >= 0) nt = k < per - 1 ? c : (waited ? min(c, t.seq_len[row] - (t.sf_first[row] + k * c)) : -1);
       const bool first = (u == u0) || k == 0;
       const bool last = (u == u1 - 1) || k == per - 1;
       const bool full = (u - k >= u0) && (u - k + per <= u1);
@@ -198,7 +201,17 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
     for (int i = 0; i < cnt; ++i) {
       const int i_chunk = __shfl_sync(0xffffffffu, chunk, i);
       const int i_item = __shfl_sync(0xffffffffu, item, i);
-      const int i_nt = __shfl_sync(0xffffffffu, nt, i);
+      int i_nt = __shfl_sync(0xffffffffu, nt, i);
+      const int i_flags0 = __shfl_sync(0xffffffffu, flags, i);
+      if (!waited && (i_nt < 0 || ((i_flags0 & F_LAST) && (i_flags0 & F_FULL)))) {
+        pdl_wait();  // first unit touching this step's append / chunk-first output
+        waited = true;
+      }
+      if (i_nt < 0) {  // last chunk of an item described before the wait
+        const int row = i_item / h;
+        const int k_i = __shfl_sync(0xffffffffu, k, i);
+        i_nt = min(c, t.seq_len[row] - (t.sf_first[row] + k_i * c));
+      }
       const int i_flags = __shfl_sync(0xffffffffu, flags, i);
       const int i_caller = __shfl_sync(0xffffffffu, caller, i);
       const int i_mg0 = __shfl_sync(0xffffffffu, mg0, i);
@@ -240,7 +253,7 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
         bulk_prefetch_l2(pf_k, pf_bytes);
         bulk_prefetch_l2(vpool + (pf_k - kpool), pf_bytes);
       }
-      if (tr && lane == 0 && jj < kTraceUnits) tr[3 + 2 * jj] = globaltimer_ns();
+      if (tr && lane == 0 && jj < kTraceUnits) tr[3 + 3 * jj] = globaltimer_ns();
       ++jj;
     }
   }
@@ -257,6 +270,7 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
                         const DevTables& t, int h, int ct) {
   constexpr int PR = D + 4;
   const int head = md.item % h;
+  pdl_wait();  // chunk-first partials (and the append) complete; a no-op once satisfied
   if (md.flags & F_FULL) {
     const int np = min(md.mg1 - md.mg0, kMaxPrefetchSlots);
     for (int x = ct; x < D; x += kConsumerWarps * 32) {
@@ -381,7 +395,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     for (int u = u0; u < u1; ++u, ++jj) {
       const int s = jj % nst;
       mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
-      if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 2 * jj] = globaltimer_ns();
+      if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 3 * jj] = globaltimer_ns();
       const StageMeta md = S.meta[s];
       const unsigned char* st = smem_raw + (size_t)s * stage_bytes;
       if (md.flags & F_FIRST) {
@@ -417,6 +431,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty_bar[s]);
+      if (tr && ct == 0 && jj < kTraceUnits) tr[5 + 3 * jj] = globaltimer_ns();
     }
   } else {
     const int g = ct / G::kTpt, j = ct % G::kTpt;
@@ -425,7 +440,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     for (int u = u0; u < u1; ++u, ++jj) {
       const int s = jj % nst;
       mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
-      if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 2 * jj] = globaltimer_ns();
+      if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 3 * jj] = globaltimer_ns();
       const StageMeta md = S.meta[s];
       const unsigned char* st = smem_raw + (size_t)s * stage_bytes;
       if (md.flags & F_FIRST) {
@@ -456,6 +471,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty_bar[s]);
+      if (tr && ct == 0 && jj < kTraceUnits) tr[5 + 3 * jj] = globaltimer_ns();
     }
   }
   (void)cw;
@@ -473,6 +489,7 @@ __global__ void __launch_bounds__(128) cf_simt_kernel(const T* __restrict__ kpoo
   __shared__ float sm_m[G::kGroups], sm_n[G::kGroups];
   __shared__ float sm_o[G::kGroups][D];
 
+  pdl_launch_dependents();
   const int head = blockIdx.y;
   const int32_t* tile = t.cf_tile + blockIdx.x * kCfTileInts;
   const int row = tile[CF_ROW0] + blockIdx.z;
@@ -539,6 +556,7 @@ __global__ void __launch_bounds__(128) cf_simt_kernel(const T* __restrict__ kpoo
     prow[x] = ao;
     if (x == 0) *reinterpret_cast<float4*>(prow + D) = make_float4(M, an, 0.f, 0.f);
   }
+  pdl_wait();  // PDL chain: complete only after the append (see chunk_first.cu)
 }
 
 cudaError_t set_smem(const void* kern, size_t smem) {
@@ -559,10 +577,10 @@ cudaError_t launch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) 
   if (e != cudaSuccess) return e;
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;
-  kern<<<t.n_sf_ctas, kSfThreads, smem, st>>>(kp, vp, (const T*)a.q, (TO*)a.out, a.pO, a.segO, a.counters, t, p.h,
-                                              p.c, a.scale_log2, nst, (uint32_t)stage, a.trace_cf ? nullptr : a.trace,
-                                              std::min(a.sf_prefetch, 31));
-  return cudaGetLastError();
+  return launch_ex(kern, dim3(t.n_sf_ctas), dim3(kSfThreads), smem, st, a.use_pdl, kp, vp, (const T*)a.q,
+                   (TO*)a.out, (const float*)a.pO, a.segO, a.counters, t, (int32_t)p.h, (int32_t)p.c, a.scale_log2,
+                   (int32_t)nst, (uint32_t)stage, a.trace_cf ? (uint64_t*)nullptr : a.trace,
+                   (int32_t)std::min(a.sf_prefetch, 31));
 }
 
 template <typename T, int D>
@@ -577,9 +595,8 @@ cudaError_t launch_cf_simt(const AttnLaunch& a, const DevTables& t, cudaStream_t
   if (e != cudaSuccess) return e;
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;
-  kern<<<dim3(t.n_cf_tiles, p.h, t.max_tile_rows), 128, smem, st>>>(kp, vp, (const T*)a.q, a.pO, t, p.h, p.c,
-                                                                     a.scale_log2, nst);
-  return cudaGetLastError();
+  return launch_ex(kern, dim3(t.n_cf_tiles, p.h, t.max_tile_rows), dim3(128), smem, st, a.use_pdl, kp, vp,
+                   (const T*)a.q, a.pO, t, (int32_t)p.h, (int32_t)p.c, a.scale_log2, (int32_t)nst);
 }
 
 // tokens per consumer warp of the MMA seq-first kernel (0 = use SIMT)

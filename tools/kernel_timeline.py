@@ -21,7 +21,7 @@ import torch  # noqa: E402
 
 from bench import DecodeWorkload, flush_l2, time_steps  # noqa: E402
 
-TRACE_STRIDE, TRACE_CTAS, TRACE_UNITS = 128, 2048, 61
+TRACE_STRIDE, TRACE_CTAS, TRACE_UNITS = 128, 2048, 41
 
 
 def summarise(tr, name, ncta):
@@ -32,22 +32,29 @@ def summarise(tr, name, ncta):
     starts = (t[:, 0] - t0) / 1e3
     print(f"   CTA start offset us: min {starts.min():.2f} med {np.median(starts):.2f} max {starts.max():.2f}")
     print(f"   CTA active us: med {np.median((ends - t[:, 0]) / 1e3):.2f} max {((ends - t[:, 0]) / 1e3).max():.2f}")
-    lat, gap, first = [], [], []
+    lat, gap, first, comp, waitc = [], [], [], [], []
     for c in range(ncta):
-        issue = t[c, 3::2][:TRACE_UNITS]
-        ready = t[c, 4::2][:TRACE_UNITS]
-        n = int(((issue > 0) & (ready > 0)).sum())
-        if n == 0:
+        issue = t[c, 3::3][:TRACE_UNITS]
+        ready = t[c, 4::3][:TRACE_UNITS]
+        done = t[c, 5::3][:TRACE_UNITS]
+        ok = (issue > 0) & (ready > 0) & (done > 0)
+        if not ok.any():
             continue
         first.append((ready[0] - t[c, 0]) / 1e3)
-        for u in range(n):
+        prev_done = None
+        for u in np.nonzero(ok)[0]:
             lat.append((ready[u] - issue[u]) / 1e3)
-            if u:
-                gap.append((ready[u] - ready[u - 1]) / 1e3)
-    q = lambda v: f"p10 {np.percentile(v, 10):.2f} med {np.median(v):.2f} p90 {np.percentile(v, 90):.2f}" if v else "-"
+            comp.append((done[u] - ready[u]) / 1e3)
+            if prev_done is not None:
+                waitc.append(max(0, ready[u] - prev_done) / 1e3)
+                gap.append((ready[u] - ready[prev_u]) / 1e3)
+            prev_done, prev_u = done[u], u
+    q = lambda v: f"p10 {np.percentile(v, 10):.2f} med {np.median(v):.2f} p90 {np.percentile(v, 90):.2f} mean {np.mean(v):.2f}" if v else "-"
     print(f"   first data after entry us: {q(first)}")
     print(f"   load latency (ready - issue) us: {q(lat)}")
-    print(f"   gap between consecutive ready us: {q(gap)}")
+    print(f"   consume time (done - ready) us: {q(comp)}")
+    print(f"   consumer idle before unit (ready - prev done) us: {q(waitc)}")
+    print(f"   gap between consecutive traced ready us: {q(gap)}")
 
 
 def main():
