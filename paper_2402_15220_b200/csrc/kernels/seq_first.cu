@@ -127,6 +127,7 @@ struct SfShared {
   float m[NG], n[NG];
   float o[NG][D];
   int last;
+  int pdl_done;
 };
 
 // Stage layout: K tile | V tile | q row | chunk-first partial rows.
@@ -270,7 +271,11 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
                         const DevTables& t, int h, int ct) {
   constexpr int PR = D + 4;
   const int head = md.item % h;
-  pdl_wait();  // chunk-first partials (and the append) complete; a no-op once satisfied
+  if (!S.pdl_done) {  // chunk-first partials (and the append) complete -- waited once per CTA
+    pdl_wait();
+    named_sync_consumers();
+    if (ct == 0) S.pdl_done = 1;
+  }
   if (md.flags & F_FULL) {
     const int np = min(md.mg1 - md.mg0, kMaxPrefetchSlots);
     for (int x = ct; x < D; x += kConsumerWarps * 32) {
@@ -369,6 +374,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     *reinterpret_cast<uint4*>(smem_raw + i) = make_uint4(0, 0, 0, 0);
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) {
+      S.pdl_done = 0;
       mbar_init(&S.full_bar[s], 1);
       mbar_init(&S.empty_bar[s], kConsumerWarps);
     }
