@@ -359,6 +359,11 @@ def run_ours(args):
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get(f"{args.mode}:{dom}")
+    traffic_note = None
+    if isinstance(traffic, dict):  # one ncu --set full launch: its DRAM bytes vs its algorithmic bytes
+        traffic_note = {"alg_bytes_same_launch": traffic.get("alg_bytes"), "decode_step": traffic.get("step"),
+                        "capture": traffic.get("capture")}
+        traffic = traffic.get("bytes")
     kernels = {k: {"ms_total": kt[k][0], "launches": kt[k][1],
                    "us_avg": 1e3 * kt[k][0] / kt[k][1] if kt[k][1] else None,
                    "alg_bytes_per_launch": kbytes[k] / kt[k][1] if kt[k][1] and k in kbytes else None,
@@ -386,6 +391,7 @@ def run_ours(args):
                    "parallelism": f"independent batch per GPU x{world}"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
+                     "traffic_note": traffic_note,
                      "peak_source": peak_src, "avg_launch_us": 1e3 * dom_ms / dom_n if dom_n else None},
         "kernels": kernels,
         "step_unique_bytes_avg": step_bytes / K,

@@ -302,3 +302,26 @@ def test_two_level_tree_decode_evict():
         tm.remove_sequence(sid)
     st = hs.ca.memory_stats()
     assert st["used"] == 0 and st["free"] == st["created"]
+
+
+def test_head_sharded_handles_match_single_gpu():
+    """Two head-slice handles on one GPU (what two ranks hold) concatenate to the
+    single-handle output; with the same forced split they agree bitwise."""
+    H, d, c, seed = 8, 128, 64, 23
+    full = Harness(H, d, c, "f16", "f16", seed=seed, alpha=8.0)
+    ids = build_shared(full, 640, [3, 70, 0, 129])
+    halves = []
+    for h0 in (0, 4):
+        def kv_fn(which, toks, pos, h0=h0):
+            return synth.kv_values(seed, which, toks, pos, 1, 4, d, head_offset=h0)
+        hs = Harness(4, d, c, "f16", "f16", seed=seed, alpha=8.0, kv_fn=kv_fn)
+        build_shared(hs, 640, [3, 70, 0, 129])
+        halves.append(hs)
+    q64 = full.queries(ids)
+    for opt in (("cf_splits", 2), ("sf_ctas", 16)):
+        full.ca.set_option(*opt)
+        for hs in halves:
+            hs.ca.set_option(*opt)
+    ref = full.ca.attend(ids, q64.to(full.dev, full.dt).contiguous())
+    parts = [hs.ca.attend(ids, q64[:, i * 4:(i + 1) * 4].to(hs.dev, hs.dt).contiguous()) for i, hs in enumerate(halves)]
+    assert torch.equal(torch.cat(parts, dim=1), ref)
