@@ -306,7 +306,8 @@ def test_two_level_tree_decode_evict():
 
 def test_head_sharded_handles_match_single_gpu():
     """Two head-slice handles on one GPU (what two ranks hold) concatenate to the
-    single-handle output; with the same forced split they agree bitwise."""
+    single-handle output (the chunk-first split is forced equal; the seq-first
+    CTA ranges differ with the head count, so agreement is within rounding)."""
     H, d, c, seed = 8, 128, 64, 23
     full = Harness(H, d, c, "f16", "f16", seed=seed, alpha=8.0)
     ids = build_shared(full, 640, [3, 70, 0, 129])
@@ -324,4 +325,4 @@ def test_head_sharded_handles_match_single_gpu():
             hs.ca.set_option(*opt)
     ref = full.ca.attend(ids, q64.to(full.dev, full.dt).contiguous())
     parts = [hs.ca.attend(ids, q64[:, i * 4:(i + 1) * 4].to(hs.dev, hs.dt).contiguous()) for i, hs in enumerate(halves)]
-    assert torch.equal(torch.cat(parts, dim=1), ref)
+    assert float((torch.cat(parts, dim=1).double() - ref.double()).abs().max()) <= 1e-3
