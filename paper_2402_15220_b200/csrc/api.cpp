@@ -76,8 +76,8 @@ WsLayout ws_layout(const chunkattn_config* c) {
   w.segO = o;
   o = align_up(o + (size_t)4 * 2 * kMaxSfCtas * (c->head_dim + 4), 256);
   w.segMN = o;
-  w.counters = o;  // arrival counters of split items, [B][h] int32, zero between launches
-  o = align_up(o + (size_t)4 * B * c->num_heads, 256);
+  w.counters = o;  // release flags of segment partials [2 * kMaxSfCtas] u32 (zeroed; tag-compared)
+  o = align_up(o + (size_t)4 * 2 * kMaxSfCtas, 256);
   w.trace = o;  // debug timeline (option "trace"): the last kTraceCtas*kTraceStride u64 words
   o = align_up(o + (size_t)8 * kTraceCtas * kTraceStride, 256);
   w.total = o;
@@ -102,6 +102,7 @@ struct chunkattn {
   bool sf_simt = false;
   int trace_kernel = 0;    // 1: trace seq-first, 2: trace chunk-first
   int sf_ctas_per_sm = 2;  // persistent seq-first residency (smem budget per CTA)
+  uint32_t launch_tag = 0;
   int sf_prefetch = 0;     // seq-first L2 prefetch distance (units); measured slower on B200
   bool use_pdl = true;
   int num_sms = 148;
@@ -514,7 +515,10 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   a.pMN = reinterpret_cast<float2*>(h->wsp + h->ws.pMN);
   a.segO = reinterpret_cast<float*>(h->wsp + h->ws.segO);
   a.segMN = reinterpret_cast<float2*>(h->wsp + h->ws.segMN);
-  a.counters = reinterpret_cast<int32_t*>(h->wsp + h->ws.counters);
+  a.counters = nullptr;
+  a.segflags = reinterpret_cast<uint32_t*>(h->wsp + h->ws.counters);
+  if (++h->launch_tag == 0) ++h->launch_tag;  // flags compare against a nonzero per-launch tag
+  a.tag = h->launch_tag;
   a.scale_log2 = h->scale() * 1.4426950408889634f;
   a.cf_tensor_cores = h->tma_ok && !h->cf_simt;
   a.sf_tensor_cores = !h->sf_simt;

@@ -59,7 +59,9 @@ struct AttnLaunch {
   float2* pMN;     // unused (m, n live inside pO rows)
   float* segO;     // [seg slots][d+4] seq-first segment partials, same format
   float2* segMN;   // unused
-  int32_t* counters;  // [b*h] arrival counters (zero between launches)
+  int32_t* counters;  // unused
+  uint32_t* segflags;  // [seg slots] release flags of segment partials (== tag when written)
+  uint32_t tag;        // this launch's flag value (nonzero, increments per attend)
   float scale_log2;
   uint64_t* trace;       // optional per-CTA timeline ([cta][kTraceWords] globaltimer ns), or null
   bool trace_cf;         // trace the chunk-first kernel instead of seq-first

@@ -106,7 +106,7 @@ constexpr int kConsumerWarps = 4;
 constexpr int kSfThreads = (kProducerWarps + kConsumerWarps) * 32;
 constexpr int kMaxPrefetchSlots = 4;  // chunk-first partial rows staged per item
 
-enum : int { F_FIRST = 1, F_LAST = 2, F_FULL = 4 };
+enum : int { F_FIRST = 1, F_LAST = 2, F_FULL = 4, F_FINISH = 8 };
 
 struct StageMeta {
   int item, nt, flags, caller;
@@ -126,8 +126,9 @@ struct SfShared {
   StageMeta meta[kMaxStages];
   float m[NG], n[NG];
   float o[NG][D];
-  int last;
   int pdl_done;
+  int fix_pending;
+  StageMeta fix;  // split item this CTA finishes after its own units
 };
 
 // Stage layout: K tile | V tile | q row | chunk-first partial rows.
@@ -174,6 +175,7 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
         const int4 rec = *reinterpret_cast<const int4*>(t.sf_item + (size_t)item * kSfItemInts);
         nsegs = rec.y;
         seg = rec.x + ((int)blockIdx.x - rec.z);
+        if ((int)blockIdx.x - rec.z == nsegs - 1) flags |= F_FINISH;
       }
       if (last && full) {
 #pragma unroll
@@ -267,7 +269,8 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
 // n-ary Eqn 2: rebase to the common max, sum in the fixed list order.
 template <typename TO, int D, int NG>
 CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* pst, const float* __restrict__ pO,
-                        float* __restrict__ segO, int32_t* __restrict__ counters, TO* __restrict__ out,
+                        float* __restrict__ segO, uint32_t* __restrict__ segflags, uint32_t tag,
+                        TO* __restrict__ out,
                         const DevTables& t, int h, int ct) {
   constexpr int PR = D + 4;
   const int head = md.item % h;
@@ -320,17 +323,43 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
       srow[D + 1] = an;
     }
   }
+  named_sync_consumers();
+  if (ct == 0) {
+    __threadfence();  // the segment row is visible GPU-wide before its flag
+    *reinterpret_cast<volatile uint32_t*>(segflags + md.seg) = tag;
+    // The CTA holding the item's last segment meets it first in its range (the
+    // item continues from the previous CTA): it finishes the item after its
+    // own units, so the ring never stalls on the other segments.
+    if (md.flags & F_FINISH) {
+      S.fix = md;
+      S.fix_pending = 1;
+    }
+  }
+}
+
+// Deferred finish of the split item whose last segment this CTA holds: wait for
+// the other segments' flags (this launch's tag), then merge the chunk-first
+// partials and all segments in CTA order and write O / n.
+template <typename TO, int D, int NG>
+CA_DEV void sf_fixup(SfShared<D, NG>& S, const float* __restrict__ pO, const float* __restrict__ segO,
+                     const uint32_t* __restrict__ segflags, uint32_t tag, TO* __restrict__ out, const DevTables& t,
+                     int h, int ct) {
+  constexpr int PR = D + 4;
+  named_sync_consumers();
+  if (!S.fix_pending) return;
+  const StageMeta md = S.fix;
+  const int base = md.seg - (md.nsegs - 1);
+  const int head = md.item % h;
+  if (ct < md.nsegs - 1) {
+    const volatile uint32_t* f = segflags + base + ct;
+    while (*f != tag) __nanosleep(32);
+  }
   __threadfence();
   named_sync_consumers();
-  if (ct == 0) S.last = (atomicAdd(&counters[md.item], 1) == md.nsegs - 1);
-  named_sync_consumers();
-  if (!S.last) return;
-  __threadfence();
-  const int4 rec = *reinterpret_cast<const int4*>(t.sf_item + (size_t)md.item * kSfItemInts);
   for (int x = ct; x < D; x += kConsumerWarps * 32) {
     float M = -INFINITY;
     for (int e = md.mg0; e < md.mg1; ++e) M = fmaxf(M, __ldcg(pO + ((size_t)t.mg_slot[e] * h + head) * PR + D));
-    for (int sg = 0; sg < md.nsegs; ++sg) M = fmaxf(M, __ldcg(segO + (size_t)(rec.x + sg) * PR + D));
+    for (int sg = 0; sg < md.nsegs; ++sg) M = fmaxf(M, __ldcg(segO + (size_t)(base + sg) * PR + D));
     float ao = 0.f, an = 0.f;
     for (int e = md.mg0; e < md.mg1; ++e) {
       const float* pr = pO + ((size_t)t.mg_slot[e] * h + head) * PR;
@@ -339,14 +368,13 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
       an = fmaf(w, __ldcg(pr + D + 1), an);
     }
     for (int sg = 0; sg < md.nsegs; ++sg) {
-      const float* sr = segO + (size_t)(rec.x + sg) * PR;
+      const float* sr = segO + (size_t)(base + sg) * PR;
       const float w = fast_exp2(__ldcg(sr + D) - M);
       ao = fmaf(w, __ldcg(sr + x), ao);
       an = fmaf(w, __ldcg(sr + D + 1), an);
     }
     Elem<TO>::store1(out + ((size_t)md.caller * h + head) * D + x, ao / an);
   }
-  if (ct == 0) counters[md.item] = 0;  // every segment has arrived: reset for the next launch
 }
 
 // MMA: consumers run WarpAttn with the row's query in row 0 of the 16-row
@@ -355,7 +383,8 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
 template <typename T, typename TO, int D, bool MMA, int TPW>
 __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     const T* __restrict__ kpool, const T* __restrict__ vpool, const T* __restrict__ q, TO* __restrict__ out,
-    const float* __restrict__ pO, float* __restrict__ segO, int32_t* __restrict__ counters, DevTables t,
+    const float* __restrict__ pO, float* __restrict__ segO, uint32_t* __restrict__ segflags, uint32_t tag,
+    DevTables t,
     int32_t h, int32_t c, float scale_log2, int32_t nst, uint32_t stage_bytes,
     uint64_t* __restrict__ trace, int32_t pf) {
   using G = Geo<T, D>;
@@ -375,6 +404,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) {
       S.pdl_done = 0;
+      S.fix_pending = 0;
       mbar_init(&S.full_bar[s], 1);
       mbar_init(&S.empty_bar[s], kConsumerWarps);
     }
@@ -432,7 +462,8 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
             *reinterpret_cast<float2*>(&S.o[cw][i * 8 + lane * 2]) = make_float2(wa.o[i][0], wa.o[i][1]);
         }
         named_sync_consumers();
-        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, counters, out, t, h, ct);
+        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, segflags, tag, out, t, h,
+                               ct);
         named_sync_consumers();  // S.o / stage reuse
       }
       __syncwarp();
@@ -472,7 +503,8 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
 #pragma unroll
         for (int v = 0; v < G::kVec; ++v) S.o[g][j * G::kVec + v] = o[v];
         named_sync_consumers();
-        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, counters, out, t, h, ct);
+        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, segflags, tag, out, t, h,
+                               ct);
         named_sync_consumers();
       }
       __syncwarp();
@@ -481,6 +513,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     }
   }
   (void)cw;
+  sf_fixup<TO, D, NG>(S, pO, segO, segflags, tag, out, t, h, ct);
   if (tr && ct == 0) tr[2] = globaltimer_ns();
 }
 
@@ -584,7 +617,8 @@ cudaError_t launch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) 
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;
   return launch_ex(kern, dim3(t.n_sf_ctas), dim3(kSfThreads), smem, st, a.use_pdl, kp, vp, (const T*)a.q,
-                   (TO*)a.out, (const float*)a.pO, a.segO, a.counters, t, (int32_t)p.h, (int32_t)p.c, a.scale_log2,
+                   (TO*)a.out, (const float*)a.pO, a.segO, a.segflags, a.tag, t, (int32_t)p.h, (int32_t)p.c,
+                   a.scale_log2,
                    (int32_t)nst, (uint32_t)stage, a.trace_cf ? (uint64_t*)nullptr : a.trace,
                    (int32_t)std::min(a.sf_prefetch, 31));
 }
