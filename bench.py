@@ -315,6 +315,9 @@ def run_ours(args):
     stream = torch.cuda.Stream(dev)
     wl = DecodeWorkload(dev, seed=rank, steps=max(K, W), mode=args.mode, question=args.question,
                         n_shared=args.n_shared, b=args.batch)
+    for o in args.opt:
+        key, val = o.split("=")
+        wl.ca.set_option(key, int(val))
     # warm-up on the same cache, then drain and refill: timed steps are tokens 1..K
     wl.fill()
     time_steps(wl, W, flush_buf, stream)
@@ -423,6 +426,7 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--cpu-budget", dest="cpu_budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
+    ap.add_argument("--opt", action="append", default=[], help="library option key=value (A/B experiments)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -100,6 +100,7 @@ struct chunkattn {
   bool tma_ok = false;
   bool cf_simt = false;
   bool sf_simt = false;
+  bool cf_small = true;
   int trace_kernel = 0;    // 1: trace seq-first, 2: trace chunk-first
   int sf_ctas_per_sm = 2;  // persistent seq-first residency (smem budget per CTA)
   uint32_t launch_tag = 0;
@@ -522,6 +523,7 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   a.scale_log2 = h->scale() * 1.4426950408889634f;
   a.cf_tensor_cores = h->tma_ok && !h->cf_simt;
   a.sf_tensor_cores = !h->sf_simt;
+  a.cf_small = h->cf_small;
   a.trace = h->trace_kernel ? reinterpret_cast<uint64_t*>(h->wsp + h->ws.trace) : nullptr;
   a.trace_cf = h->trace_kernel == 2;
   a.sf_ctas_per_sm = h->sf_ctas_per_sm;
@@ -604,6 +606,8 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->cf_simt = value != 0;
   } else if (k == "sf_simt") {
     h->sf_simt = value != 0;
+  } else if (k == "cf_small") {
+    h->cf_small = value != 0;
   } else if (k == "sf_prefetch") {
     h->sf_prefetch = value < 0 ? 0 : (int)std::min<int64_t>(value, 31);
     return CA_OK;

@@ -27,19 +27,21 @@ cudaError_t launch_chunk_first_simt(const AttnLaunch& a, const DevTables& t, cud
 
 namespace {
 
-constexpr int kWarps = 8;                // consumer warps: G row groups x L chunk lanes
-constexpr int kThreads = (kWarps + 1) * 32;  // + 1 producer warp
 constexpr int kMaxStages = 8;
 
+// kWarps consumer warps = G row groups x L chunk lanes, + 1 producer warp.
 // Warp (g, l) owns query rows [16 g, 16 g + 16) of the tile and the chunks
-// k = l, l + L, ... -- whole chunks, TPW = min(c, 64) tokens per MMA pass --
-// so L chunks are attended concurrently with no CTA-wide sync per chunk.  The
-// producer warp refills a stage as soon as its G consumers release it.
-template <typename T, int D, int TPW>
-__global__ void __launch_bounds__(kThreads, 1)
+// k = l, l + L, ... -- whole chunks, TPW tokens per MMA pass -- so L chunks
+// are attended concurrently with no CTA-wide sync per chunk.  The producer
+// warp refills a stage as soon as its G consumers release it.  kWarps = 4 (for
+// tiles of <= 64 rows) keeps the CTA small enough for a seq-first CTA to run
+// beside it on the same SM (PDL overlap of the two phases).
+template <typename T, int D, int TPW, int kWarps>
+__global__ void __launch_bounds__((kWarps + 1) * 32, 1)
     cf_mma_kernel(const T* __restrict__ kpool, const T* __restrict__ vpool, const T* __restrict__ q,
                   float* __restrict__ pO, DevTables t, int32_t h, int32_t C, int32_t L, float scale_log2,
                   int32_t nst, uint64_t* __restrict__ trace) {
+  constexpr int kThreads = (kWarps + 1) * 32;
   using WA = WarpAttn<T, D, TPW>;
   constexpr int PR = D + 4;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -180,41 +182,41 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_wait();
 }
 
-template <typename T, int D, int TPW>
-cudaError_t launch_mma(const AttnLaunch& a, const DevTables& t, int L, cudaStream_t st) {
+template <typename T, int D, int TPW, int W>
+cudaError_t launch_mma(const AttnLaunch& a, const DevTables& t, int L, size_t budget, cudaStream_t st) {
   const PoolGeom& p = a.pool;
   const size_t stage = (size_t)2 * p.c * D * 2;
-  int nst = (int)std::min<size_t>(kMaxStages, (size_t)(200 * 1024) / stage);
-  nst = std::max(1, nst);
-  const size_t epi = (size_t)kWarps * 16 * D * 4;
+  int nst = (int)std::min<size_t>(kMaxStages, budget / stage);
+  nst = std::max(2, nst);
+  const size_t epi = (size_t)W * 16 * D * 4;
   const size_t smem = std::max(nst * stage, epi);
-  auto kern = cf_mma_kernel<T, D, TPW>;
+  auto kern = cf_mma_kernel<T, D, TPW, W>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;
-  return launch_ex(kern, dim3(t.n_cf_tiles, p.h), dim3(kThreads), smem, st, a.use_pdl, kp, vp, (const T*)a.q, a.pO,
-                   t, (int32_t)p.h, (int32_t)p.c, (int32_t)L, a.scale_log2, (int32_t)nst,
+  return launch_ex(kern, dim3(t.n_cf_tiles, p.h), dim3((W + 1) * 32), smem, st, a.use_pdl, kp, vp, (const T*)a.q,
+                   a.pO, t, (int32_t)p.h, (int32_t)p.c, (int32_t)L, a.scale_log2, (int32_t)nst,
                    a.trace_cf ? a.trace : (uint64_t*)nullptr);
 }
 
-template <typename T>
-cudaError_t dispatch_mma(const AttnLaunch& a, const DevTables& t, int tpw, int L, cudaStream_t st) {
+template <typename T, int W>
+cudaError_t dispatch_mma(const AttnLaunch& a, const DevTables& t, int tpw, int L, size_t budget, cudaStream_t st) {
   const int d = a.pool.d;
 #define CA_CASE(DD, TT) \
-  if (d == DD && tpw == TT) return launch_mma<T, DD, TT>(a, t, L, st);
+  if (d == DD && tpw == TT) return launch_mma<T, DD, TT, W>(a, t, L, budget, st);
   CA_CASE(64, 16) CA_CASE(64, 32) CA_CASE(64, 64) CA_CASE(128, 16) CA_CASE(128, 32) CA_CASE(128, 64)
 #undef CA_CASE
   return cudaErrorInvalidValue;
 }
 
-// chunk lanes L (= warps per row group; G = 8 / L row groups of 16 rows) and
+// chunk lanes L (= warps per row group; G = W / L row groups of 16 rows) and
 // tokens per MMA pass TPW (a warp walks its whole chunk in TPW-token passes)
-bool pick_slices(int c, int max_rows, int* L, int* tpw) {
+bool pick_slices(int c, int max_rows, int warps, int* L, int* tpw) {
   int groups = 1;
   while (groups * 16 < max_rows) groups *= 2;
-  if (groups > kWarps) return false;
-  *L = kWarps / groups;
+  if (groups > warps) return false;
+  *L = warps / groups;
   *tpw = c % 64 == 0 ? 64 : (c % 32 == 0 ? 32 : 16);
   return true;
 }
@@ -229,11 +231,20 @@ bool cf_mma_supported(const PoolGeom& p) {
 cudaError_t launch_chunk_first(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   if (t.n_cf_tiles == 0) return cudaSuccess;
   int L = 1, tpw = 16;
-  if (!a.cf_tensor_cores || !cf_mma_supported(a.pool) || !pick_slices(a.pool.c, t.max_tile_rows, &L, &tpw))
+  // small CTA (4 consumer warps, ~100 KB ring) when the tiles allow it, so a
+  // seq-first CTA fits beside it; 8 warps for tiles of up to 128 rows
+  const bool small = a.cf_small && t.max_tile_rows <= 64;
+  const int warps = small ? 4 : 8;
+  if (!a.cf_tensor_cores || !cf_mma_supported(a.pool) || !pick_slices(a.pool.c, t.max_tile_rows, warps, &L, &tpw))
     return launch_chunk_first_simt(a, t, st);
   if (a.pool.d == 128 && tpw == 64) tpw = 32;  // keeps the d = 128 warp state under the register cap
-  if (a.pool.dtype == DT_F16) return dispatch_mma<__half>(a, t, tpw, L, st);
-  return dispatch_mma<__nv_bfloat16>(a, t, tpw, L, st);
+  const size_t budget = small ? (size_t)100 * 1024 : (size_t)200 * 1024;
+  if (small) {
+    if (a.pool.dtype == DT_F16) return dispatch_mma<__half, 4>(a, t, tpw, L, budget, st);
+    return dispatch_mma<__nv_bfloat16, 4>(a, t, tpw, L, budget, st);
+  }
+  if (a.pool.dtype == DT_F16) return dispatch_mma<__half, 8>(a, t, tpw, L, budget, st);
+  return dispatch_mma<__nv_bfloat16, 8>(a, t, tpw, L, budget, st);
 }
 
 }  // namespace pakv

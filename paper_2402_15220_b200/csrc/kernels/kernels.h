@@ -68,6 +68,7 @@ struct AttnLaunch {
   int sf_ctas_per_sm;    // 1 or 2: shared-memory budget of the seq-first CTA
   int sf_prefetch;       // seq-first L2 prefetch distance in units (0 = off)
   bool cf_tensor_cores;  // use the mma chunk-first kernel
+  bool cf_small;         // 4-warp chunk-first CTA (co-resident with seq-first) when tiles allow
   bool sf_tensor_cores;  // use the mma consumers in the seq-first kernel (16-bit types)
   bool use_pdl;
 };
