@@ -192,6 +192,9 @@ cudaError_t launch_mma(const AttnLaunch& a, const DevTables& t, int L, size_t bu
   const size_t smem = std::max(nst * stage, epi);
   auto kern = cf_mma_kernel<T, D, TPW, W>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // max shared-memory carveout: a seq-first CTA must fit beside this one (PDL overlap)
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;

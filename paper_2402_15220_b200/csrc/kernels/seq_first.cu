@@ -599,7 +599,10 @@ __global__ void __launch_bounds__(128) cf_simt_kernel(const T* __restrict__ kpoo
 }
 
 cudaError_t set_smem(const void* kern, size_t smem) {
-  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  return e;
 }
 
 template <typename T, typename TO, int D, bool MMA, int TPW>
