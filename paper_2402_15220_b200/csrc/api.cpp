@@ -78,6 +78,8 @@ WsLayout ws_layout(const chunkattn_config* c) {
   w.segMN = o;
   w.counters = o;  // release flags of segment partials [2 * kMaxSfCtas] u32 (zeroed; tag-compared)
   o = align_up(o + (size_t)4 * 2 * kMaxSfCtas, 256);
+  w.pMN = o;  // fused chunk-first readiness flags [tiles <= slot_cap][h] u32 (zeroed; tag-compared)
+  o = align_up(o + (size_t)4 * w.slot_cap * c->num_heads, 256);
   w.trace = o;  // debug timeline (option "trace"): the last kTraceCtas*kTraceStride u64 words
   o = align_up(o + (size_t)8 * kTraceCtas * kTraceStride, 256);
   w.total = o;
@@ -101,6 +103,7 @@ struct chunkattn {
   bool cf_simt = false;
   bool sf_simt = false;
   bool cf_small = true;
+  bool fused_opt = true;  // run chunk-first inside the persistent seq-first kernel when possible
   int trace_kernel = 0;    // 1: trace seq-first, 2: trace chunk-first
   int sf_ctas_per_sm = 2;  // persistent seq-first residency (smem budget per CTA)
   uint32_t launch_tag = 0;
@@ -226,6 +229,8 @@ struct chunkattn {
   chunkattn_status ensure_context(cudaStream_t st) {
     if (ctx.epoch == tree.epoch()) return CA_OK;
     sopt.cf_chunks_per_tile = cf_cpt_forced;
+    // fused kernel: tensor-core consumers in both phases (16-bit K/V, c % 16 == 0)
+    sopt.fused = fused_opt && !cf_simt && !sf_simt && cfg.dtype != CA_F32 && cfg.chunk_size % 16 == 0;
     Context nc;
     std::string err;
     if (!build_context(tree, sopt, &nc, &err)) return fail(CA_ENOMEM, err);
@@ -260,6 +265,10 @@ struct chunkattn {
     t.sf_cta = base + L.sf_cta;
     t.sf_item = base + L.sf_item;
     t.sf_unit = base + L.sf_unit;
+    t.mg_tile = base + L.mg_tile;
+    t.cf_unit = base + L.cf_unit;
+    t.n_cf_units = ctx.n_cf_units;
+    t.fused = ctx.fused ? 1 : 0;
     t.n_sf_ctas = ctx.n_sf_ctas;
     return t;
   }
@@ -520,6 +529,7 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   a.segflags = reinterpret_cast<uint32_t*>(h->wsp + h->ws.counters);
   if (++h->launch_tag == 0) ++h->launch_tag;  // flags compare against a nonzero per-launch tag
   a.tag = h->launch_tag;
+  a.cf_flags = reinterpret_cast<uint32_t*>(h->wsp + h->ws.pMN);
   a.scale_log2 = h->scale() * 1.4426950408889634f;
   a.cf_tensor_cores = h->tma_ok && !h->cf_simt;
   a.sf_tensor_cores = !h->sf_simt;
@@ -531,7 +541,7 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   a.use_pdl = h->use_pdl && !h->kernel_events;
   const DevTables t = h->dev_tables();
   cudaError_t e = cudaSuccess;
-  if (t.n_cf_tiles > 0) {
+  if (t.n_cf_tiles > 0 && !t.fused) {
     e = h->timed_launch(chunkattn::K_CF, st, [&] { return launch_chunk_first(a, t, st); });
     if (e != cudaSuccess) return h->cuda_fail(e, "chunk_first");
     ++h->n_launches;
@@ -606,6 +616,10 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->cf_simt = value != 0;
   } else if (k == "sf_simt") {
     h->sf_simt = value != 0;
+  } else if (k == "fused") {
+    h->fused_opt = value != 0;
+  } else if (k == "cf_unit_cost") {
+    h->sopt.cf_unit_cost = value < 1 ? 0.1 : (double)value / 10.0;  // tenths of a seq-first unit
   } else if (k == "cf_small") {
     h->cf_small = value != 0;
   } else if (k == "sf_prefetch") {

@@ -2,6 +2,7 @@
 #include "schedule.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 
 namespace pakv {
@@ -18,18 +19,26 @@ struct RunTiling {
   int64_t splits, row_tiles, rows_per_tile;
 };
 
-RunTiling tile_run(const Run& r, int64_t cpt) {
+RunTiling tile_run(const Run& r, int64_t cpt, int64_t max_rows) {
   const int64_t rows = r.j - r.i + 1;
   const int64_t n = (int64_t)r.chunks.size();
   RunTiling t;
   t.splits = (n + cpt - 1) / cpt;
-  t.row_tiles = (rows + kMaxCfTileRows - 1) / kMaxCfTileRows;
+  t.row_tiles = (rows + max_rows - 1) / max_rows;
   // balanced row tiles, multiples of 16 rows (one MMA row group) where possible
   int64_t per = (rows + t.row_tiles - 1) / t.row_tiles;
-  per = std::min<int64_t>(kMaxCfTileRows, (per + 15) / 16 * 16);
+  per = std::min<int64_t>(max_rows, (per + 15) / 16 * 16);
   t.rows_per_tile = per;
   t.row_tiles = (rows + per - 1) / per;
   return t;
+}
+
+// Fused kernel: 4 consumer warps = G row groups (16 rows each, G a power of
+// two) x L token lanes; each lane writes its own partial row.
+int32_t fused_lanes(int64_t rows) {
+  int32_t g = 1;
+  while (g * 16 < rows) g *= 2;
+  return 4 / g;
 }
 
 }  // namespace
@@ -85,13 +94,15 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   // ---- split rule: chunks per tile so that heads * tiles >= target CTAs
   int64_t max_n = 1;
   for (const Run& r : runs) max_n = std::max<int64_t>(max_n, (int64_t)r.chunks.size());
+  const int64_t tile_rows = opt.fused ? kFusedTileRows : kMaxCfTileRows;
+  auto lanes_of = [&](const RunTiling& t) { return opt.fused ? fused_lanes(t.rows_per_tile) : 1; };
   auto count = [&](int64_t cpt, int64_t* tiles, int64_t* slots) {
     *tiles = 0;
     *slots = 0;
     for (const Run& r : runs) {
-      RunTiling t = tile_run(r, cpt);
+      RunTiling t = tile_run(r, cpt, tile_rows);
       *tiles += t.splits * t.row_tiles;
-      *slots += t.splits * (r.j - r.i + 1);
+      *slots += t.splits * (r.j - r.i + 1) * lanes_of(t);
     }
   };
   int64_t cpt = max_n, tiles = 0, slots = 0;
@@ -128,18 +139,19 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   std::vector<int32_t> cf_chunk, cf_tile;
   std::vector<int32_t> mg_cnt(b + 1, 0);
   for (const Run& r : runs) {
-    RunTiling t = tile_run(r, cpt);
-    for (int32_t row = r.i; row <= r.j; ++row) mg_cnt[row + 1] += (int32_t)t.splits;
+    RunTiling t = tile_run(r, cpt, tile_rows);
+    for (int32_t row = r.i; row <= r.j; ++row) mg_cnt[row + 1] += (int32_t)(t.splits * lanes_of(t));
   }
   std::vector<int32_t> mg_ptr(b + 1, 0);
   for (int32_t r = 0; r < b; ++r) mg_ptr[r + 1] = mg_ptr[r] + mg_cnt[r + 1];
-  std::vector<int32_t> mg_slot(mg_ptr[b]);
+  std::vector<int32_t> mg_slot(mg_ptr[b]), mg_tile(mg_ptr[b]);
   std::vector<int32_t> mg_fill(mg_ptr.begin(), mg_ptr.end() - 1);
   int64_t slot = 0;
   int32_t max_rows = 0;
   for (size_t ri = 0; ri < runs.size(); ++ri) {
     const Run& r = runs[ri];
-    RunTiling t = tile_run(r, cpt);
+    RunTiling t = tile_run(r, cpt, tile_rows);
+    const int32_t L = lanes_of(t);
     const int64_t n = (int64_t)r.chunks.size();
     for (int64_t s = 0; s < t.splits; ++s) {
       const int64_t k0 = s * n / t.splits, k1 = (s + 1) * n / t.splits;  // balanced split
@@ -148,9 +160,14 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
       for (int64_t rt = 0; rt < t.row_tiles; ++rt) {
         const int32_t r0 = r.i + (int32_t)(rt * t.rows_per_tile);
         const int32_t r1 = std::min<int32_t>(r.j + 1, r0 + (int32_t)t.rows_per_tile);
-        cf_tile.insert(cf_tile.end(), {off, (int32_t)(k1 - k0), r0, r1, (int32_t)slot, (int32_t)ri, 0, 0});
-        for (int32_t row = r0; row < r1; ++row) mg_slot[mg_fill[row]++] = (int32_t)(slot + (row - r0));
-        slot += r1 - r0;
+        const int32_t tile_id = (int32_t)(cf_tile.size() / kCfTileInts);
+        cf_tile.insert(cf_tile.end(), {off, (int32_t)(k1 - k0), r0, r1, (int32_t)slot, (int32_t)ri, L, 0});
+        for (int32_t row = r0; row < r1; ++row)
+          for (int32_t l = 0; l < L; ++l) {  // lane partials in lane order (fixed merge order, A12)
+            mg_tile[mg_fill[row]] = tile_id;
+            mg_slot[mg_fill[row]++] = (int32_t)(slot + (int64_t)l * (r1 - r0) + (row - r0));
+          }
+        slot += (int64_t)(r1 - r0) * L;
         max_rows = std::max(max_rows, r1 - r0);
       }
     }
@@ -185,11 +202,59 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
       }
     }
   }
+  // Fused: chunk-first jobs (tile, head) go first, by longest-processing-time
+  // greedy to the least-loaded CTA; the seq-first units then fill every CTA up
+  // to the common target (contiguous ranges, proportional to the room left).
+  std::vector<int64_t> ubound(G + 1, 0);
+  std::vector<int32_t> cf_unit;
+  std::vector<int32_t> cf_range(2 * G, 0);
+  if (opt.fused && G > 0 && X.n_cf_tiles > 0) {
+    const int64_t n_tiles = X.n_cf_tiles;
+    std::vector<std::pair<int64_t, int64_t>> jobs;  // (-chunks, job) -> sorted: big first, then index
+    for (int64_t tl = 0; tl < n_tiles; ++tl)
+      for (int32_t hh = 0; hh < H; ++hh) jobs.push_back({-(int64_t)cf_tile[kCfTileInts * tl + CF_NCHUNK], tl * H + hh});
+    std::sort(jobs.begin(), jobs.end());
+    std::vector<double> load(G, 0.0);
+    std::vector<std::vector<int64_t>> mine(G);
+    for (const auto& jb : jobs) {
+      int64_t best = 0;
+      for (int64_t g = 1; g < G; ++g)
+        if (load[g] < load[best]) best = g;
+      load[best] += (double)(-jb.first) * opt.cf_unit_cost;
+      mine[best].push_back(jb.second);
+    }
+    double total = (double)U;
+    for (double l : load) total += l;
+    const double target = total / (double)G;
+    std::vector<double> room(G);
+    double room_sum = 0;
+    for (int64_t g = 0; g < G; ++g) room_sum += (room[g] = std::max(0.0, target - load[g]));
+    double acc = 0;
+    for (int64_t g = 0; g < G; ++g) {
+      ubound[g] = room_sum > 0 ? (int64_t)std::llround((double)U * acc / room_sum) : U * g / G;
+      acc += room[g];
+      cf_range[2 * g] = (int32_t)(cf_unit.size() / kCfUnitInts);
+      for (int64_t job : mine[g]) {
+        const int64_t tl = job / H;
+        const int32_t nk = cf_tile[kCfTileInts * tl + CF_NCHUNK];
+        for (int32_t k = 0; k < nk; ++k)
+          cf_unit.insert(cf_unit.end(), {(int32_t)tl, (int32_t)(job % H), k, (k == 0 ? 1 : 0) | (k == nk - 1 ? 2 : 0)});
+      }
+      cf_range[2 * g + 1] = (int32_t)(cf_unit.size() / kCfUnitInts);
+    }
+    ubound[G] = U;
+  } else {
+    for (int64_t g = 0; g <= G; ++g) ubound[g] = G > 0 ? U * g / G : 0;
+  }
+  X.n_cf_units = (int32_t)(cf_unit.size() / kCfUnitInts);
+  X.fused = opt.fused && X.n_cf_tiles > 0;
   int32_t seg_slots = 0;
   for (int64_t g = 0; g < G; ++g) {
-    const int64_t u0 = U * g / G, u1 = U * (g + 1) / G;
+    const int64_t u0 = ubound[g], u1 = ubound[g + 1];
     sf_cta[kSfCtaInts * g + 0] = (int32_t)u0;
     sf_cta[kSfCtaInts * g + 1] = (int32_t)u1;
+    sf_cta[kSfCtaInts * g + 2] = cf_range[2 * g];
+    sf_cta[kSfCtaInts * g + 3] = cf_range[2 * g + 1];
     // one segment for every item this CTA touches
     int64_t u = u0;
     while (u < u1) {
@@ -232,6 +297,8 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   L.sf_cta = place((int64_t)sf_cta.size());
   L.sf_item = place((int64_t)sf_item.size());
   L.sf_unit = place((int64_t)sf_unit.size());
+  L.mg_tile = place((int64_t)mg_tile.size());
+  L.cf_unit = place((int64_t)cf_unit.size());
   L.total = o;
   if (o > opt.table_capacity) {
     *err = "context tables exceed workspace capacity";
@@ -254,6 +321,8 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   put(L.sf_cta, sf_cta);
   put(L.sf_item, sf_item);
   put(L.sf_unit, sf_unit);
+  put(L.mg_tile, mg_tile);
+  put(L.cf_unit, cf_unit);
   X.epoch = tree.epoch();
   return true;
 }

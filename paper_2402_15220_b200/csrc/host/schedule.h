@@ -16,9 +16,15 @@
 namespace pakv {
 
 // Chunk-first tile record in the blob (kCfTileInts int32 each).
-enum CfTileField { CF_CHUNK_OFF = 0, CF_NCHUNK, CF_ROW0, CF_ROW1, CF_SLOT, CF_RUN, CF_PAD0, CF_PAD1 };
+// CF_LANES: number of token-lane partials per row (1 when the chunk-first CTA
+// merges its lanes itself; L = 4 / row groups in the fused kernel, which writes
+// one partial per lane: slot = CF_SLOT + lane * rows + (row - CF_ROW0)).
+enum CfTileField { CF_CHUNK_OFF = 0, CF_NCHUNK, CF_ROW0, CF_ROW1, CF_SLOT, CF_RUN, CF_LANES, CF_PAD1 };
 constexpr int kCfTileInts = 8;
 constexpr int kMaxCfTileRows = 128;  // rows of one chunk-first tile (8 warps x 16 rows)
+constexpr int kFusedTileRows = 64;   // fused kernel: 4 consumer warps x 16 rows
+// Fused-kernel chunk-first unit (kCfUnitInts int32): {tile, head, k, flags}
+constexpr int kCfUnitInts = 4;
 
 // Seq-first CTA record (kSfCtaInts int32 each): a contiguous range of
 // (row, head, chunk) units [u0, u1) starting inside item `item0` at unit `off0`.
@@ -37,6 +43,8 @@ struct ScheduleOptions {
   int64_t cf_chunks_per_tile = 0;  // 0 = auto
   int64_t cf_target_ctas = 296;    // auto rule: heads * tiles >= this
   int64_t sf_ctas = 296;           // persistent seq-first grid (<= kMaxSfCtas)
+  bool fused = false;              // chunk-first units run inside the persistent seq-first kernel
+  double cf_unit_cost = 2.0;       // fused balance: cost of a chunk-first unit in seq-first units
   int64_t slot_capacity = 0;       // partial slots available in the workspace
   int64_t table_capacity = 0;      // int32 entries available for the blob
 };
@@ -44,7 +52,8 @@ struct ScheduleOptions {
 // Offsets (int32 units) of the arrays inside the blob.
 struct BlobLayout {
   int64_t seq_len = 0, sf_first = 0, last_chunk = 0, last_start = 0, sf_ptr = 0, mg_ptr = 0,
-          sf_chunk = 0, mg_slot = 0, cf_chunk = 0, cf_tile = 0, sf_cta = 0, sf_item = 0, sf_unit = 0, total = 0;
+          sf_chunk = 0, mg_slot = 0, cf_chunk = 0, cf_tile = 0, sf_cta = 0, sf_item = 0, sf_unit = 0, mg_tile = 0,
+          cf_unit = 0, total = 0;
 };
 
 struct Context {
@@ -62,6 +71,8 @@ struct Context {
   int64_t cf_chunks_per_tile = 0;
   int32_t n_sf_ctas = 0;
   int32_t n_seg_slots = 0;  // segment partials of items split across CTAs
+  int32_t n_cf_units = 0;   // fused: chunk-first units (all CTAs)
+  bool fused = false;
 };
 
 // Build the context of the current tree.  Returns false (and sets *err) when

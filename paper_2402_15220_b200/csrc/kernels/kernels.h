@@ -27,6 +27,10 @@ struct DevTables {
   const int32_t* sf_cta;      // [n_sf_ctas][4] persistent seq-first ranges
   const int32_t* sf_item;     // [b*h][4] split-item records
   const int32_t* sf_unit;     // [units][4] unit descriptors
+  const int32_t* mg_tile;     // chunk-first tile owning each merge-list slot (fused readiness flags)
+  const int32_t* cf_unit;     // fused: [units][4] {tile, head, k, flags}
+  int32_t n_cf_units;
+  int32_t fused;              // chunk-first runs inside the persistent seq-first kernel
   int32_t b, n_cf_tiles, max_tile_rows, n_sf_ctas;
 };
 
@@ -62,6 +66,7 @@ struct AttnLaunch {
   int32_t* counters;  // unused
   uint32_t* segflags;  // [seg slots] release flags of segment partials (== tag when written)
   uint32_t tag;        // this launch's flag value (nonzero, increments per attend)
+  uint32_t* cf_flags;  // fused: [tile * h + head] partial-ready flags (== tag when written)
   float scale_log2;
   uint64_t* trace;       // optional per-CTA timeline ([cta][kTraceWords] globaltimer ns), or null
   bool trace_cf;         // trace the chunk-first kernel instead of seq-first

@@ -106,7 +106,7 @@ constexpr int kConsumerWarps = 4;
 constexpr int kSfThreads = (kProducerWarps + kConsumerWarps) * 32;
 constexpr int kMaxPrefetchSlots = 4;  // chunk-first partial rows staged per item
 
-enum : int { F_FIRST = 1, F_LAST = 2, F_FULL = 4, F_FINISH = 8 };
+enum : int { F_FIRST = 1, F_LAST = 2, F_FULL = 4, F_FINISH = 8, F_CF = 16 };
 
 struct StageMeta {
   int item, nt, flags, caller;
@@ -145,11 +145,46 @@ template <typename T, int D, int NG>
 CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __restrict__ kpool,
                        const T* __restrict__ vpool, const T* __restrict__ q, const float* __restrict__ pO,
                        const DevTables& t, int h, int c, int nst, uint32_t stage_bytes, int u0, int u1, int lane,
-                       uint64_t* __restrict__ tr, int pf) {
+                       uint64_t* __restrict__ tr, int pf, int cf0, int cf1) {
   constexpr int PR = D + 4;
   const size_t tile_bytes = (size_t)c * D * sizeof(T);
   int jj = 0;
   bool waited = false;  // PDL: append (new token, seq_len) and chunk-first (partials) complete
+  // Fused chunk-first units first (shared chunks: untouched by this step's
+  // append, so no PDL wait): full K and V tiles of (chunk, head).
+  for (int base = cf0; base < cf1; base += 32) {
+    const int u = base + lane;
+    int tile = 0, head = 0, k = 0, uf = 0, chunk = 0;
+    if (u < cf1) {
+      const int4 d = *reinterpret_cast<const int4*>(t.cf_unit + (size_t)u * kCfUnitInts);
+      tile = d.x;
+      head = d.y;
+      k = d.z;
+      uf = d.w;
+      chunk = t.cf_chunk[t.cf_tile[tile * kCfTileInts + CF_CHUNK_OFF] + k];
+    }
+    const int cnt = min(32, cf1 - base);
+    for (int i = 0; i < cnt; ++i) {
+      const int i_tile = __shfl_sync(0xffffffffu, tile, i);
+      const int i_head = __shfl_sync(0xffffffffu, head, i);
+      const int i_k = __shfl_sync(0xffffffffu, k, i);
+      const int i_uf = __shfl_sync(0xffffffffu, uf, i);
+      const int i_chunk = __shfl_sync(0xffffffffu, chunk, i);
+      const int s = jj % nst;
+      if (jj >= nst) mbar_wait(&S.empty_bar[s], (uint32_t)(((jj / nst) - 1) & 1));
+      if (lane == 0) {
+        const int fl = F_CF | ((i_uf & 1) ? F_FIRST : 0) | ((i_uf & 2) ? F_LAST : 0);
+        S.meta[s] = StageMeta{i_tile, c, fl, i_head, 0, 0, i_k, 0};
+        unsigned char* st = smem_raw + (size_t)s * stage_bytes;
+        const size_t off = ((size_t)i_chunk * h + i_head) * c * D;
+        mbar_arrive_expect_tx(&S.full_bar[s], 2 * (uint32_t)tile_bytes);
+        bulk_g2s(st, kpool + off, (uint32_t)tile_bytes, &S.full_bar[s]);
+        bulk_g2s(st + tile_bytes, vpool + off, (uint32_t)tile_bytes, &S.full_bar[s]);
+      }
+      __syncwarp();
+      ++jj;
+    }
+  }
   for (int base = u0; base < u1; base += 32) {
     const int u = base + lane;
     int chunk = -1, item = 0, k = 0, per = 1, nt = 0, caller = 0, mg0 = 0, mg1 = 0, seg = -1, nsegs = 1;
@@ -231,7 +266,8 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
       const int head = i_item % h;
       const bool want_q = (i_flags & F_FIRST) && i_chunk >= 0;
       const bool want_p = (i_flags & F_LAST) && (i_flags & F_FULL);
-      const int np = want_p ? min(i_mg1 - i_mg0, kMaxPrefetchSlots) : 0;
+      // fused: the partials are produced inside this kernel -> read at finalize, not staged
+      const int np = (want_p && !t.fused) ? min(i_mg1 - i_mg0, kMaxPrefetchSlots) : 0;
       if (jj >= nst) mbar_wait(&S.empty_bar[s], (uint32_t)(((jj / nst) - 1) & 1));
       unsigned char* st = smem_raw + (size_t)s * stage_bytes;
       const uint32_t kv_bytes = (uint32_t)(i_nt * D * (int)sizeof(T));
@@ -267,10 +303,24 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
 // global) with the states and writes O / n; a segment of a split item writes
 // its partial and the last-arriving segment merges all of them in CTA order.
 // n-ary Eqn 2: rebase to the common max, sum in the fixed list order.
+// Fused kernel: the chunk-first partials of (row, head) come from other CTAs
+// of this launch -- wait for their tiles' readiness flags (this launch's tag).
+// Deadlock-free: every CTA runs all its chunk-first units before any
+// seq-first unit, and chunk-first work never waits.
+CA_DEV void wait_cf_ready(const DevTables& t, const uint32_t* __restrict__ cf_flags, uint32_t tag, int mg0, int mg1,
+                          int head, int h, int ct) {
+  for (int e = mg0 + ct; e < mg1; e += kConsumerWarps * 32) {
+    const volatile uint32_t* f = cf_flags + (size_t)t.mg_tile[e] * h + head;
+    while (*f != tag) __nanosleep(20);
+  }
+  __threadfence();
+  named_sync_consumers();
+}
+
 template <typename TO, int D, int NG>
 CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* pst, const float* __restrict__ pO,
                         float* __restrict__ segO, uint32_t* __restrict__ segflags, uint32_t tag,
-                        TO* __restrict__ out,
+                        const uint32_t* __restrict__ cf_flags, TO* __restrict__ out,
                         const DevTables& t, int h, int ct) {
   constexpr int PR = D + 4;
   const int head = md.item % h;
@@ -280,11 +330,13 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
     if (ct == 0) S.pdl_done = 1;
   }
   if (md.flags & F_FULL) {
-    const int np = min(md.mg1 - md.mg0, kMaxPrefetchSlots);
+    if (t.fused) wait_cf_ready(t, cf_flags, tag, md.mg0, md.mg1, head, h, ct);
+    const int np = t.fused ? 0 : min(md.mg1 - md.mg0, kMaxPrefetchSlots);
     for (int x = ct; x < D; x += kConsumerWarps * 32) {
       float M = -INFINITY;
       for (int e = 0; e < np; ++e) M = fmaxf(M, pst[e * PR + D]);
-      for (int e = md.mg0 + np; e < md.mg1; ++e) M = fmaxf(M, pO[((size_t)t.mg_slot[e] * h + head) * PR + D]);
+      for (int e = md.mg0 + np; e < md.mg1; ++e)
+        M = fmaxf(M, __ldcg(pO + ((size_t)t.mg_slot[e] * h + head) * PR + D));
       for (int gg = 0; gg < NG; ++gg) M = fmaxf(M, S.m[gg]);
       float ao = 0.f, an = 0.f;
       for (int e = 0; e < np; ++e) {
@@ -294,9 +346,9 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
       }
       for (int e = md.mg0 + np; e < md.mg1; ++e) {
         const float* pr = pO + ((size_t)t.mg_slot[e] * h + head) * PR;
-        const float w = fast_exp2(pr[D] - M);
-        ao = fmaf(w, pr[x], ao);
-        an = fmaf(w, pr[D + 1], an);
+        const float w = fast_exp2(__ldcg(pr + D) - M);
+        ao = fmaf(w, __ldcg(pr + x), ao);
+        an = fmaf(w, __ldcg(pr + D + 1), an);
       }
       for (int gg = 0; gg < NG; ++gg) {
         const float w = fast_exp2(S.m[gg] - M);
@@ -342,14 +394,15 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
 // partials and all segments in CTA order and write O / n.
 template <typename TO, int D, int NG>
 CA_DEV void sf_fixup(SfShared<D, NG>& S, const float* __restrict__ pO, const float* __restrict__ segO,
-                     const uint32_t* __restrict__ segflags, uint32_t tag, TO* __restrict__ out, const DevTables& t,
-                     int h, int ct) {
+                     const uint32_t* __restrict__ segflags, uint32_t tag, const uint32_t* __restrict__ cf_flags,
+                     TO* __restrict__ out, const DevTables& t, int h, int ct) {
   constexpr int PR = D + 4;
   named_sync_consumers();
   if (!S.fix_pending) return;
   const StageMeta md = S.fix;
   const int base = md.seg - (md.nsegs - 1);
   const int head = md.item % h;
+  if (t.fused) wait_cf_ready(t, cf_flags, tag, md.mg0, md.mg1, head, h, ct);
   if (ct < md.nsegs - 1) {
     const volatile uint32_t* f = segflags + base + ct;
     while (*f != tag) __nanosleep(32);
@@ -383,10 +436,9 @@ CA_DEV void sf_fixup(SfShared<D, NG>& S, const float* __restrict__ pO, const flo
 template <typename T, typename TO, int D, bool MMA, int TPW>
 __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     const T* __restrict__ kpool, const T* __restrict__ vpool, const T* __restrict__ q, TO* __restrict__ out,
-    const float* __restrict__ pO, float* __restrict__ segO, uint32_t* __restrict__ segflags, uint32_t tag,
-    DevTables t,
-    int32_t h, int32_t c, float scale_log2, int32_t nst, uint32_t stage_bytes,
-    uint64_t* __restrict__ trace, int32_t pf) {
+    float* __restrict__ pO, float* __restrict__ segO, uint32_t* __restrict__ segflags, uint32_t tag,
+    uint32_t* __restrict__ cf_flags, DevTables t, int32_t h, int32_t c, float scale_log2, int32_t nst,
+    uint32_t stage_bytes, uint64_t* __restrict__ trace, int32_t pf) {
   using G = Geo<T, D>;
   constexpr int NG = MMA ? kConsumerWarps : G::kGroups;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -414,7 +466,10 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
   __syncthreads();
 
   if (warp == 0) {
-    sf_produce<T, D, NG>(S, smem_raw, kpool, vpool, q, pO, t, h, c, nst, stage_bytes, u0, u1, lane, tr, pf);
+    const int cf0 = MMA && t.fused ? t.sf_cta[blockIdx.x * kSfCtaInts + 2] : 0;
+    const int cf1 = MMA && t.fused ? t.sf_cta[blockIdx.x * kSfCtaInts + 3] : 0;
+    sf_produce<T, D, NG>(S, smem_raw, kpool, vpool, q, pO, t, h, c, nst, stage_bytes, u0, u1, lane, tr, pf, cf0,
+                         cf1);
     if (tr && lane == 0) tr[1] = globaltimer_ns();
     return;
   }
@@ -424,10 +479,82 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
   int jj = 0;
   if constexpr (MMA) {
     using WA = WarpAttn<T, D, TPW>;
+    constexpr int PR = D + 4;
     const int L = c / TPW;  // token slices per chunk (<= 4)
     uint32_t qa[WA::KS][4];
     WA wa;
     wa.reset();
+    // ---- fused chunk-first units (Alg 1): job = (tile, head); warp (g, l)
+    // owns rows [16 g, 16 g + 16) of the tile and the job's chunks k with
+    // k % L == l; at the job's end every lane writes its own partial rows and
+    // the job's readiness flag is released.
+    {
+      const int cf0 = t.fused ? t.sf_cta[blockIdx.x * kSfCtaInts + 2] : 0;
+      const int cf1 = t.fused ? t.sf_cta[blockIdx.x * kSfCtaInts + 3] : 0;
+      int cfL = 1, cfg = 0, cfl = 0, crow0 = 0, crows = 0, cslot = 0;
+      bool cact = false;
+      for (int u = cf0; u < cf1; ++u, ++jj) {
+        const int s = jj % nst;
+        mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
+        const StageMeta md = S.meta[s];
+        const int tile = md.item, head = md.caller, k = md.seg;
+        if (md.flags & F_FIRST) {
+          const int32_t* rec = t.cf_tile + tile * kCfTileInts;
+          crow0 = rec[CF_ROW0];
+          crows = rec[CF_ROW1] - crow0;
+          cslot = rec[CF_SLOT];
+          cfL = rec[CF_LANES];
+          cfg = cw / cfL;
+          cfl = cw % cfL;
+          cact = cfg * 16 < crows;
+          wa.reset();
+          const int rlo = crow0 + cfg * 16 + (lane >> 2), rhi = rlo + 8;
+          const T* qlo = (cact && rlo < crow0 + crows) ? q + ((size_t)t.row_caller[rlo] * h + head) * D : nullptr;
+          const T* qhi = (cact && rhi < crow0 + crows) ? q + ((size_t)t.row_caller[rhi] * h + head) * D : nullptr;
+          const int cq = (lane & 3) * 2;
+#pragma unroll
+          for (int ks = 0; ks < WA::KS; ++ks) {
+            qa[ks][0] = qlo ? *reinterpret_cast<const uint32_t*>(qlo + ks * 16 + cq) : 0u;
+            qa[ks][1] = qhi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16 + cq) : 0u;
+            qa[ks][2] = qlo ? *reinterpret_cast<const uint32_t*>(qlo + ks * 16 + 8 + cq) : 0u;
+            qa[ks][3] = qhi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16 + 8 + cq) : 0u;
+          }
+        }
+        if (cact && (k % cfL) == cfl) {
+          const uint32_t k_u32 = smem_u32(smem_raw + (size_t)s * stage_bytes);
+          for (int t0 = 0; t0 < c; t0 += TPW)
+            wa.template chunk<false>(qa, k_u32, k_u32 + (uint32_t)tile_bytes, t0, c, scale_log2, lane);
+        }
+        if (md.flags & F_LAST) {
+          wa.finish();
+          if (cact) {
+            const int rl = lane >> 2, cq = (lane & 3) * 2;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              const int rloc = cfg * 16 + rl + 8 * hf;
+              if (rloc < crows) {
+                float* prow = pO + ((size_t)(cslot + cfl * crows + rloc) * h + head) * PR;
+#pragma unroll
+                for (int i = 0; i < WA::DT; ++i)
+                  *reinterpret_cast<float2*>(prow + i * 8 + cq) =
+                      make_float2(wa.o[i][2 * hf], wa.o[i][2 * hf + 1]);
+                if ((lane & 3) == 0)
+                  *reinterpret_cast<float2*>(prow + D) =
+                      hf ? make_float2(wa.m_hi, wa.n_hi) : make_float2(wa.m_lo, wa.n_lo);
+              }
+            }
+          }
+          named_sync_consumers();
+          if (ct == 0) {
+            __threadfence();  // partial rows visible GPU-wide before the flag
+            *reinterpret_cast<volatile uint32_t*>(cf_flags + (size_t)tile * h + head) = tag;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty_bar[s]);
+      }
+      wa.reset();
+    }
     for (int u = u0; u < u1; ++u, ++jj) {
       const int s = jj % nst;
       mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
@@ -462,8 +589,8 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
             *reinterpret_cast<float2*>(&S.o[cw][i * 8 + lane * 2]) = make_float2(wa.o[i][0], wa.o[i][1]);
         }
         named_sync_consumers();
-        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, segflags, tag, out, t, h,
-                               ct);
+        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, segflags, tag, cf_flags, out,
+                               t, h, ct);
         named_sync_consumers();  // S.o / stage reuse
       }
       __syncwarp();
@@ -503,8 +630,8 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
 #pragma unroll
         for (int v = 0; v < G::kVec; ++v) S.o[g][j * G::kVec + v] = o[v];
         named_sync_consumers();
-        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, segflags, tag, out, t, h,
-                               ct);
+        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, segflags, tag, cf_flags, out,
+                               t, h, ct);
         named_sync_consumers();
       }
       __syncwarp();
@@ -513,7 +640,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     }
   }
   (void)cw;
-  sf_fixup<TO, D, NG>(S, pO, segO, segflags, tag, out, t, h, ct);
+  sf_fixup<TO, D, NG>(S, pO, segO, segflags, tag, cf_flags, out, t, h, ct);
   if (tr && ct == 0) tr[2] = globaltimer_ns();
 }
 
@@ -620,7 +747,7 @@ cudaError_t launch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) 
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;
   return launch_ex(kern, dim3(t.n_sf_ctas), dim3(kSfThreads), smem, st, a.use_pdl, kp, vp, (const T*)a.q,
-                   (TO*)a.out, (const float*)a.pO, a.segO, a.segflags, a.tag, t, (int32_t)p.h, (int32_t)p.c,
+                   (TO*)a.out, a.pO, a.segO, a.segflags, a.tag, a.cf_flags, t, (int32_t)p.h, (int32_t)p.c,
                    a.scale_log2,
                    (int32_t)nst, (uint32_t)stage, a.trace_cf ? (uint64_t*)nullptr : a.trace,
                    (int32_t)std::min(a.sf_prefetch, 31));
