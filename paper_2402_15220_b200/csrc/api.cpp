@@ -60,7 +60,9 @@ WsLayout ws_layout(const chunkattn_config* c) {
   w.table_cap = 4 * (B + 4) + 2 * (B + 5) + (sfcap + 4) + (w.slot_cap + 4) + (c->max_chunks + 4) +
                 kCfTileInts * (w.slot_cap + 1) + kSfCtaInts * kMaxSfCtas + 4 +
                 (int64_t)kSfItemInts * B * c->num_heads + 4 +
-                (int64_t)kSfUnitInts * c->num_heads * B * (msc + 1) + 4;
+                (int64_t)kSfUnitInts * c->num_heads * B * (msc + 1) + 4 +
+                (w.slot_cap + 4) +                                      // mg_tile
+                (int64_t)kCfUnitInts * c->num_heads * w.slot_cap + 4;  // fused chunk-first units
   size_t o = 0;
   w.attend_perm = o;
   o = align_up(o + 4 * B, 256);

@@ -255,6 +255,8 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
     sf_cta[kSfCtaInts * g + 1] = (int32_t)u1;
     sf_cta[kSfCtaInts * g + 2] = cf_range[2 * g];
     sf_cta[kSfCtaInts * g + 3] = cf_range[2 * g + 1];
+    sf_cta[kSfCtaInts * g + 4] = 0;
+    if (u0 < u1) sf_cta[kSfCtaInts * g + 4] = sf_item[kSfItemInts * sf_unit[(size_t)kSfUnitInts * u0 + 1] + 1];
     // one segment for every item this CTA touches
     int64_t u = u0;
     while (u < u1) {

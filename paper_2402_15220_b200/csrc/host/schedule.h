@@ -26,9 +26,11 @@ constexpr int kFusedTileRows = 64;   // fused kernel: 4 consumer warps x 16 rows
 // Fused-kernel chunk-first unit (kCfUnitInts int32): {tile, head, k, flags}
 constexpr int kCfUnitInts = 4;
 
-// Seq-first CTA record (kSfCtaInts int32 each): a contiguous range of
-// (row, head, chunk) units [u0, u1) starting inside item `item0` at unit `off0`.
-constexpr int kSfCtaInts = 4;
+// Seq-first CTA record (kSfCtaInts int32 each): {u0, u1, cf0, cf1, ord0, ...}:
+// seq-first units [u0, u1), fused chunk-first units [cf0, cf1), and the segment
+// ordinal of the CTA's first item when that item continues from an earlier CTA
+// (CTAs without seq-first units may sit between an item's segments).
+constexpr int kSfCtaInts = 8;
 // Seq-first item record (kSfItemInts int32 each), item = row * h + head:
 // segment-partial slot base, number of CTA segments, first CTA.
 constexpr int kSfItemInts = 4;

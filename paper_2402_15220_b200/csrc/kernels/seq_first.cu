@@ -209,8 +209,10 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
       if (last && !full) {
         const int4 rec = *reinterpret_cast<const int4*>(t.sf_item + (size_t)item * kSfItemInts);
         nsegs = rec.y;
-        seg = rec.x + ((int)blockIdx.x - rec.z);
-        if ((int)blockIdx.x - rec.z == nsegs - 1) flags |= F_FINISH;
+        // ordinal among the CTAs touching the item: only a continued first item has one > 0
+        const int ord = (u - k < u0) ? t.sf_cta[blockIdx.x * kSfCtaInts + 4] : 0;
+        seg = rec.x + ord;
+        if (ord == nsegs - 1) flags |= F_FINISH;
       }
       if (last && full) {
 #pragma unroll
@@ -310,8 +312,8 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
 CA_DEV void wait_cf_ready(const DevTables& t, const uint32_t* __restrict__ cf_flags, uint32_t tag, int mg0, int mg1,
                           int head, int h, int ct) {
   for (int e = mg0 + ct; e < mg1; e += kConsumerWarps * 32) {
-    const volatile uint32_t* f = cf_flags + (size_t)t.mg_tile[e] * h + head;
-    while (*f != tag) __nanosleep(20);
+    const uint32_t* f = cf_flags + (size_t)t.mg_tile[e] * h + head;
+    while (ld_acquire_gpu(f) != tag) __nanosleep(20);
   }
   __threadfence();
   named_sync_consumers();
@@ -375,10 +377,10 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
       srow[D + 1] = an;
     }
   }
+  __threadfence();  // every writer's part of the segment row visible GPU-wide ...
   named_sync_consumers();
   if (ct == 0) {
-    __threadfence();  // the segment row is visible GPU-wide before its flag
-    *reinterpret_cast<volatile uint32_t*>(segflags + md.seg) = tag;
+    st_release_gpu(segflags + md.seg, tag);  // ... before its flag
     // The CTA holding the item's last segment meets it first in its range (the
     // item continues from the previous CTA): it finishes the item after its
     // own units, so the ring never stalls on the other segments.
@@ -404,8 +406,7 @@ CA_DEV void sf_fixup(SfShared<D, NG>& S, const float* __restrict__ pO, const flo
   const int head = md.item % h;
   if (t.fused) wait_cf_ready(t, cf_flags, tag, md.mg0, md.mg1, head, h, ct);
   if (ct < md.nsegs - 1) {
-    const volatile uint32_t* f = segflags + base + ct;
-    while (*f != tag) __nanosleep(32);
+    while (ld_acquire_gpu(segflags + base + ct) != tag) __nanosleep(32);
   }
   __threadfence();
   named_sync_consumers();
@@ -544,11 +545,9 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
               }
             }
           }
+          __threadfence();  // every writer's partial rows visible GPU-wide ...
           named_sync_consumers();
-          if (ct == 0) {
-            __threadfence();  // partial rows visible GPU-wide before the flag
-            *reinterpret_cast<volatile uint32_t*>(cf_flags + (size_t)tile * h + head) = tag;
-          }
+          if (ct == 0) st_release_gpu(cf_flags + (size_t)tile * h + head, tag);  // ... before the flag
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty_bar[s]);

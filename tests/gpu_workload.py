@@ -3,6 +3,8 @@ compute the fp64 oracle on the same inputs.  (Test infrastructure: may import
 oracle/; the product package never does.)"""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -30,6 +32,9 @@ class Harness:
                                  num_layers=num_layers, share_threshold=thr, prefix_match=(mode != "b0"),
                                  device=device)
         self.dev = self.ca.device
+        for kv in filter(None, os.environ.get("CA_TEST_OPTS", "").split(",")):  # e.g. "fused=0"
+            key, val = kv.split("=")
+            self.ca.set_option(key, int(val))
         self.seqs: dict[int, list[int]] = {}
         self.step = 0
 
@@ -90,6 +95,9 @@ class Harness:
         if rows is not None:
             got, ref = got[rows], ref[rows]
         err = float(np.abs(got - ref).max()) if got.size else 0.0
+        if err > tol:  # which (row, head) cells are off
+            bad = np.argwhere(np.abs(got - ref).max(axis=-1) > tol)
+            print("bad (row, head):", bad[:20].tolist(), "of", got.shape[:2])
         assert np.isfinite(got).all(), "non-finite output"
         assert err <= tol, f"max abs err {err} > {tol}"
         return err, out
