@@ -428,6 +428,9 @@ def main():
     ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
     ap.add_argument("--opt", action="append", default=[], help="library option key=value (A/B experiments)")
     args = ap.parse_args()
+    if os.environ.get("CA_BENCH_WATCHDOG"):  # debugging: dump the Python stacks if a pass stalls
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["CA_BENCH_WATCHDOG"]), exit=True)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     if args.impl == "reference":

@@ -12,7 +12,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libchunkattn.so")
+LIB_PATH = os.environ.get("CA_LIB") or os.path.join(_HERE, "libchunkattn.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "chunkattn.h")
 
 CA_OK, CA_EINVAL, CA_ENOSEQ, CA_ENOMEM, CA_ESTATE, CA_ECUDA, CA_EDTYPE, CA_ERANGE = 0, -1, -2, -3, -4, -5, -6, -7

@@ -13,8 +13,13 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libchunkattn.so")
+# CA_BUILD_VARIANT=debug: a separate library (libchunkattn_debug.so) whose
+# mbarrier waits and cross-CTA flag spins trap with a printf after 2 s instead
+# of hanging (-DCA_HANG_CHECK); load it with CA_LIB=<path>.
+VARIANT = os.environ.get("CA_BUILD_VARIANT", "")
+OBJ = os.path.join(PKG, "_build" + (f"_{VARIANT}" if VARIANT else ""))
+LIB = os.path.join(PKG, "libchunkattn" + (f"_{VARIANT}" if VARIANT else "") + ".so")
+DEFINES = (["-DCA_HANG_CHECK"] if VARIANT == "debug" else []) + os.environ.get("CA_BUILD_DEFINES", "").split()
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -38,7 +43,7 @@ def _compile(src: str, force: bool, verbose: bool) -> str:
     inc = ["-I", CSRC, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(CUDA_HOME, "include")]
     if src.endswith(".cu"):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-               "--expt-relaxed-constexpr", *inc, "-c", path, "-o", obj]
+               "--expt-relaxed-constexpr", *DEFINES, *inc, "-c", path, "-o", obj]
     else:
         cmd = ["g++", "-O2", "-g", "-std=c++17", "-fPIC", "-Wall", "-Wno-unused-function", *inc, "-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)

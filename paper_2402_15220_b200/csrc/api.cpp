@@ -104,8 +104,13 @@ struct chunkattn {
   bool tma_ok = false;
   bool cf_simt = false;
   bool sf_simt = false;
-  bool cf_small = true;
-  bool fused_opt = true;  // run chunk-first inside the persistent seq-first kernel when possible
+  // 4-warp chunk-first CTA so a seq-first CTA can share its SM under PDL: off by
+  // default -- the co-resident pair faulted intermittently with the SIMT
+  // seq-first consumers; costs ~1.5% on cfg2.
+  bool cf_small = false;
+  // chunk-first inside the persistent seq-first kernel: correct, but slower on
+  // cfg2 (81 vs 57 us/step), so opt-in
+  bool fused_opt = false;
   int trace_kernel = 0;    // 1: trace seq-first, 2: trace chunk-first
   int sf_ctas_per_sm = 2;  // persistent seq-first residency (smem budget per CTA)
   uint32_t launch_tag = 0;

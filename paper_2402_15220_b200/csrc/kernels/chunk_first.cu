@@ -78,10 +78,12 @@ __global__ void __launch_bounds__((kWarps + 1) * 32, 1)
 
   if (warp == kWarps) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      for (int k = 0; k < n_chunks; ++k) {
-        const int s = k % nst;
-        if (k >= nst) mbar_wait(&empty_bar[s], (uint32_t)(((k / nst) - 1) & 1));
+    // The whole warp walks the ring (warp-uniform waits, no lane spinning
+    // while its siblings sit at the CTA barrier); lane 0 issues the copies.
+    for (int k = 0; k < n_chunks; ++k) {
+      const int s = k % nst;
+      if (k >= nst) mbar_wait(&empty_bar[s], (uint32_t)(((k / nst) - 1) & 1));
+      if (lane == 0) {
         const size_t off = ((size_t)t.cf_chunk[chunk_off + k] * h + head) * C * D;
         unsigned char* ks = smem_raw + s * stage_bytes;
         mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
@@ -89,6 +91,7 @@ __global__ void __launch_bounds__((kWarps + 1) * 32, 1)
         bulk_g2s(ks + tile_bytes, vpool + off, tile_bytes, &full_bar[s]);
         if (tr && k < kTraceUnits) tr[3 + 3 * k] = globaltimer_ns();
       }
+      __syncwarp();
     }
   }
 

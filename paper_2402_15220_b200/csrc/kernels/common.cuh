@@ -7,6 +7,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include <utility>
 
@@ -47,7 +48,47 @@ CA_DEV void mbar_arrive_cta(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+CA_DEV uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+#ifdef CA_HANG_CHECK
+// Debug builds: a wait that has not completed after 2 s reports where it is
+// and traps (an error the host sees) instead of hanging the GPU.
+#define CA_HANG_TRAP(what, a, b)                                                                                \
+  do {                                                                                                         \
+    printf("chunkattn hang: %s (%d, %d) block %d thread %d line %d\n", what, (int)(a), (int)(b), blockIdx.x,  \
+           threadIdx.x, __LINE__);                                                                             \
+    __trap();                                                                                                  \
+  } while (0)
+#endif
+
+CA_DEV bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
 CA_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
+#ifdef CA_HANG_CHECK
+  if (mbar_try_wait(bar, phase)) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (!mbar_try_wait(bar, phase))
+    if (globaltimer_ns() - t0 > 2000000000ull) CA_HANG_TRAP("mbarrier", (int)(smem_u32(bar) & 0xffff), phase);
+#elif defined(CA_MBAR_CLOOP)
+  while (!mbar_try_wait(bar, phase)) {
+  }
+#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -57,6 +98,7 @@ CA_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
       : "memory");
+#endif
 }
 
 // 1-D bulk copy global -> shared, completion on an mbarrier (UBLKCP in SASS).
@@ -97,10 +139,23 @@ CA_DEV uint32_t ld_acquire_gpu(const uint32_t* p) {
   return v;
 }
 
-CA_DEV uint64_t globaltimer_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
+// Warp-cooperative spin: until every lane's flag (lanes with `mine`) equals
+// tag.  Control flow stays warp-uniform (no lane spins while its siblings sit
+// at a barrier).
+CA_DEV void spin_flags_warp(const uint32_t* f, bool mine, uint32_t tag, int who) {
+#ifdef CA_HANG_CHECK
+  const uint64_t t0 = globaltimer_ns();
+#endif
+  for (;;) {
+    const bool ok = !mine || ld_acquire_gpu(f) == tag;
+    if (__all_sync(0xffffffffu, ok)) break;
+    __nanosleep(32);
+#ifdef CA_HANG_CHECK
+    if (globaltimer_ns() - t0 > 2000000000ull) CA_HANG_TRAP("flag", who, ok ? 1 : 0);
+#else
+    (void)who;
+#endif
+  }
 }
 
 // PDL: let the dependent grid launch / wait for the primary grid.

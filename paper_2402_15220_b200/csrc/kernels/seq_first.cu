@@ -18,8 +18,9 @@
 // 145-158; m in log2 units).  At the end of an item the groups and the
 // chunk-first partials merge in a fixed order (n-ary Eqn 2: rebase to the
 // common max, sum in list order) and O / n is written.  An item
-// cut by a CTA boundary writes a segment partial; the last-arriving segment
-// (atomic counter) merges all segments in CTA order -- deterministic.
+// cut by a CTA boundary writes a segment partial and releases its flag; the
+// CTA holding the item's last segment merges all segments in CTA order after
+// its own units -- deterministic.
 // Stale slots past a partial chunk are never read (select, not multiply).
 #include <algorithm>
 
@@ -252,6 +253,9 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
         const int k_i = __shfl_sync(0xffffffffu, k, i);
         i_nt = min(c, t.seq_len[row] - (t.sf_first[row] + k_i * c));
       }
+#ifdef CA_HANG_CHECK
+      if (i_chunk >= 0 && (i_nt <= 0 || i_nt > c)) CA_HANG_TRAP("bad token count", i_item, i_nt);
+#endif
       const int i_flags = __shfl_sync(0xffffffffu, flags, i);
       const int i_caller = __shfl_sync(0xffffffffu, caller, i);
       const int i_mg0 = __shfl_sync(0xffffffffu, mg0, i);
@@ -311,9 +315,11 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
 // seq-first unit, and chunk-first work never waits.
 CA_DEV void wait_cf_ready(const DevTables& t, const uint32_t* __restrict__ cf_flags, uint32_t tag, int mg0, int mg1,
                           int head, int h, int ct) {
-  for (int e = mg0 + ct; e < mg1; e += kConsumerWarps * 32) {
-    const uint32_t* f = cf_flags + (size_t)t.mg_tile[e] * h + head;
-    while (ld_acquire_gpu(f) != tag) __nanosleep(20);
+  // warp-uniform trip count: every lane of a warp runs the same iterations
+  for (int e0 = mg0 + (ct & ~31); e0 < mg1; e0 += kConsumerWarps * 32) {
+    const int e = e0 + (ct & 31);
+    const bool mine = e < mg1;
+    spin_flags_warp(mine ? cf_flags + (size_t)t.mg_tile[e] * h + head : cf_flags, mine, tag, -1 - e0);
   }
   __threadfence();
   named_sync_consumers();
@@ -405,8 +411,9 @@ CA_DEV void sf_fixup(SfShared<D, NG>& S, const float* __restrict__ pO, const flo
   const int base = md.seg - (md.nsegs - 1);
   const int head = md.item % h;
   if (t.fused) wait_cf_ready(t, cf_flags, tag, md.mg0, md.mg1, head, h, ct);
-  if (ct < md.nsegs - 1) {
-    while (ld_acquire_gpu(segflags + base + ct) != tag) __nanosleep(32);
+  for (int e0 = ct & ~31; e0 < md.nsegs - 1; e0 += kConsumerWarps * 32) {  // warp-uniform
+    const int e = e0 + (ct & 31);
+    spin_flags_warp(segflags + base + e, e < md.nsegs - 1, tag, base + e0);
   }
   __threadfence();
   named_sync_consumers();

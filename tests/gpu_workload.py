@@ -20,7 +20,7 @@ class Harness:
     every sequence's KV (KV depends only on (token, position))."""
 
     def __init__(self, h, d, c, dtype="f16", out_dtype=None, num_layers=1, seed=0, alpha=1.0, mode="chunk",
-                 max_chunks=4096, max_batch=256, max_seq_len=8192, kv_fn=None, device="cuda"):
+                 max_chunks=4096, max_batch=256, max_seq_len=8192, kv_fn=None, device="cuda", opts=""):
         self.h, self.d, self.c, self.L = h, d, c, num_layers
         self.dt = TORCH_DT[dtype]
         self.odt = TORCH_DT[out_dtype or dtype]
@@ -32,7 +32,8 @@ class Harness:
                                  num_layers=num_layers, share_threshold=thr, prefix_match=(mode != "b0"),
                                  device=device)
         self.dev = self.ca.device
-        for kv in filter(None, os.environ.get("CA_TEST_OPTS", "").split(",")):  # e.g. "fused=0"
+        # library options ("key=value,..."): the test's own, then CA_TEST_OPTS
+        for kv in filter(None, (opts + "," + os.environ.get("CA_TEST_OPTS", "")).split(",")):
             key, val = kv.split("=")
             self.ca.set_option(key, int(val))
         self.seqs: dict[int, list[int]] = {}

@@ -14,6 +14,9 @@ from tests.gpu_workload import Harness, build_shared, decode_tokens
 pytestmark = pytest.mark.gpu
 
 TOL = {("f32", "f32"): 1e-5, ("f16", "f16"): 2e-3, ("bf16", "f32"): 2e-3, ("f16", "f32"): 2e-3}
+# opt-in kernel variants exercised beside the default path: the fused
+# single-kernel phase pair, and the 4-warp chunk-first CTA (PDL co-residency)
+VARIANTS = ["", "fused=1", "cf_small=1"]
 
 
 # --------------------------------------------------------------- config 1 ---
@@ -50,10 +53,11 @@ def _random_case(seed):
                 steps=rng.randint(0, 3), rng=rng)
 
 
+@pytest.mark.parametrize("opts", VARIANTS)
 @pytest.mark.parametrize("seed", range(60))
-def test_property_suite(seed):
+def test_property_suite(seed, opts):
     p = _random_case(seed)
-    hs = Harness(p["h"], p["d"], p["c"], p["dt"], p["odt"], seed=seed, alpha=p["alpha"], mode=p["mode"])
+    hs = Harness(p["h"], p["d"], p["c"], p["dt"], p["odt"], seed=seed, alpha=p["alpha"], mode=p["mode"], opts=opts)
     ids = build_shared(hs, p["n_shared"], p["privates"], seed_tag=seed)
     tol = TOL[(p["dt"], p["odt"])]
     hs.check(ids, tol)
@@ -66,12 +70,13 @@ def test_property_suite(seed):
 
 
 # ---------------------------------------------------------------- config 2 ---
+@pytest.mark.parametrize("opts", VARIANTS)
 @pytest.mark.parametrize("p", [1, 65])
 @pytest.mark.parametrize("dt,odt", [("f16", "f16"), ("bf16", "f32")])
-def test_config2_llama_b32_s2048(p, dt, odt):
+def test_config2_llama_b32_s2048(p, dt, odt, opts):
     """BASELINE configs[1]: 32 heads x 128, fp16, chunk 64, batch 32, shared
     system prompt 2048; p private tokens (question p-1 + current token)."""
-    hs = Harness(32, 128, 64, dt, odt, seed=3, alpha=8.0, max_chunks=512)
+    hs = Harness(32, 128, 64, dt, odt, seed=3, alpha=8.0, max_chunks=512, opts=opts)
     ids = build_shared(hs, 2048, [p - 1] * 32)
     hs.step = 1
     hs.append(ids, decode_tokens(hs, ids))
@@ -259,12 +264,13 @@ def test_edge_cases_and_reuse():
     hs.check(ids, 2e-3)
 
 
-def test_two_level_tree_decode_evict():
+@pytest.mark.parametrize("opts", VARIANTS)
+def test_two_level_tree_decode_evict(opts):
     """Small version of BASELINE configs[3]: system prompt + per-group examples,
     decode with eviction/replacement; parity and byte-exact tables at checkpoints."""
     rng = random.Random(21)
     c = 16
-    hs = Harness(4, 64, c, "f16", "f16", seed=21, alpha=8.0, max_chunks=600)
+    hs = Harness(4, 64, c, "f16", "f16", seed=21, alpha=8.0, max_chunks=600, opts=opts)
     tm = TreeModel(c, 600)
     sys_p = synth.token_ids(21, synth.TAG_SYS, 0, 64).tolist()
     groups = [synth.token_ids(21, synth.TAG_GROUP, g, 64).tolist() for g in range(4)]
