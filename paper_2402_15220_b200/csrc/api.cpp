@@ -7,6 +7,7 @@
 // double-buffered staging area and one cudaMemcpyAsync on the caller's stream.
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -32,8 +33,8 @@ chunkattn_status fail(chunkattn_status s, const std::string& msg) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t attend_perm, append_row, tables, pO, pMN, segO, segMN, counters, trace, total;
-  int64_t table_cap, slot_cap;
+  size_t attend_perm, append_row, tables, pO, segO, counters, trace, total;
+  int64_t table_cap, slot_cap, seg_cap;
 };
 
 bool valid_config(const chunkattn_config* c, std::string* why) {
@@ -73,15 +74,14 @@ WsLayout ws_layout(const chunkattn_config* c) {
   // chunk-first partials [slot][h][d + 4] fp32: o[0..d), m (log2 units) at d, n at d+1
   w.pO = o;
   o = align_up(o + (size_t)4 * w.slot_cap * c->num_heads * (c->head_dim + 4), 256);
-  w.pMN = o;
-  // segment partials of seq-first items split across CTAs (<= 2 per CTA), same row format
+  // seq-first segment partials (items merged by their last contributor: split
+  // items, and in the fused kernel items with chunk-first partials), same row
+  // format; <= one per item plus one extra per CTA boundary
+  w.seg_cap = B * c->num_heads + 2 * kMaxSfCtas;
   w.segO = o;
-  o = align_up(o + (size_t)4 * 2 * kMaxSfCtas * (c->head_dim + 4), 256);
-  w.segMN = o;
-  w.counters = o;  // release flags of segment partials [2 * kMaxSfCtas] u32 (zeroed; tag-compared)
-  o = align_up(o + (size_t)4 * 2 * kMaxSfCtas, 256);
-  w.pMN = o;  // fused chunk-first readiness flags [tiles <= slot_cap][h] u32 (zeroed; tag-compared)
-  o = align_up(o + (size_t)4 * w.slot_cap * c->num_heads, 256);
+  o = align_up(o + (size_t)4 * w.seg_cap * (c->head_dim + 4), 256);
+  w.counters = o;  // per-item contribution counters [B * h] u32 (zeroed; reset by each merge)
+  o = align_up(o + (size_t)4 * B * c->num_heads, 256);
   w.trace = o;  // debug timeline (option "trace"): the last kTraceCtas*kTraceStride u64 words
   o = align_up(o + (size_t)8 * kTraceCtas * kTraceStride, 256);
   w.total = o;
@@ -108,13 +108,13 @@ struct chunkattn {
   // default -- the co-resident pair faulted intermittently with the SIMT
   // seq-first consumers; costs ~1.5% on cfg2.
   bool cf_small = false;
-  // chunk-first inside the persistent seq-first kernel: correct, but slower on
-  // cfg2 (81 vs 57 us/step), so opt-in
-  bool fused_opt = false;
+  // chunk-first units inside the persistent seq-first kernel (one launch per
+  // attend; falls back to two kernels when the schedule does not allow it)
+  bool fused_opt = true;
   int trace_kernel = 0;    // 1: trace seq-first, 2: trace chunk-first
   int sf_ctas_per_sm = 2;  // persistent seq-first residency (smem budget per CTA)
-  uint32_t launch_tag = 0;
   int sf_prefetch = 0;     // seq-first L2 prefetch distance (units); measured slower on B200
+  int diag_nocompute = 0;  // DIAGNOSTIC ONLY (wrong outputs): seq-first consumers skip the math
   bool use_pdl = true;
   int num_sms = 148;
   int64_t cf_cpt_forced = 0;
@@ -126,7 +126,7 @@ struct chunkattn {
   int64_t uploaded_epoch = -1;
   std::vector<int64_t> attend_ids;
   int64_t attend_epoch = -1;
-  std::vector<int64_t> append_ids;
+  std::vector<int64_t> append_ids, scratch_ids;
   std::vector<int32_t> append_rows;
   std::vector<AppendItem> append_items;
   int64_t append_epoch = -1;
@@ -321,6 +321,7 @@ chunkattn_status chunkattn_create(const chunkattn_config* cfg, const chunkattn_b
   h->sopt.num_heads = cfg->num_heads;
   h->sopt.slot_capacity = h->ws.slot_cap;
   h->sopt.table_capacity = h->ws.table_cap;
+  h->sopt.seg_capacity = h->ws.seg_cap;
   h->sopt.cf_target_ctas = 148;
   if (!h->host_only) {
     if (!buf || !buf->k_pool || !buf->v_pool || !buf->workspace) {
@@ -431,14 +432,16 @@ chunkattn_status chunkattn_append_kv(chunkattn_t h, int64_t n, const int64_t* se
   if (n == 0) return CA_OK;
   if (!h->host_only && (!k || !v)) return fail(CA_EINVAL, "null k/v");
   {
-    std::unordered_set<int64_t> seen;
-    seen.reserve(n * 2);
     for (int64_t i = 0; i < n; ++i) {
       const Sequence* s = h->tree.find(seq_ids[i]);
       if (!s) return fail(CA_ENOSEQ, "unknown seq id " + std::to_string(seq_ids[i]));
-      if (!seen.insert(seq_ids[i]).second) return fail(CA_EINVAL, "duplicate seq id in append");
       if (s->len + 1 > h->cfg.max_seq_len) return fail(CA_EINVAL, "sequence would exceed max_seq_len");
     }
+    // duplicates: sorted scratch copy (no per-call hashing / allocation)
+    h->scratch_ids.assign(seq_ids, seq_ids + n);
+    std::sort(h->scratch_ids.begin(), h->scratch_ids.end());
+    if (std::adjacent_find(h->scratch_ids.begin(), h->scratch_ids.end()) != h->scratch_ids.end())
+      return fail(CA_EINVAL, "duplicate seq id in append");
   }
   const int64_t need = h->tree.append_needs(seq_ids, n);
   if (need > h->tree.pool().available()) return fail(CA_ENOMEM, "chunk pool exhausted");
@@ -529,14 +532,8 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   a.out = out;
   a.out_dtype = h->cfg.out_dtype;
   a.pO = reinterpret_cast<float*>(h->wsp + h->ws.pO);
-  a.pMN = reinterpret_cast<float2*>(h->wsp + h->ws.pMN);
   a.segO = reinterpret_cast<float*>(h->wsp + h->ws.segO);
-  a.segMN = reinterpret_cast<float2*>(h->wsp + h->ws.segMN);
-  a.counters = nullptr;
-  a.segflags = reinterpret_cast<uint32_t*>(h->wsp + h->ws.counters);
-  if (++h->launch_tag == 0) ++h->launch_tag;  // flags compare against a nonzero per-launch tag
-  a.tag = h->launch_tag;
-  a.cf_flags = reinterpret_cast<uint32_t*>(h->wsp + h->ws.pMN);
+  a.counters = reinterpret_cast<uint32_t*>(h->wsp + h->ws.counters);
   a.scale_log2 = h->scale() * 1.4426950408889634f;
   a.cf_tensor_cores = h->tma_ok && !h->cf_simt;
   a.sf_tensor_cores = !h->sf_simt;
@@ -544,7 +541,7 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   a.trace = h->trace_kernel ? reinterpret_cast<uint64_t*>(h->wsp + h->ws.trace) : nullptr;
   a.trace_cf = h->trace_kernel == 2;
   a.sf_ctas_per_sm = h->sf_ctas_per_sm;
-  a.sf_prefetch = h->sf_prefetch;
+  a.sf_prefetch = h->sf_prefetch | (h->diag_nocompute ? 256 : 0);
   a.use_pdl = h->use_pdl && !h->kernel_events;
   const DevTables t = h->dev_tables();
   cudaError_t e = cudaSuccess;
@@ -629,6 +626,8 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->sopt.cf_unit_cost = value < 1 ? 0.1 : (double)value / 10.0;  // tenths of a seq-first unit
   } else if (k == "cf_small") {
     h->cf_small = value != 0;
+  } else if (k == "diag_nocompute") {
+    h->diag_nocompute = value != 0;
   } else if (k == "sf_prefetch") {
     h->sf_prefetch = value < 0 ? 0 : (int)std::min<int64_t>(value, 31);
     return CA_OK;

@@ -178,8 +178,8 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   // ---- persistent seq-first schedule: items (row, head) in row-major order,
   // each worth max(1, private chunks) units; CTA g takes units
   // [U g / G, U (g+1) / G) (balanced, contiguous; stream-K style).  Items cut
-  // by a CTA boundary are finished by the last-arriving segment, which merges
-  // the segments in CTA order (deterministic).
+  // by a CTA boundary are merged by their last contributor, in CTA order
+  // (deterministic).
   const int32_t H = opt.num_heads;
   std::vector<int64_t> row_u0(b + 1, 0);  // first unit of row r (all heads)
   for (int32_t r = 0; r < b; ++r)
@@ -199,6 +199,8 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
         d[1] = r * H + hh;
         d[2] = k;
         d[3] = per;
+        d[4] = mg_ptr[r];
+        d[5] = mg_ptr[r + 1];
       }
     }
   }
@@ -237,8 +239,10 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
       for (int64_t job : mine[g]) {
         const int64_t tl = job / H;
         const int32_t nk = cf_tile[kCfTileInts * tl + CF_NCHUNK];
+        const int32_t off = cf_tile[kCfTileInts * tl + CF_CHUNK_OFF];
         for (int32_t k = 0; k < nk; ++k)
-          cf_unit.insert(cf_unit.end(), {(int32_t)tl, (int32_t)(job % H), k, (k == 0 ? 1 : 0) | (k == nk - 1 ? 2 : 0)});
+          cf_unit.insert(cf_unit.end(), {cf_chunk[off + k], (int32_t)tl, (int32_t)(job % H),
+                                         (k << 2) | (k == 0 ? 1 : 0) | (k == nk - 1 ? 2 : 0)});
       }
       cf_range[2 * g + 1] = (int32_t)(cf_unit.size() / kCfUnitInts);
     }
@@ -255,8 +259,6 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
     sf_cta[kSfCtaInts * g + 1] = (int32_t)u1;
     sf_cta[kSfCtaInts * g + 2] = cf_range[2 * g];
     sf_cta[kSfCtaInts * g + 3] = cf_range[2 * g + 1];
-    sf_cta[kSfCtaInts * g + 4] = 0;
-    if (u0 < u1) sf_cta[kSfCtaInts * g + 4] = sf_item[kSfItemInts * sf_unit[(size_t)kSfUnitInts * u0 + 1] + 1];
     // one segment for every item this CTA touches
     int64_t u = u0;
     while (u < u1) {
@@ -267,11 +269,62 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
       u += d[3] - d[2];
     }
   }
+  // Segment slots for the items merged by their last contributor: split
+  // items, and (fused) items whose chunk-first partials come from this same
+  // launch.  Every other item is finished in place (slot base -1).
   for (int64_t i = 0; i < (int64_t)b * H; ++i) {
     int32_t* rec = &sf_item[kSfItemInts * i];
-    if (rec[1] > 1) {
+    const int32_t row = (int32_t)(i / H);
+    if (rec[1] > 1 || (X.fused && mg_ptr[row + 1] > mg_ptr[row])) {
       rec[0] = seg_slots;
       seg_slots += rec[1];
+    } else {
+      rec[0] = -1;
+    }
+  }
+  // each unit's segment slot: base + ordinal of its CTA among the item's CTAs
+  {
+    std::vector<int32_t> ord((size_t)b * H, 0);
+    for (int64_t g = 0; g < G; ++g) {
+      for (int64_t u = ubound[g]; u < ubound[g + 1];) {
+        int32_t* d = &sf_unit[(size_t)kSfUnitInts * u];
+        const int32_t item = d[1], left = d[3] - d[2];
+        const int32_t* rec = &sf_item[kSfItemInts * item];
+        const int32_t seg = rec[0] < 0 ? -1 : rec[0] + ord[item]++;
+        const int64_t end = std::min<int64_t>(u + left, ubound[g + 1]);
+        for (int64_t v = u; v < end; ++v) {
+          sf_unit[(size_t)kSfUnitInts * v + 6] = seg;
+          sf_unit[(size_t)kSfUnitInts * v + 7] = rec[1];
+        }
+        u += left;
+      }
+    }
+  }
+  if (seg_slots > opt.seg_capacity) {
+    *err = "segment partials exceed workspace capacity";
+    return false;
+  }
+  // merges a CTA may owe at its end: items it touches that have slots, plus
+  // (fused) the rows of its chunk-first jobs
+  for (int64_t g = 0; g < G; ++g) {
+    int64_t owed = 0;
+    for (int64_t u = ubound[g]; u < ubound[g + 1];) {
+      const int32_t* d = &sf_unit[(size_t)kSfUnitInts * u];
+      owed += sf_item[kSfItemInts * d[1]] >= 0 ? 1 : 0;
+      u += d[3] - d[2];
+    }
+    for (int32_t cu = cf_range[2 * g]; cu < cf_range[2 * g + 1]; ++cu) {
+      const int32_t* d = &cf_unit[(size_t)kCfUnitInts * cu];
+      if (d[3] & 1) owed += cf_tile[kCfTileInts * d[1] + CF_ROW1] - cf_tile[kCfTileInts * d[1] + CF_ROW0];
+    }
+    if (owed > kMaxPendingMerges) {
+      if (X.fused) {  // too many merges for one CTA: run the two-kernel schedule instead
+        ScheduleOptions o2 = opt;
+        o2.fused = false;
+        return build_context(tree, o2, ctx, err);
+      }
+      *err = "too many pending merges per seq-first CTA";
+      return false;
     }
   }
   X.n_sf_ctas = (int32_t)G;

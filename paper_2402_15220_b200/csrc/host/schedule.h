@@ -23,21 +23,27 @@ enum CfTileField { CF_CHUNK_OFF = 0, CF_NCHUNK, CF_ROW0, CF_ROW1, CF_SLOT, CF_RU
 constexpr int kCfTileInts = 8;
 constexpr int kMaxCfTileRows = 128;  // rows of one chunk-first tile (8 warps x 16 rows)
 constexpr int kFusedTileRows = 64;   // fused kernel: 4 consumer warps x 16 rows
-// Fused-kernel chunk-first unit (kCfUnitInts int32): {tile, head, k, flags}
+// Fused-kernel chunk-first unit (kCfUnitInts int32): {chunk id, tile, head,
+// k << 2 | flags (1 first, 2 last)}
 constexpr int kCfUnitInts = 4;
 
-// Seq-first CTA record (kSfCtaInts int32 each): {u0, u1, cf0, cf1, ord0, ...}:
-// seq-first units [u0, u1), fused chunk-first units [cf0, cf1), and the segment
-// ordinal of the CTA's first item when that item continues from an earlier CTA
-// (CTAs without seq-first units may sit between an item's segments).
+// Seq-first CTA record (kSfCtaInts int32 each): {u0, u1, cf0, cf1, ...}:
+// seq-first units [u0, u1) and fused chunk-first units [cf0, cf1).
 constexpr int kSfCtaInts = 8;
 // Seq-first item record (kSfItemInts int32 each), item = row * h + head:
-// segment-partial slot base, number of CTA segments, first CTA.
+// segment-partial slot base (-1: the item is finished in place, no merge),
+// number of CTA segments, first CTA.
 constexpr int kSfItemInts = 4;
 constexpr int kMaxSfCtas = 2048;
-// Seq-first unit descriptor (kSfUnitInts int32 each): {chunk id or -1 (row
-// without private chunks), item, chunk index k in the item, units of the item}.
-constexpr int kSfUnitInts = 4;
+// Contributions one seq-first CTA makes (and merges it may owe) at its end:
+// the host checks the bound per CTA (fused: its chunk-first rows + its items).
+constexpr int kMaxPendingMerges = 256;
+// Seq-first unit descriptor (kSfUnitInts int32 each), resolved on the host so
+// the producer issues its copies after one load: {chunk id or -1 (row without
+// private chunks), item, chunk index k in the item, units of the item, merge
+// list [mg0, mg1) of the row, segment slot of this CTA's part of the item (-1:
+// finished in place), segments of the item}.
+constexpr int kSfUnitInts = 8;
 
 struct ScheduleOptions {
   int32_t share_threshold = 2;
@@ -46,9 +52,10 @@ struct ScheduleOptions {
   int64_t cf_target_ctas = 296;    // auto rule: heads * tiles >= this
   int64_t sf_ctas = 296;           // persistent seq-first grid (<= kMaxSfCtas)
   bool fused = false;              // chunk-first units run inside the persistent seq-first kernel
-  double cf_unit_cost = 2.0;       // fused balance: cost of a chunk-first unit in seq-first units
+  double cf_unit_cost = 1.6;       // fused balance: cost of a chunk-first unit in seq-first units (swept on cfg2)
   int64_t slot_capacity = 0;       // partial slots available in the workspace
   int64_t table_capacity = 0;      // int32 entries available for the blob
+  int64_t seg_capacity = 0;        // seq-first segment partial rows available
 };
 
 // Offsets (int32 units) of the arrays inside the blob.

@@ -89,7 +89,10 @@ __global__ void __launch_bounds__((kWarps + 1) * 32, 1)
         mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
         bulk_g2s(ks, kpool + off, tile_bytes, &full_bar[s]);
         bulk_g2s(ks + tile_bytes, vpool + off, tile_bytes, &full_bar[s]);
-        if (tr && k < kTraceUnits) tr[3 + 3 * k] = globaltimer_ns();
+        if (tr && k < kTraceUnits) {
+          tr[3 + 4 * k] = globaltimer_ns();
+          tr[6 + 4 * k] = stage_bytes;
+        }
       }
       __syncwarp();
     }
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__((kWarps + 1) * 32, 1)
     for (int k = lslice; k < n_chunks; k += L) {
       const int s = k % nst;
       mbar_wait(&full_bar[s], (uint32_t)((k / nst) & 1));
-      if (tr && lane == 0 && rgroup == 0 && k < kTraceUnits) tr[4 + 3 * k] = globaltimer_ns();
+      if (tr && lane == 0 && rgroup == 0 && k < kTraceUnits) tr[4 + 4 * k] = globaltimer_ns();
       if (active) {
         const uint32_t ks_u32 = base_u32 + s * stage_bytes;
         for (int t0 = 0; t0 < C; t0 += TPW)
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__((kWarps + 1) * 32, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&empty_bar[s]);
-      if (tr && lane == 0 && rgroup == 0 && k < kTraceUnits) tr[5 + 3 * k] = globaltimer_ns();
+      if (tr && lane == 0 && rgroup == 0 && k < kTraceUnits) tr[5 + 4 * k] = globaltimer_ns();
     }
   }
   wa.finish();
@@ -194,10 +197,8 @@ cudaError_t launch_mma(const AttnLaunch& a, const DevTables& t, int L, size_t bu
   const size_t epi = (size_t)W * 16 * D * 4;
   const size_t smem = std::max(nst * stage, epi);
   auto kern = cf_mma_kernel<T, D, TPW, W>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  // max shared-memory carveout: a seq-first CTA must fit beside this one (PDL overlap)
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  // max shared-memory carveout: a seq-first CTA can fit beside this one (PDL overlap)
+  cudaError_t e = set_smem_once((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;

@@ -9,6 +9,8 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <map>
+#include <mutex>
 #include <utility>
 
 #define CA_DEV __device__ __forceinline__
@@ -139,6 +141,11 @@ CA_DEV uint32_t ld_acquire_gpu(const uint32_t* p) {
   return v;
 }
 
+// GPU-scope acquire-release fence: after a CTA barrier, one thread's fence is
+// cumulative over the writes the barrier ordered before it (release side), and
+// orders its later reads after what it observed (acquire side).
+CA_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // Warp-cooperative spin: until every lane's flag (lanes with `mine`) equals
 // tag.  Control flow stays warp-uniform (no lane spins while its siblings sit
 // at a barrier).
@@ -163,6 +170,25 @@ CA_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_depend
 CA_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 }  // namespace dev
+
+// Allow `smem` bytes of dynamic shared memory (and the max carveout) for a
+// kernel, once per (kernel, device) and size: cudaFuncSetAttribute costs host
+// microseconds per call, paid on every decode step otherwise.
+inline cudaError_t set_smem_once(const void* kern, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({kern, dev});
+  if (it != done.end() && it->second >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) done[{kern, dev}] = smem;
+  return e;
+}
 
 // Launch `kern` on `st`; with pdl the launch may begin before the previous
 // kernel in the stream finishes (programmatic dependent launch): the kernel

@@ -36,11 +36,12 @@ struct DevTables {
 
 // Trace record per CTA (debug timing, option "trace"): words
 //   [0] kernel entry, [1] producer done, [2] consumers done,
-//   [3 + 3u] producer issue time of unit u, [4 + 3u] consumer data-ready time,
-//   [5 + 3u] consumer done time, for the first kTraceUnits units.
+//   [3 + 4u] producer issue time of unit u, [4 + 4u] consumer data-ready time,
+//   [5 + 4u] consumer done time, [6 + 4u] bytes the unit's copies move, for the
+//   first kTraceUnits units (fused: chunk-first units first).
 // Chunk-first uses the same layout per tile.
-constexpr int kTraceUnits = 41;
-constexpr int kTraceWords = 3 + 3 * kTraceUnits;  // 126 -> padded to 128
+constexpr int kTraceUnits = 31;
+constexpr int kTraceWords = 3 + 4 * kTraceUnits;  // 127 -> padded to 128
 constexpr int kTraceStride = 128;
 constexpr int kTraceCtas = 2048;
 
@@ -60,13 +61,8 @@ struct AttnLaunch {
   void* out;       // [n][h][d] out_dtype, caller order
   int32_t out_dtype;
   float* pO;       // [slots][h][d+4]: o, then m (log2 units), n
-  float2* pMN;     // unused (m, n live inside pO rows)
   float* segO;     // [seg slots][d+4] seq-first segment partials, same format
-  float2* segMN;   // unused
-  int32_t* counters;  // unused
-  uint32_t* segflags;  // [seg slots] release flags of segment partials (== tag when written)
-  uint32_t tag;        // this launch's flag value (nonzero, increments per attend)
-  uint32_t* cf_flags;  // fused: [tile * h + head] partial-ready flags (== tag when written)
+  uint32_t* counters;  // [b * h] per-item contribution counters (zero between launches)
   float scale_log2;
   uint64_t* trace;       // optional per-CTA timeline ([cta][kTraceWords] globaltimer ns), or null
   bool trace_cf;         // trace the chunk-first kernel instead of seq-first

@@ -105,11 +105,26 @@ struct WarpAttn {
 #pragma unroll
     for (int kk = 0; kk < TPW / 16; ++kk) {
       const uint32_t a[4] = {pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1]};
+      // masked tokens: P = 0 there, and their V rows (stale shared memory, maybe
+      // not finite) are zeroed in the B fragments so 0 * V cannot produce NaN.
+      // b0/b2 hold tokens tb, tb + 1 (low, high half); b1/b3 tokens tb + 8, tb + 9.
+      uint32_t vm0 = 0xffffffffu, vm1 = 0xffffffffu;
+      if (MASK) {
+        const int tb = tok0 + kk * 16 + (lane & 3) * 2;
+        vm0 = (tb < nvalid ? 0x0000ffffu : 0u) | (tb + 1 < nvalid ? 0xffff0000u : 0u);
+        vm1 = (tb + 8 < nvalid ? 0x0000ffffu : 0u) | (tb + 9 < nvalid ? 0xffff0000u : 0u);
+      }
 #pragma unroll
       for (int dp = 0; dp < DT / 2; ++dp) {
         uint32_t b0, b1, b2, b3;
         const int tok = tok0 + kk * 16 + (mi & 1) * 8 + r8;
         ldmatrix_x4_trans(v_u32 + tile_off<D>(tok, dp * 16 + (mi >> 1) * 8), b0, b1, b2, b3);
+        if (MASK) {
+          b0 &= vm0;
+          b2 &= vm0;
+          b1 &= vm1;
+          b3 &= vm1;
+        }
         Mma<T>::run(o[2 * dp], a, b0, b1);
         Mma<T>::run(o[2 * dp + 1], a, b2, b3);
       }

@@ -106,8 +106,9 @@ constexpr int kProducerWarps = 1;
 constexpr int kConsumerWarps = 4;
 constexpr int kSfThreads = (kProducerWarps + kConsumerWarps) * 32;
 constexpr int kMaxPrefetchSlots = 4;  // chunk-first partial rows staged per item
+constexpr int kMaxPend = kMaxPendingMerges;  // merges one CTA may owe (host-checked)
 
-enum : int { F_FIRST = 1, F_LAST = 2, F_FULL = 4, F_FINISH = 8, F_CF = 16 };
+enum : int { F_FIRST = 1, F_LAST = 2, F_FULL = 4, F_CF = 16 };
 
 struct StageMeta {
   int item, nt, flags, caller;
@@ -128,8 +129,10 @@ struct SfShared {
   float m[NG], n[NG];
   float o[NG][D];
   int pdl_done;
-  int fix_pending;
-  StageMeta fix;  // split item this CTA finishes after its own units
+  int n_pend;
+  int pend[kMaxPend];      // items whose merge this CTA owes (last contributor)
+  int n_contrib;
+  int2 contrib[kMaxPend];  // (item, weight) counted at the CTA's end
 };
 
 // Stage layout: K tile | V tile | q row | chunk-first partial rows.
@@ -155,32 +158,29 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
   // append, so no PDL wait): full K and V tiles of (chunk, head).
   for (int base = cf0; base < cf1; base += 32) {
     const int u = base + lane;
-    int tile = 0, head = 0, k = 0, uf = 0, chunk = 0;
-    if (u < cf1) {
-      const int4 d = *reinterpret_cast<const int4*>(t.cf_unit + (size_t)u * kCfUnitInts);
-      tile = d.x;
-      head = d.y;
-      k = d.z;
-      uf = d.w;
-      chunk = t.cf_chunk[t.cf_tile[tile * kCfTileInts + CF_CHUNK_OFF] + k];
-    }
+    int4 d = make_int4(0, 0, 0, 0);  // {chunk, tile, head, k << 2 | flags}
+    if (u < cf1) d = *reinterpret_cast<const int4*>(t.cf_unit + (size_t)u * kCfUnitInts);
     const int cnt = min(32, cf1 - base);
     for (int i = 0; i < cnt; ++i) {
-      const int i_tile = __shfl_sync(0xffffffffu, tile, i);
-      const int i_head = __shfl_sync(0xffffffffu, head, i);
-      const int i_k = __shfl_sync(0xffffffffu, k, i);
-      const int i_uf = __shfl_sync(0xffffffffu, uf, i);
-      const int i_chunk = __shfl_sync(0xffffffffu, chunk, i);
+      const int i_chunk = __shfl_sync(0xffffffffu, d.x, i);
+      const int i_tile = __shfl_sync(0xffffffffu, d.y, i);
+      const int i_head = __shfl_sync(0xffffffffu, d.z, i);
+      const int i_kf = __shfl_sync(0xffffffffu, d.w, i);
       const int s = jj % nst;
       if (jj >= nst) mbar_wait(&S.empty_bar[s], (uint32_t)(((jj / nst) - 1) & 1));
       if (lane == 0) {
-        const int fl = F_CF | ((i_uf & 1) ? F_FIRST : 0) | ((i_uf & 2) ? F_LAST : 0);
-        S.meta[s] = StageMeta{i_tile, c, fl, i_head, 0, 0, i_k, 0};
+        const int fl = F_CF | ((i_kf & 1) ? F_FIRST : 0) | ((i_kf & 2) ? F_LAST : 0);
+        S.meta[s] = StageMeta{i_tile, c, fl, i_head, 0, 0, i_kf >> 2, 0};
         unsigned char* st = smem_raw + (size_t)s * stage_bytes;
         const size_t off = ((size_t)i_chunk * h + i_head) * c * D;
         mbar_arrive_expect_tx(&S.full_bar[s], 2 * (uint32_t)tile_bytes);
         bulk_g2s(st, kpool + off, (uint32_t)tile_bytes, &S.full_bar[s]);
         bulk_g2s(st + tile_bytes, vpool + off, (uint32_t)tile_bytes, &S.full_bar[s]);
+        mbar_arrive_cta(&S.full_bar[s]);  // second arrival (the stage barrier counts 2)
+        if (tr && jj < kTraceUnits) {
+          tr[3 + 4 * jj] = globaltimer_ns();
+          tr[6 + 4 * jj] = 2 * tile_bytes;
+        }
       }
       __syncwarp();
       ++jj;
@@ -191,15 +191,17 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
     int chunk = -1, item = 0, k = 0, per = 1, nt = 0, caller = 0, mg0 = 0, mg1 = 0, seg = -1, nsegs = 1;
     int flags = 0, slot4[kMaxPrefetchSlots] = {0, 0, 0, 0};
     if (u < u1) {
-      const int4 d = *reinterpret_cast<const int4*>(t.sf_unit + (size_t)u * kSfUnitInts);
-      chunk = d.x;
-      item = d.y;
-      k = d.z;
-      per = d.w;
+      const int4 d0 = *reinterpret_cast<const int4*>(t.sf_unit + (size_t)u * kSfUnitInts);
+      const int4 d1 = *reinterpret_cast<const int4*>(t.sf_unit + (size_t)u * kSfUnitInts + 4);
+      chunk = d0.x;
+      item = d0.y;
+      k = d0.z;
+      per = d0.w;
+      mg0 = d1.x;
+      mg1 = d1.y;
+      seg = d1.z;
+      nsegs = d1.w;
       const int row = item / h;
-      caller = t.row_caller[row];
-      mg0 = t.mg_ptr[row];
-      mg1 = t.mg_ptr[row + 1];
       // only an item's last chunk can be partial -- and it is the one this
       // step's append writes: its length is read after the PDL wait
       if (chunk >= 0) nt = k < per - 1 ? c : (waited ? min(c, t.seq_len[row] - (t.sf_first[row] + k * c)) : -1);
@@ -207,15 +209,9 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
       const bool last = (u == u1 - 1) || k == per - 1;
       const bool full = (u - k >= u0) && (u - k + per <= u1);
       flags = (first ? F_FIRST : 0) | (last ? F_LAST : 0) | (full ? F_FULL : 0);
-      if (last && !full) {
-        const int4 rec = *reinterpret_cast<const int4*>(t.sf_item + (size_t)item * kSfItemInts);
-        nsegs = rec.y;
-        // ordinal among the CTAs touching the item: only a continued first item has one > 0
-        const int ord = (u - k < u0) ? t.sf_cta[blockIdx.x * kSfCtaInts + 4] : 0;
-        seg = rec.x + ord;
-        if (ord == nsegs - 1) flags |= F_FINISH;
-      }
-      if (last && full) {
+      // dependent loads, consumed only after the unit's K/V copies are issued
+      caller = t.row_caller[row];
+      if (last && seg < 0 && !t.fused) {
 #pragma unroll
         for (int e = 0; e < kMaxPrefetchSlots; ++e)
           if (mg0 + e < mg1) slot4[e] = t.mg_slot[mg0 + e];
@@ -243,8 +239,15 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
       const int i_chunk = __shfl_sync(0xffffffffu, chunk, i);
       const int i_item = __shfl_sync(0xffffffffu, item, i);
       int i_nt = __shfl_sync(0xffffffffu, nt, i);
-      const int i_flags0 = __shfl_sync(0xffffffffu, flags, i);
-      if (!waited && (i_nt < 0 || ((i_flags0 & F_LAST) && (i_flags0 & F_FULL)))) {
+      const int i_flags = __shfl_sync(0xffffffffu, flags, i);
+      const int i_mg0 = __shfl_sync(0xffffffffu, mg0, i);
+      const int i_mg1 = __shfl_sync(0xffffffffu, mg1, i);
+      const int i_seg = __shfl_sync(0xffffffffu, seg, i);
+      const int i_nsegs = __shfl_sync(0xffffffffu, nsegs, i);
+      // partials staged only for an item finished in place (fused: they are
+      // produced inside this kernel, so never staged)
+      const bool want_p = (i_flags & F_LAST) && i_seg < 0 && !t.fused;
+      if (!waited && (i_nt < 0 || want_p)) {
         pdl_wait();  // first unit touching this step's append / chunk-first output
         waited = true;
       }
@@ -256,37 +259,37 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
 #ifdef CA_HANG_CHECK
       if (i_chunk >= 0 && (i_nt <= 0 || i_nt > c)) CA_HANG_TRAP("bad token count", i_item, i_nt);
 #endif
-      const int i_flags = __shfl_sync(0xffffffffu, flags, i);
-      const int i_caller = __shfl_sync(0xffffffffu, caller, i);
-      const int i_mg0 = __shfl_sync(0xffffffffu, mg0, i);
-      const int i_mg1 = __shfl_sync(0xffffffffu, mg1, i);
-      const int i_seg = __shfl_sync(0xffffffffu, seg, i);
-      const int i_nsegs = __shfl_sync(0xffffffffu, nsegs, i);
-      int my_slot = 0;
-#pragma unroll
-      for (int e = 0; e < kMaxPrefetchSlots; ++e) {
-        const int v = __shfl_sync(0xffffffffu, slot4[e], i);
-        if (lane == e) my_slot = v;
-      }
       const int s = jj % nst;
       const int head = i_item % h;
       const bool want_q = (i_flags & F_FIRST) && i_chunk >= 0;
-      const bool want_p = (i_flags & F_LAST) && (i_flags & F_FULL);
-      // fused: the partials are produced inside this kernel -> read at finalize, not staged
-      const int np = (want_p && !t.fused) ? min(i_mg1 - i_mg0, kMaxPrefetchSlots) : 0;
+      const int np = want_p ? min(i_mg1 - i_mg0, kMaxPrefetchSlots) : 0;
       if (jj >= nst) mbar_wait(&S.empty_bar[s], (uint32_t)(((jj / nst) - 1) & 1));
       unsigned char* st = smem_raw + (size_t)s * stage_bytes;
       const uint32_t kv_bytes = (uint32_t)(i_nt * D * (int)sizeof(T));
       const uint32_t q_bytes = want_q ? (uint32_t)(D * sizeof(T)) : 0u;
       const uint32_t p_bytes = (uint32_t)(np * PR * 4);
+      // arrival 1: arm every byte of the stage and start the K/V copies (they
+      // need only the descriptor) ...
       if (lane == 0) {
-        S.meta[s] = StageMeta{i_item, i_nt, i_flags, i_caller, i_mg0, i_mg1, i_seg, i_nsegs};
         mbar_arrive_expect_tx(&S.full_bar[s], 2 * kv_bytes + q_bytes + p_bytes);
         if (kv_bytes) {
           const size_t off = ((size_t)i_chunk * h + head) * c * D;
           bulk_g2s(st, kpool + off, kv_bytes, &S.full_bar[s]);
           bulk_g2s(st + tile_bytes, vpool + off, kv_bytes, &S.full_bar[s]);
         }
+      }
+      // ... arrival 2 publishes the metadata once the dependent loads (caller,
+      // partial slots) are in; then the q row and the partial rows
+      const int i_caller = __shfl_sync(0xffffffffu, caller, i);
+      int my_slot = 0;
+#pragma unroll
+      for (int e = 0; e < kMaxPrefetchSlots; ++e) {
+        const int v = __shfl_sync(0xffffffffu, slot4[e], i);
+        if (lane == e) my_slot = v;
+      }
+      if (lane == 0) {
+        S.meta[s] = StageMeta{i_item, i_nt, i_flags, i_caller, i_mg0, i_mg1, i_seg, i_nsegs};
+        mbar_arrive_cta(&S.full_bar[s]);
         if (q_bytes) bulk_g2s(st + 2 * tile_bytes, q + ((size_t)i_caller * h + head) * D, q_bytes, &S.full_bar[s]);
       }
       __syncwarp();
@@ -298,47 +301,85 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
         bulk_prefetch_l2(pf_k, pf_bytes);
         bulk_prefetch_l2(vpool + (pf_k - kpool), pf_bytes);
       }
-      if (tr && lane == 0 && jj < kTraceUnits) tr[3 + 3 * jj] = globaltimer_ns();
+      if (tr && lane == 0 && jj < kTraceUnits) {
+        tr[3 + 4 * jj] = globaltimer_ns();
+        tr[6 + 4 * jj] = 2 * kv_bytes + q_bytes + p_bytes;
+      }
       ++jj;
     }
   }
 }
 
-// End of an item segment: the NG consumer states sit in S.m/S.n/S.o.  A whole
-// item merges the chunk-first partials (staged rows first, the rest from
-// global) with the states and writes O / n; a segment of a split item writes
-// its partial and the last-arriving segment merges all of them in CTA order.
-// n-ary Eqn 2: rebase to the common max, sum in the fixed list order.
-// Fused kernel: the chunk-first partials of (row, head) come from other CTAs
-// of this launch -- wait for their tiles' readiness flags (this launch's tag).
-// Deadlock-free: every CTA runs all its chunk-first units before any
-// seq-first unit, and chunk-first work never waits.
-CA_DEV void wait_cf_ready(const DevTables& t, const uint32_t* __restrict__ cf_flags, uint32_t tag, int mg0, int mg1,
-                          int head, int h, int ct) {
-  // warp-uniform trip count: every lane of a warp runs the same iterations
-  for (int e0 = mg0 + (ct & ~31); e0 < mg1; e0 += kConsumerWarps * 32) {
-    const int e = e0 + (ct & 31);
-    const bool mine = e < mg1;
-    spin_flags_warp(mine ? cf_flags + (size_t)t.mg_tile[e] * h + head : cf_flags, mine, tag, -1 - e0);
-  }
-  __threadfence();
-  named_sync_consumers();
+// Queue an item whose last contribution this CTA made: merged at the CTA's end.
+template <int D, int NG>
+CA_DEV void push_pending(SfShared<D, NG>& S, int item) {
+  const int i = atomicAdd(&S.n_pend, 1);
+  if (i < kMaxPend) S.pend[i] = item;
+#ifdef CA_HANG_CHECK
+  else CA_HANG_TRAP("pending merge list overflow", item, i);
+#endif
 }
 
+// Record a contribution (its partial rows are written): counted at the CTA's
+// end, so the stream never stalls on a GPU-scope fence.
+template <int D, int NG>
+CA_DEV void record_contribution(SfShared<D, NG>& S, int item, int w) {
+  const int i = atomicAdd(&S.n_contrib, 1);
+  if (i < kMaxPend) S.contrib[i] = make_int2(item, w);
+#ifdef CA_HANG_CHECK
+  else CA_HANG_TRAP("contribution list overflow", item, i);
+#endif
+}
+
+// CTA end: one warp counts the CTA's contributions.  The CTA barrier orders
+// every writer's partial rows before the warp's release fence (cumulative);
+// the add that completes an item's count (expected = its segments + its
+// chunk-first lane rows when those come from this launch) queues its merge
+// after an acquire fence.  Counters return to 0 when merged.
+template <int D, int NG>
+CA_DEV void settle_contributions(SfShared<D, NG>& S, uint32_t* __restrict__ cnt, const DevTables& t, int h,
+                                 int ct) {
+  named_sync_consumers();
+  const int n = min(S.n_contrib, kMaxPend);
+  if (ct < 32 && n > 0) {
+    fence_acq_rel_gpu();
+    bool any_last = false;
+    for (int i = ct; i < n; i += 32) {
+      const int2 c = S.contrib[i];
+      const int row = c.x / h;
+      const uint32_t expect = (uint32_t)(t.sf_item[(size_t)c.x * kSfItemInts + 1] +
+                                         (t.fused ? t.mg_ptr[row + 1] - t.mg_ptr[row] : 0));
+      const uint32_t old = atomicAdd(cnt + c.x, (uint32_t)c.y);
+      if (old + (uint32_t)c.y == expect) {
+        any_last = true;
+        push_pending(S, c.x);
+      }
+    }
+    if (__any_sync(0xffffffffu, any_last)) fence_acq_rel_gpu();
+  }
+}
+
+// End of an item segment: the NG consumer states sit in S.m/S.n/S.o.  An item
+// finished here with no outside contribution (one segment; chunk-first
+// partials already complete) merges the chunk-first partials (staged rows
+// first, the rest from global) with the states and writes O / n.  Otherwise the
+// segment's state goes to its slot in segO and the item's counter is bumped:
+// the last contributor (a segment, or in the fused kernel a chunk-first job)
+// merges everything in the fixed list order (chunk-first partials in merge-list
+// order, then the segments in CTA order): deterministic, and nobody waits.
+// n-ary Eqn 2: rebase to the common max, sum in the fixed list order.
 template <typename TO, int D, int NG>
 CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* pst, const float* __restrict__ pO,
-                        float* __restrict__ segO, uint32_t* __restrict__ segflags, uint32_t tag,
-                        const uint32_t* __restrict__ cf_flags, TO* __restrict__ out,
+                        float* __restrict__ segO, uint32_t* __restrict__ cnt, TO* __restrict__ out,
                         const DevTables& t, int h, int ct) {
   constexpr int PR = D + 4;
   const int head = md.item % h;
-  if (!S.pdl_done) {  // chunk-first partials (and the append) complete -- waited once per CTA
+  if (!S.pdl_done) {  // append (and chunk-first partials when not fused) complete -- waited once per CTA
     pdl_wait();
     named_sync_consumers();
     if (ct == 0) S.pdl_done = 1;
   }
-  if (md.flags & F_FULL) {
-    if (t.fused) wait_cf_ready(t, cf_flags, tag, md.mg0, md.mg1, head, h, ct);
+  if (md.seg < 0) {
     const int np = t.fused ? 0 : min(md.mg1 - md.mg0, kMaxPrefetchSlots);
     for (int x = ct; x < D; x += kConsumerWarps * 32) {
       float M = -INFINITY;
@@ -383,58 +424,90 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
       srow[D + 1] = an;
     }
   }
-  __threadfence();  // every writer's part of the segment row visible GPU-wide ...
-  named_sync_consumers();
-  if (ct == 0) {
-    st_release_gpu(segflags + md.seg, tag);  // ... before its flag
-    // The CTA holding the item's last segment meets it first in its range (the
-    // item continues from the previous CTA): it finishes the item after its
-    // own units, so the ring never stalls on the other segments.
-    if (md.flags & F_FINISH) {
-      S.fix = md;
-      S.fix_pending = 1;
-    }
-  }
+  if (ct == 0) record_contribution(S, md.item, 1);
 }
 
-// Deferred finish of the split item whose last segment this CTA holds: wait for
-// the other segments' flags (this launch's tag), then merge the chunk-first
-// partials and all segments in CTA order and write O / n.
+// The CTA's queued merges, one warp per item: contributions = the row's
+// chunk-first partials in merge-list order, then the item's segments in CTA
+// order (n-ary Eqn 2, fixed order).  Lane e holds contribution e's row and
+// (m, n): one round of loads for the max and the weights, one for the rows
+// (each lane 4 columns of every row).  Writes O / n, resets the counter.
 template <typename TO, int D, int NG>
-CA_DEV void sf_fixup(SfShared<D, NG>& S, const float* __restrict__ pO, const float* __restrict__ segO,
-                     const uint32_t* __restrict__ segflags, uint32_t tag, const uint32_t* __restrict__ cf_flags,
-                     TO* __restrict__ out, const DevTables& t, int h, int ct) {
+CA_DEV void merge_pending(SfShared<D, NG>& S, const float* __restrict__ pO, const float* __restrict__ segO,
+                          uint32_t* __restrict__ cnt, TO* __restrict__ out, const DevTables& t, int h, int ct) {
   constexpr int PR = D + 4;
   named_sync_consumers();
-  if (!S.fix_pending) return;
-  const StageMeta md = S.fix;
-  const int base = md.seg - (md.nsegs - 1);
-  const int head = md.item % h;
-  if (t.fused) wait_cf_ready(t, cf_flags, tag, md.mg0, md.mg1, head, h, ct);
-  for (int e0 = ct & ~31; e0 < md.nsegs - 1; e0 += kConsumerWarps * 32) {  // warp-uniform
-    const int e = e0 + (ct & 31);
-    spin_flags_warp(segflags + base + e, e < md.nsegs - 1, tag, base + e0);
-  }
-  __threadfence();
-  named_sync_consumers();
-  for (int x = ct; x < D; x += kConsumerWarps * 32) {
-    float M = -INFINITY;
-    for (int e = md.mg0; e < md.mg1; ++e) M = fmaxf(M, __ldcg(pO + ((size_t)t.mg_slot[e] * h + head) * PR + D));
-    for (int sg = 0; sg < md.nsegs; ++sg) M = fmaxf(M, __ldcg(segO + (size_t)(base + sg) * PR + D));
-    float ao = 0.f, an = 0.f;
-    for (int e = md.mg0; e < md.mg1; ++e) {
-      const float* pr = pO + ((size_t)t.mg_slot[e] * h + head) * PR;
-      const float w = fast_exp2(__ldcg(pr + D) - M);
-      ao = fmaf(w, __ldcg(pr + x), ao);
-      an = fmaf(w, __ldcg(pr + D + 1), an);
+  const int np = min(S.n_pend, kMaxPend);
+  const int lane = ct & 31;
+  for (int p = ct >> 5; p < np; p += kConsumerWarps) {
+    const int item = S.pend[p];
+    const int row = item / h, head = item % h;
+    const int mg0 = t.mg_ptr[row], ncf = t.mg_ptr[row + 1] - mg0;
+    const int4 rec = *reinterpret_cast<const int4*>(t.sf_item + (size_t)item * kSfItemInts);
+    const int E = ncf + rec.y;
+    TO* orow = out + ((size_t)t.row_caller[row] * h + head) * D;
+    if (E <= 32) {
+      const float* pr = nullptr;
+      float me = -INFINITY, ne = 0.f;
+      if (lane < E) {
+        pr = lane < ncf ? pO + ((size_t)t.mg_slot[mg0 + lane] * h + head) * PR : segO + (size_t)(rec.x + lane - ncf) * PR;
+        const float2 mn = __ldcg(reinterpret_cast<const float2*>(pr + D));
+        me = mn.x;
+        ne = mn.y;
+      }
+      float M = me;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+      const float w = lane < E ? fast_exp2(me - M) : 0.f;
+      float nsum = w * ne;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, off);
+      float4 ao = make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint64_t pu = reinterpret_cast<uint64_t>(pr);
+#pragma unroll 8
+      for (int e = 0; e < E; ++e) {
+        const float we = __shfl_sync(0xffffffffu, w, e);
+        const uint64_t pe = (uint64_t)__shfl_sync(0xffffffffu, (uint32_t)pu, e) |
+                            ((uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(pu >> 32), e) << 32);
+        if (lane * 4 < D) {
+          const float4 v = __ldcg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(pe) + lane * 4));
+          ao.x = fmaf(we, v.x, ao.x);
+          ao.y = fmaf(we, v.y, ao.y);
+          ao.z = fmaf(we, v.z, ao.z);
+          ao.w = fmaf(we, v.w, ao.w);
+        }
+      }
+      if (lane * 4 < D) {
+        Elem<TO>::store1(orow + lane * 4 + 0, ao.x / nsum);
+        Elem<TO>::store1(orow + lane * 4 + 1, ao.y / nsum);
+        Elem<TO>::store1(orow + lane * 4 + 2, ao.z / nsum);
+        Elem<TO>::store1(orow + lane * 4 + 3, ao.w / nsum);
+      }
+    } else {  // many contributions: per-column passes
+      for (int x = lane * 4; x < D; x += 128) {
+        float M = -INFINITY;
+        for (int e = 0; e < ncf; ++e) M = fmaxf(M, __ldcg(pO + ((size_t)t.mg_slot[mg0 + e] * h + head) * PR + D));
+        for (int sg = 0; sg < rec.y; ++sg) M = fmaxf(M, __ldcg(segO + (size_t)(rec.x + sg) * PR + D));
+        float4 ao = make_float4(0.f, 0.f, 0.f, 0.f);
+        float an = 0.f;
+        auto add = [&](const float* pr) {
+          const float w = fast_exp2(__ldcg(pr + D) - M);
+          const float4 v = __ldcg(reinterpret_cast<const float4*>(pr + x));
+          ao.x = fmaf(w, v.x, ao.x);
+          ao.y = fmaf(w, v.y, ao.y);
+          ao.z = fmaf(w, v.z, ao.z);
+          ao.w = fmaf(w, v.w, ao.w);
+          an = fmaf(w, __ldcg(pr + D + 1), an);
+        };
+        for (int e = 0; e < ncf; ++e) add(pO + ((size_t)t.mg_slot[mg0 + e] * h + head) * PR);
+        for (int sg = 0; sg < rec.y; ++sg) add(segO + (size_t)(rec.x + sg) * PR);
+        Elem<TO>::store1(orow + x + 0, ao.x / an);
+        Elem<TO>::store1(orow + x + 1, ao.y / an);
+        Elem<TO>::store1(orow + x + 2, ao.z / an);
+        Elem<TO>::store1(orow + x + 3, ao.w / an);
+      }
     }
-    for (int sg = 0; sg < md.nsegs; ++sg) {
-      const float* sr = segO + (size_t)(base + sg) * PR;
-      const float w = fast_exp2(__ldcg(sr + D) - M);
-      ao = fmaf(w, __ldcg(sr + x), ao);
-      an = fmaf(w, __ldcg(sr + D + 1), an);
-    }
-    Elem<TO>::store1(out + ((size_t)md.caller * h + head) * D + x, ao / an);
+    if (lane == 0) cnt[item] = 0u;
   }
 }
 
@@ -444,8 +517,7 @@ CA_DEV void sf_fixup(SfShared<D, NG>& S, const float* __restrict__ pO, const flo
 template <typename T, typename TO, int D, bool MMA, int TPW>
 __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     const T* __restrict__ kpool, const T* __restrict__ vpool, const T* __restrict__ q, TO* __restrict__ out,
-    float* __restrict__ pO, float* __restrict__ segO, uint32_t* __restrict__ segflags, uint32_t tag,
-    uint32_t* __restrict__ cf_flags, DevTables t, int32_t h, int32_t c, float scale_log2, int32_t nst,
+    float* __restrict__ pO, float* __restrict__ segO, uint32_t* __restrict__ cnt, DevTables t, int32_t h, int32_t c, float scale_log2, int32_t nst,
     uint32_t stage_bytes, uint64_t* __restrict__ trace, int32_t pf) {
   using G = Geo<T, D>;
   constexpr int NG = MMA ? kConsumerWarps : G::kGroups;
@@ -453,24 +525,25 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
   __shared__ SfShared<D, NG> S;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool diag_nocompute = (pf & 256) != 0;  // diagnostic: stream only (outputs wrong)
+  pf &= 255;
   uint64_t* tr = trace && blockIdx.x < kTraceCtas ? trace + (size_t)blockIdx.x * kTraceStride : nullptr;
   if (tr && tid == 0) tr[0] = globaltimer_ns();
   const int u0 = t.sf_cta[blockIdx.x * kSfCtaInts + 0], u1 = t.sf_cta[blockIdx.x * kSfCtaInts + 1];
   const size_t tile_bytes = (size_t)c * D * sizeof(T);
 
-  // stale shared memory must be finite: masked MMA columns multiply P = 0 by it
-  for (size_t i = tid * 16; i < (size_t)nst * stage_bytes; i += kSfThreads * 16)
-    *reinterpret_cast<uint4*>(smem_raw + i) = make_uint4(0, 0, 0, 0);
+  // no zero fill: stale rows past a partial chunk are masked by select (S) and
+  // zeroed in the B fragments (V, mma_attn.cuh); the SIMT path never reads them
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) {
       S.pdl_done = 0;
-      S.fix_pending = 0;
-      mbar_init(&S.full_bar[s], 1);
+      S.n_pend = 0;
+      S.n_contrib = 0;
+      mbar_init(&S.full_bar[s], 2);  // producer: arm + copies, then metadata
       mbar_init(&S.empty_bar[s], kConsumerWarps);
     }
     fence_barrier_init();
   }
-  fence_proxy_async();  // generic-proxy zero fill before async-proxy bulk writes
   __syncthreads();
 
   if (warp == 0) {
@@ -504,6 +577,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
       for (int u = cf0; u < cf1; ++u, ++jj) {
         const int s = jj % nst;
         mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
+        if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 4 * jj] = globaltimer_ns();
         const StageMeta md = S.meta[s];
         const int tile = md.item, head = md.caller, k = md.seg;
         if (md.flags & F_FIRST) {
@@ -528,7 +602,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
             qa[ks][3] = qhi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16 + 8 + cq) : 0u;
           }
         }
-        if (cact && (k % cfL) == cfl) {
+        if (cact && (k % cfL) == cfl && !diag_nocompute) {
           const uint32_t k_u32 = smem_u32(smem_raw + (size_t)s * stage_bytes);
           for (int t0 = 0; t0 < c; t0 += TPW)
             wa.template chunk<false>(qa, k_u32, k_u32 + (uint32_t)tile_bytes, t0, c, scale_log2, lane);
@@ -552,19 +626,31 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
               }
             }
           }
-          __threadfence();  // every writer's partial rows visible GPU-wide ...
+          // counted now (one fence per job, early in the CTA): the seq-first
+          // segments, counted at their CTAs' ends, are then the last
+          // contributors and the merges spread over the seq-first CTAs
           named_sync_consumers();
-          if (ct == 0) st_release_gpu(cf_flags + (size_t)tile * h + head, tag);  // ... before the flag
+          if (ct < crows) {
+            fence_acq_rel_gpu();
+            const int row = crow0 + ct, item = row * h + head;
+            const uint32_t expect =
+                (uint32_t)(t.sf_item[(size_t)item * kSfItemInts + 1] + t.mg_ptr[row + 1] - t.mg_ptr[row]);
+            if (atomicAdd(cnt + item, (uint32_t)cfL) + (uint32_t)cfL == expect) {
+              fence_acq_rel_gpu();
+              push_pending(S, item);
+            }
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty_bar[s]);
+        if (tr && ct == 0 && jj < kTraceUnits) tr[5 + 4 * jj] = globaltimer_ns();
       }
       wa.reset();
     }
     for (int u = u0; u < u1; ++u, ++jj) {
       const int s = jj % nst;
       mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
-      if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 3 * jj] = globaltimer_ns();
+      if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 4 * jj] = globaltimer_ns();
       const StageMeta md = S.meta[s];
       const unsigned char* st = smem_raw + (size_t)s * stage_bytes;
       if (md.flags & F_FIRST) {
@@ -579,7 +665,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
           }
         }
       }
-      if (cw < L && cw * TPW < md.nt) {
+      if (cw < L && cw * TPW < md.nt && !diag_nocompute) {
         const uint32_t k_u32 = smem_u32(st);
         wa.template chunk<true>(qa, k_u32, k_u32 + (uint32_t)tile_bytes, cw * TPW, md.nt, scale_log2, lane);
       }
@@ -595,13 +681,13 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
             *reinterpret_cast<float2*>(&S.o[cw][i * 8 + lane * 2]) = make_float2(wa.o[i][0], wa.o[i][1]);
         }
         named_sync_consumers();
-        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, segflags, tag, cf_flags, out,
+        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, cnt, out,
                                t, h, ct);
         named_sync_consumers();  // S.o / stage reuse
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty_bar[s]);
-      if (tr && ct == 0 && jj < kTraceUnits) tr[5 + 3 * jj] = globaltimer_ns();
+      if (tr && ct == 0 && jj < kTraceUnits) tr[5 + 4 * jj] = globaltimer_ns();
     }
   } else {
     const int g = ct / G::kTpt, j = ct % G::kTpt;
@@ -610,7 +696,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     for (int u = u0; u < u1; ++u, ++jj) {
       const int s = jj % nst;
       mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
-      if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 3 * jj] = globaltimer_ns();
+      if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 4 * jj] = globaltimer_ns();
       const StageMeta md = S.meta[s];
       const unsigned char* st = smem_raw + (size_t)s * stage_bytes;
       if (md.flags & F_FIRST) {
@@ -636,17 +722,18 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
 #pragma unroll
         for (int v = 0; v < G::kVec; ++v) S.o[g][j * G::kVec + v] = o[v];
         named_sync_consumers();
-        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, segflags, tag, cf_flags, out,
+        sf_finalize<TO, D, NG>(S, md, stage_partials<T, D>(st, tile_bytes), pO, segO, cnt, out,
                                t, h, ct);
         named_sync_consumers();
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty_bar[s]);
-      if (tr && ct == 0 && jj < kTraceUnits) tr[5 + 3 * jj] = globaltimer_ns();
+      if (tr && ct == 0 && jj < kTraceUnits) tr[5 + 4 * jj] = globaltimer_ns();
     }
   }
   (void)cw;
-  sf_fixup<TO, D, NG>(S, pO, segO, segflags, tag, cf_flags, out, t, h, ct);
+  settle_contributions(S, cnt, t, h, ct);
+  merge_pending<TO, D, NG>(S, pO, segO, cnt, out, t, h, ct);
   if (tr && ct == 0) tr[2] = globaltimer_ns();
 }
 
@@ -731,12 +818,7 @@ __global__ void __launch_bounds__(128) cf_simt_kernel(const T* __restrict__ kpoo
   pdl_wait();  // PDL chain: complete only after the append (see chunk_first.cu)
 }
 
-cudaError_t set_smem(const void* kern, size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  return e;
-}
+cudaError_t set_smem(const void* kern, size_t smem) { return set_smem_once(kern, smem); }
 
 template <typename T, typename TO, int D, bool MMA, int TPW>
 cudaError_t launch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
@@ -753,10 +835,10 @@ cudaError_t launch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) 
   const T* kp = (const T*)p.k + (size_t)a.layer * p.layer_stride;
   const T* vp = (const T*)p.v + (size_t)a.layer * p.layer_stride;
   return launch_ex(kern, dim3(t.n_sf_ctas), dim3(kSfThreads), smem, st, a.use_pdl, kp, vp, (const T*)a.q,
-                   (TO*)a.out, a.pO, a.segO, a.segflags, a.tag, a.cf_flags, t, (int32_t)p.h, (int32_t)p.c,
+                   (TO*)a.out, a.pO, a.segO, a.counters, t, (int32_t)p.h, (int32_t)p.c,
                    a.scale_log2,
                    (int32_t)nst, (uint32_t)stage, a.trace_cf ? (uint64_t*)nullptr : a.trace,
-                   (int32_t)std::min(a.sf_prefetch, 31));
+                   (int32_t)(std::min(a.sf_prefetch & 255, 31) | (a.sf_prefetch & 256)));
 }
 
 template <typename T, int D>

@@ -14,9 +14,9 @@ from tests.gpu_workload import Harness, build_shared, decode_tokens
 pytestmark = pytest.mark.gpu
 
 TOL = {("f32", "f32"): 1e-5, ("f16", "f16"): 2e-3, ("bf16", "f32"): 2e-3, ("f16", "f32"): 2e-3}
-# opt-in kernel variants exercised beside the default path: the fused
-# single-kernel phase pair, and the 4-warp chunk-first CTA (PDL co-residency)
-VARIANTS = ["", "fused=1", "cf_small=1"]
+# kernel variants exercised beside the default (fused single-kernel) path: the
+# two-kernel phase pair, and its 4-warp chunk-first CTA (PDL co-residency)
+VARIANTS = ["", "fused=0", "fused=0,cf_small=1"]
 
 
 # --------------------------------------------------------------- config 1 ---

@@ -21,7 +21,7 @@ import torch  # noqa: E402
 
 from bench import DecodeWorkload, flush_l2, time_steps  # noqa: E402
 
-TRACE_STRIDE, TRACE_CTAS, TRACE_UNITS = 128, 2048, 41
+TRACE_STRIDE, TRACE_CTAS, TRACE_UNITS = 128, 2048, 31
 
 
 def summarise(tr, name, ncta):
@@ -32,11 +32,23 @@ def summarise(tr, name, ncta):
     starts = (t[:, 0] - t0) / 1e3
     print(f"   CTA start offset us: min {starts.min():.2f} med {np.median(starts):.2f} max {starts.max():.2f}")
     print(f"   CTA active us: med {np.median((ends - t[:, 0]) / 1e3):.2f} max {((ends - t[:, 0]) / 1e3).max():.2f}")
+    eo = (ends - t0) / 1e3
+    print(f"   CTA end offset us: p10 {np.percentile(eo, 10):.2f} med {np.median(eo):.2f} "
+          f"p90 {np.percentile(eo, 90):.2f} max {eo.max():.2f}")
+    tails = []
+    for c in range(ncta):
+        d = t[c, 5::4][:TRACE_UNITS]
+        d = d[d > 0]
+        if d.size:
+            tails.append((ends[c] - d.max()) / 1e3)
+    if tails:
+        print(f"   tail after last traced unit us (finalize/fixup): med {np.median(tails):.2f} "
+              f"p90 {np.percentile(tails, 90):.2f} max {max(tails):.2f}")
     lat, gap, first, comp, waitc = [], [], [], [], []
     for c in range(ncta):
-        issue = t[c, 3::3][:TRACE_UNITS]
-        ready = t[c, 4::3][:TRACE_UNITS]
-        done = t[c, 5::3][:TRACE_UNITS]
+        issue = t[c, 3::4][:TRACE_UNITS]
+        ready = t[c, 4::4][:TRACE_UNITS]
+        done = t[c, 5::4][:TRACE_UNITS]
         ok = (issue > 0) & (ready > 0) & (done > 0)
         if not ok.any():
             continue
@@ -50,11 +62,24 @@ def summarise(tr, name, ncta):
                 gap.append((ready[u] - ready[prev_u]) / 1e3)
             prev_done, prev_u = done[u], u
     q = lambda v: f"p10 {np.percentile(v, 10):.2f} med {np.median(v):.2f} p90 {np.percentile(v, 90):.2f} mean {np.mean(v):.2f}" if v else "-"
+    fi = [(t[c, 3] - t[c, 0]) / 1e3 for c in range(ncta) if t[c, 3] > 0]
+    print(f"   first issue after entry us: {q(fi)}")
     print(f"   first data after entry us: {q(first)}")
     print(f"   load latency (ready - issue) us: {q(lat)}")
     print(f"   consume time (done - ready) us: {q(comp)}")
     print(f"   consumer idle before unit (ready - prev done) us: {q(waitc)}")
     print(f"   gap between consecutive traced ready us: {q(gap)}")
+    # aggregate data arrival rate over the kernel (bytes of each unit at its ready time)
+    rd = t[:, 4:4 + 4 * TRACE_UNITS:4].ravel()
+    by = t[:, 6:6 + 4 * TRACE_UNITS:4].ravel()
+    ok = (rd > 0) & (by > 0)
+    if ok.any():
+        rel = (rd[ok] - t0) / 1e3
+        span = (ends.max() - t0) / 1e3
+        bins = np.arange(0, span + 2, 2.0)
+        hist, _ = np.histogram(rel, bins=bins, weights=by[ok].astype(np.float64))
+        print(f"   traced bytes {by[ok].sum() / 1e6:.1f} MB; arrival TB/s per 2 us bin:")
+        print("   " + " ".join(f"{h / 2e-6 / 1e12:.1f}" for h in hist))
 
 
 def main():
@@ -62,6 +87,8 @@ def main():
     ap.add_argument("--step", type=int, default=400)
     ap.add_argument("--opt", action="append", default=[])
     ap.add_argument("--kernel", default="sf", choices=["sf", "cf"])
+    ap.add_argument("--flush", default="write", choices=["write", "clean"],
+                    help="clean: write then read the flush buffer (no dirty lines left in L2)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     wl = DecodeWorkload(dev, steps=args.step + 2)
@@ -80,6 +107,8 @@ def main():
     tr_t.zero_()
     with torch.cuda.stream(stream):
         flush_l2(flush)
+        if args.flush == "clean":
+            flush.sum()
         wl.step(args.step, stream.cuda_stream)
     stream.synchronize()
     tr = tr_t.view(TRACE_CTAS, TRACE_STRIDE).cpu().numpy()
