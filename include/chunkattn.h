@@ -167,13 +167,28 @@ chunkattn_status chunkattn_memory_stats(chunkattn_t h, int64_t out[6]);
  *           kernels launched, current epoch, partial slots of the context}. */
 chunkattn_status chunkattn_counters(chunkattn_t h, int64_t out[6]);
 
-/* Tuning / test knobs (host-side scheduling only; any setting gives the same
- * result within rounding, and a fixed setting is bitwise reproducible):
+/* Tuning / test knobs (scheduling only; any setting gives the same result
+ * within rounding, and a fixed setting is bitwise reproducible).  Unknown keys
+ * fail with CA_EINVAL.
+ *   "fused"            1 (default) = both phases in one persistent launch
+ *                      (chunk-first units first in each CTA, last-contributor
+ *                      merges); 0 = chunk-first kernel + seq-first kernel
+ *   "cf_unit_cost"     fused balance: a chunk-first unit's weight in tenths of
+ *                      a seq-first unit (default 16)
  *   "cf_splits"        0 = auto, else force chunks-per-split of chunk-first tiles
  *   "cf_target_ctas"   chunk-first CTA target for the auto split rule
- *   "cf_simt"          1 = force the SIMT chunk-first kernel (no tensor cores)
- *   "pdl"              1 (default) = programmatic dependent launch of seq-first
- *   "kernel_events"    1 = time every kernel launch (chunkattn_kernel_times) */
+ *   "cf_simt"          1 = force the SIMT chunk-first kernel (no tensor cores;
+ *                      implies fused = 0)
+ *   "sf_simt"          1 = SIMT seq-first consumers (implies fused = 0)
+ *   "cf_small"         1 = 4-warp chunk-first CTA when tiles have <= 64 rows
+ *                      (two-kernel path; default 0)
+ *   "sf_ctas"          persistent grid size (default 296 = 2 per SM)
+ *   "sf_ctas_per_sm"   1 or 2: shared-memory budget per seq-first CTA
+ *   "sf_prefetch"      L2 bulk-prefetch distance in units (default 0 = off)
+ *   "pdl"              1 (default) = programmatic dependent launch after the append
+ *   "kernel_events"    1 = time every kernel launch (chunkattn_kernel_times)
+ *   "trace"            debug timeline in the workspace tail (1 seq-first, 2 chunk-first)
+ *   "diag_nocompute"   DIAGNOSTIC ONLY, outputs are wrong: consumers skip the math */
 chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t value);
 
 /* Per-kernel device time, measured with CUDA events recorded on the launch

@@ -290,11 +290,14 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
         int32_t* d = &sf_unit[(size_t)kSfUnitInts * u];
         const int32_t item = d[1], left = d[3] - d[2];
         const int32_t* rec = &sf_item[kSfItemInts * item];
-        const int32_t seg = rec[0] < 0 ? -1 : rec[0] + ord[item]++;
+        const int32_t o = ord[item]++;
+        const int32_t seg = rec[0] < 0 ? -1 : rec[0] + o;
+        // the CTA holding the item's last segment is its merger (kSfMerger bit)
+        const int32_t word = rec[1] | (rec[0] >= 0 && o == rec[1] - 1 ? kSfMerger : 0);
         const int64_t end = std::min<int64_t>(u + left, ubound[g + 1]);
         for (int64_t v = u; v < end; ++v) {
           sf_unit[(size_t)kSfUnitInts * v + 6] = seg;
-          sf_unit[(size_t)kSfUnitInts * v + 7] = rec[1];
+          sf_unit[(size_t)kSfUnitInts * v + 7] = word;
         }
         u += left;
       }
@@ -304,18 +307,14 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
     *err = "segment partials exceed workspace capacity";
     return false;
   }
-  // merges a CTA may owe at its end: items it touches that have slots, plus
-  // (fused) the rows of its chunk-first jobs
+  // merges a CTA may owe at its end / segment contributions it records: at
+  // most the items it touches that have slots
   for (int64_t g = 0; g < G; ++g) {
     int64_t owed = 0;
     for (int64_t u = ubound[g]; u < ubound[g + 1];) {
       const int32_t* d = &sf_unit[(size_t)kSfUnitInts * u];
       owed += sf_item[kSfItemInts * d[1]] >= 0 ? 1 : 0;
       u += d[3] - d[2];
-    }
-    for (int32_t cu = cf_range[2 * g]; cu < cf_range[2 * g + 1]; ++cu) {
-      const int32_t* d = &cf_unit[(size_t)kCfUnitInts * cu];
-      if (d[3] & 1) owed += cf_tile[kCfTileInts * d[1] + CF_ROW1] - cf_tile[kCfTileInts * d[1] + CF_ROW0];
     }
     if (owed > kMaxPendingMerges) {
       if (X.fused) {  // too many merges for one CTA: run the two-kernel schedule instead

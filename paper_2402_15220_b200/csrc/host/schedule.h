@@ -42,8 +42,10 @@ constexpr int kMaxPendingMerges = 256;
 // the producer issues its copies after one load: {chunk id or -1 (row without
 // private chunks), item, chunk index k in the item, units of the item, merge
 // list [mg0, mg1) of the row, segment slot of this CTA's part of the item (-1:
-// finished in place), segments of the item}.
+// finished in place), segments of the item | kSfMerger on the merger's units}.
 constexpr int kSfUnitInts = 8;
+// bit of the {nsegs} word: this CTA's segment is the item's last -- its merger
+constexpr int kSfMerger = 1 << 30;
 
 struct ScheduleOptions {
   int32_t share_threshold = 2;

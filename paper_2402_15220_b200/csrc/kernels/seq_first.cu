@@ -331,31 +331,19 @@ CA_DEV void record_contribution(SfShared<D, NG>& S, int item, int w) {
 #endif
 }
 
-// CTA end: one warp counts the CTA's contributions.  The CTA barrier orders
-// every writer's partial rows before the warp's release fence (cumulative);
-// the add that completes an item's count (expected = its segments + its
-// chunk-first lane rows when those come from this launch) queues its merge
-// after an acquire fence.  Counters return to 0 when merged.
+// CTA end: one warp counts the CTA's recorded contributions (segments of items
+// merged elsewhere).  The CTA barrier orders every writer's partial rows
+// before the warp's release fence (cumulative); the adds are relaxed.
 template <int D, int NG>
-CA_DEV void settle_contributions(SfShared<D, NG>& S, uint32_t* __restrict__ cnt, const DevTables& t, int h,
-                                 int ct) {
+CA_DEV void settle_contributions(SfShared<D, NG>& S, uint32_t* __restrict__ cnt, int ct) {
   named_sync_consumers();
   const int n = min(S.n_contrib, kMaxPend);
   if (ct < 32 && n > 0) {
     fence_acq_rel_gpu();
-    bool any_last = false;
     for (int i = ct; i < n; i += 32) {
       const int2 c = S.contrib[i];
-      const int row = c.x / h;
-      const uint32_t expect = (uint32_t)(t.sf_item[(size_t)c.x * kSfItemInts + 1] +
-                                         (t.fused ? t.mg_ptr[row + 1] - t.mg_ptr[row] : 0));
-      const uint32_t old = atomicAdd(cnt + c.x, (uint32_t)c.y);
-      if (old + (uint32_t)c.y == expect) {
-        any_last = true;
-        push_pending(S, c.x);
-      }
+      atomicAdd(cnt + c.x, (uint32_t)c.y);
     }
-    if (__any_sync(0xffffffffu, any_last)) fence_acq_rel_gpu();
   }
 }
 
@@ -424,14 +412,24 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
       srow[D + 1] = an;
     }
   }
-  if (ct == 0) record_contribution(S, md.item, 1);
+  if (ct == 0) {
+    if (md.nsegs & kSfMerger)
+      push_pending(S, md.item);  // this CTA merges the item at its end
+    else
+      record_contribution(S, md.item, 1);
+  }
 }
 
-// The CTA's queued merges, one warp per item: contributions = the row's
-// chunk-first partials in merge-list order, then the item's segments in CTA
-// order (n-ary Eqn 2, fixed order).  Lane e holds contribution e's row and
-// (m, n): one round of loads for the max and the weights, one for the rows
-// (each lane 4 columns of every row).  Writes O / n, resets the counter.
+// The CTA's owed merges (items whose last segment it holds), one warp per
+// item, after all its own units: wait until the item's other contributions
+// are counted (chunk-first jobs of this launch when fused, the earlier
+// segments), then merge the row's chunk-first partials in merge-list order and
+// the item's segments in CTA order (n-ary Eqn 2, fixed order).  Lane e holds
+// contribution e's row and (m, n): one round of loads for the max and the
+// weights, one for the rows (each lane 4 columns of every row).  Writes O / n
+// and resets the counter.  Deadlock-free: chunk-first work never waits and
+// every CTA counts its own contributions before it waits; the grid is one
+// wave (2 CTAs per SM).
 template <typename TO, int D, int NG>
 CA_DEV void merge_pending(SfShared<D, NG>& S, const float* __restrict__ pO, const float* __restrict__ segO,
                           uint32_t* __restrict__ cnt, TO* __restrict__ out, const DevTables& t, int h, int ct) {
@@ -446,6 +444,9 @@ CA_DEV void merge_pending(SfShared<D, NG>& S, const float* __restrict__ pO, cons
     const int4 rec = *reinterpret_cast<const int4*>(t.sf_item + (size_t)item * kSfItemInts);
     const int E = ncf + rec.y;
     TO* orow = out + ((size_t)t.row_caller[row] * h + head) * D;
+    const uint32_t others = (uint32_t)((t.fused ? ncf : 0) + rec.y - 1);
+    if (others > 0) spin_flags_warp(cnt + item, lane == 0, others, item);
+    __syncwarp();
     if (E <= 32) {
       const float* pr = nullptr;
       float me = -INFINITY, ne = 0.f;
@@ -626,19 +627,12 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
               }
             }
           }
-          // counted now (one fence per job, early in the CTA): the seq-first
-          // segments, counted at their CTAs' ends, are then the last
-          // contributors and the merges spread over the seq-first CTAs
+          // counted now (one fence per job, early in the CTA): each row's
+          // merger (the CTA holding its item's last segment) waits for them
           named_sync_consumers();
           if (ct < crows) {
             fence_acq_rel_gpu();
-            const int row = crow0 + ct, item = row * h + head;
-            const uint32_t expect =
-                (uint32_t)(t.sf_item[(size_t)item * kSfItemInts + 1] + t.mg_ptr[row + 1] - t.mg_ptr[row]);
-            if (atomicAdd(cnt + item, (uint32_t)cfL) + (uint32_t)cfL == expect) {
-              fence_acq_rel_gpu();
-              push_pending(S, item);
-            }
+            atomicAdd(cnt + (crow0 + ct) * h + head, (uint32_t)cfL);
           }
         }
         __syncwarp();
@@ -732,7 +726,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     }
   }
   (void)cw;
-  settle_contributions(S, cnt, t, h, ct);
+  settle_contributions(S, cnt, ct);
   merge_pending<TO, D, NG>(S, pO, segO, cnt, out, t, h, ct);
   if (tr && ct == 0) tr[2] = globaltimer_ns();
 }
