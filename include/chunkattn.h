@@ -28,7 +28,10 @@
  *     library keeps one set of device tables and relies on stream order.
  *   - "device" pointers are CUDA device pointers valid on config.device;
  *     "host" pointers are plain host memory.  Device inputs must stay valid
- *     until `stream` has passed the call (as with cudaMemcpyAsync).
+ *     until `stream` has passed the call (as with cudaMemcpyAsync).  The
+ *     per-step tensors of append_kv (k, v) and attend (q, out) may also be
+ *     PINNED host memory (cudaHostAlloc / page-locked, UVA): the kernels then
+ *     read and write them over PCIe directly (zero-copy; no staging copy).
  *   - Layouts are dense, row-major, element type config.dtype unless stated.
  *     h = num_heads, d = head_dim, c = chunk_size, L = num_layers.
  *   - Host-only mode: config.device = -1 builds the prefix tree and tables
@@ -150,6 +153,21 @@ chunkattn_status chunkattn_remove_sequence(chunkattn_t h, int64_t seq_id, int64_
  * Asynchronous on `stream` (cudaStream_t; NULL = legacy default stream). */
 chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const int64_t* seq_ids,
                                   const void* q, void* out, void* stream);
+
+/* One whole decode step from HOST buffers (append_kv of the step's new K/V,
+ * then attend of `layer`), with the host<->device copies inside the call:
+ *   in_host   host (pinned for asynchrony) packed [q | k_new | v_new]:
+ *             q [n][h][d] dtype, k_new and v_new [n][L][h][d] dtype, all in
+ *             seq_ids order (the layouts of attend / append_kv)
+ *   out_host  host [n][h][d] out_dtype (pinned for asynchrony)
+ *   staging   device scratch, 16-byte aligned, >= in bytes + out bytes
+ *             (caller-owned, as all device memory; must not be in use)
+ * Enqueues one H2D copy, the append, the attend and one D2H copy on `stream`;
+ * the output is in out_host once `stream` has passed the call.  Errors as
+ * append_kv / attend; CA_EINVAL if staging_bytes is too small. */
+chunkattn_status chunkattn_decode_step_host(chunkattn_t h, int32_t layer, int64_t n, const int64_t* seq_ids,
+                                            const int32_t* tokens, const void* in_host, void* out_host,
+                                            void* staging, size_t staging_bytes, void* stream);
 
 /* Sequence ids in batch-row order (DFS of the prefix tree). */
 chunkattn_status chunkattn_batch_order(chunkattn_t h, int64_t* seq_ids_out, int64_t cap,

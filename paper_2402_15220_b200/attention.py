@@ -152,6 +152,19 @@ class ChunkAttention:
         C.check(self.lib.chunkattn_attend(self._h, layer, n, _p64(ids), qp, op, self._stream()))
         return out
 
+    def decode_step_host(self, ids: np.ndarray, toks: np.ndarray, in_host: torch.Tensor, out_host: torch.Tensor,
+                         staging: torch.Tensor, layer: int = 0, stream_ptr: int | None = None) -> None:
+        """One decode step from host buffers (chunkattn_decode_step_host): in_host
+        packed [q | k_new | v_new] (pinned), out_host [n][h][d] (pinned), staging a
+        device scratch tensor.  Asynchronous on the stream."""
+        if in_host.is_cuda or out_host.is_cuda or not staging.is_cuda:
+            raise ValueError("in_host/out_host must be host tensors and staging a device tensor")
+        st = ctypes.c_void_p(stream_ptr) if stream_ptr is not None else self._stream()
+        C.check(self.lib.chunkattn_decode_step_host(
+            self._h, layer, len(ids), _p64(ids), _p32(toks), ctypes.c_void_p(in_host.data_ptr()),
+            ctypes.c_void_p(out_host.data_ptr()), ctypes.c_void_p(staging.data_ptr()),
+            staging.numel() * staging.element_size(), st))
+
     def attend_raw(self, layer: int, ids: np.ndarray, q_ptr: int, out_ptr: int, stream_ptr: int) -> None:
         """Pre-marshalled attend for timing loops (ids int64 contiguous)."""
         C.check(self.lib.chunkattn_attend(self._h, layer, len(ids), _p64(ids), ctypes.c_void_p(q_ptr),

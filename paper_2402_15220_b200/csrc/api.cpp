@@ -557,6 +557,38 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   CA_GUARD_END
 }
 
+chunkattn_status chunkattn_decode_step_host(chunkattn_t h, int32_t layer, int64_t n, const int64_t* seq_ids,
+                                            const int32_t* tokens, const void* in_host, void* out_host,
+                                            void* staging, size_t staging_bytes, void* stream) {
+  CA_GUARD_BEGIN
+  if (!h || n < 0 || (n > 0 && (!seq_ids || !tokens))) return fail(CA_EINVAL, "bad argument");
+  if (h->host_only) return fail(CA_EINVAL, "host-only handle");
+  if (h->failed) return fail(CA_ECUDA, "handle failed on an earlier CUDA error");
+  if (n == 0) return CA_OK;
+  if (!in_host || !out_host || !staging) return fail(CA_EINVAL, "null buffer");
+  if ((uintptr_t)staging & 15) return fail(CA_EINVAL, "staging must be 16-byte aligned");
+  const size_t E = dtype_bytes(h->cfg.dtype);
+  const size_t q_bytes = (size_t)n * h->cfg.num_heads * h->cfg.head_dim * E;
+  const size_t kv_bytes = q_bytes * (size_t)h->cfg.num_layers;
+  const size_t in_bytes = q_bytes + 2 * kv_bytes;
+  const size_t out_off = (in_bytes + 15) / 16 * 16;
+  const size_t out_bytes = (size_t)n * h->cfg.num_heads * h->cfg.head_dim * dtype_bytes(h->cfg.out_dtype);
+  if (staging_bytes < out_off + out_bytes) return fail(CA_EINVAL, "staging buffer too small");
+  if (h->set_device() != CA_OK) return CA_ECUDA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* dev = static_cast<char*>(staging);
+  cudaError_t e = cudaMemcpyAsync(dev, in_host, in_bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return h->cuda_fail(e, "decode_step_host H2D");
+  chunkattn_status s = chunkattn_append_kv(h, n, seq_ids, tokens, dev + q_bytes, dev + q_bytes + kv_bytes, stream);
+  if (s != CA_OK) return s;
+  s = chunkattn_attend(h, layer, n, seq_ids, dev, dev + out_off, stream);
+  if (s != CA_OK) return s;
+  e = cudaMemcpyAsync(out_host, dev + out_off, out_bytes, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return h->cuda_fail(e, "decode_step_host D2H");
+  return CA_OK;
+  CA_GUARD_END
+}
+
 chunkattn_status chunkattn_batch_order(chunkattn_t h, int64_t* ids, int64_t cap, int64_t* n) {
   CA_GUARD_BEGIN
   if (!h || !n || (cap > 0 && !ids)) return fail(CA_EINVAL, "bad argument");

@@ -332,3 +332,82 @@ def test_head_sharded_handles_match_single_gpu():
     ref = full.ca.attend(ids, q64.to(full.dev, full.dt).contiguous())
     parts = [hs.ca.attend(ids, q64[:, i * 4:(i + 1) * 4].to(hs.dev, hs.dt).contiguous()) for i, hs in enumerate(halves)]
     assert float((torch.cat(parts, dim=1).double() - ref.double()).abs().max()) <= 1e-3
+
+
+def test_host_buffers_zero_copy_match_device():
+    """The C ABI takes pinned host q / k / v / out (UVA): the kernels read and
+    write them over PCIe; results are bitwise those of device buffers."""
+    import numpy as _np
+    outs = []
+    for host in (False, True):
+        hs = Harness(4, 128, 64, "f16", "f16", seed=23, alpha=8.0)
+        ids = build_shared(hs, 256, [0, 3, 70, 130, 5])
+        n = len(ids)
+        ida = _np.asarray(ids, dtype=_np.int64)
+        stream = torch.cuda.current_stream().cuda_stream
+        res = []
+        for st in range(3):
+            hs.step = st + 1
+            toks = decode_tokens(hs, ids)
+            pos = [len(hs.seqs[s]) for s in ids]
+            k, v = hs.kv(toks, pos)
+            for s, t in zip(ids, toks):
+                hs.seqs[s].append(int(t))
+            q = hs.queries(ids).to(torch.float16)
+            k, v = k.to(torch.float16).contiguous(), v.to(torch.float16).contiguous()
+            if host:
+                k, v, q = k.cpu().pin_memory(), v.cpu().pin_memory(), q.cpu().pin_memory()
+                out = torch.empty((n, 4, 128), dtype=torch.float16).pin_memory()
+            else:
+                k, v, q = k.cuda(), v.cuda(), q.cuda()
+                out = torch.empty((n, 4, 128), dtype=torch.float16, device="cuda")
+            hs.ca.append_raw(ida, _np.asarray(toks, dtype=_np.int32), k.data_ptr(), v.data_ptr(), stream)
+            hs.ca.attend_raw(0, ida, q.data_ptr(), out.data_ptr(), stream)
+            torch.cuda.synchronize()
+            res.append(out.cpu().clone())
+        outs.append(torch.stack(res))
+        ref = hs.oracle(ids, hs.queries(ids))
+        assert float(_np.abs(outs[-1][-1].double().numpy() - ref).max()) <= 2e-3
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_decode_step_host_matches_device_path():
+    """chunkattn_decode_step_host (host buffers, copies inside the call) gives
+    bitwise the outputs of append_kv + attend on device buffers."""
+    import numpy as _np
+    outs = []
+    for via_host in (False, True):
+        hs = Harness(4, 128, 64, "f16", "f16", seed=29, alpha=8.0)
+        ids = build_shared(hs, 192, [1, 64, 0, 90])
+        n = len(ids)
+        ida = _np.asarray(ids, dtype=_np.int64)
+        staging = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+        res = []
+        for st in range(3):
+            hs.step = st + 1
+            toks = decode_tokens(hs, ids)
+            pos = [len(hs.seqs[s]) for s in ids]
+            k, v = hs.kv(toks, pos)
+            for s, t in zip(ids, toks):
+                hs.seqs[s].append(int(t))
+            q = hs.queries(ids).to(torch.float16)
+            k, v = k.to(torch.float16).cpu(), v.to(torch.float16).cpu()
+            if via_host:
+                packed = torch.cat([q.reshape(-1), k.reshape(-1), v.reshape(-1)]).pin_memory()
+                out = torch.empty((n, 4, 128), dtype=torch.float16).pin_memory()
+                hs.ca.decode_step_host(ida, _np.asarray(toks, dtype=_np.int32), packed, out, staging)
+            else:
+                out = torch.empty((n, 4, 128), dtype=torch.float16, device="cuda")
+                stream = torch.cuda.current_stream().cuda_stream
+                kd, vd, qd = k.cuda(), v.cuda(), q.cuda()
+                hs.ca.append_raw(ida, _np.asarray(toks, dtype=_np.int32), kd.data_ptr(), vd.data_ptr(), stream)
+                hs.ca.attend_raw(0, ida, qd.data_ptr(), out.data_ptr(), stream)
+            torch.cuda.synchronize()
+            res.append(out.cpu().clone())
+        outs.append(torch.stack(res))
+        ref = hs.oracle(ids, hs.queries(ids))
+        assert float(_np.abs(outs[-1][-1].double().numpy() - ref).max()) <= 2e-3
+    assert torch.equal(outs[0], outs[1])
+    with pytest.raises(Exception):  # staging too small
+        hs.ca.decode_step_host(ida, _np.zeros(len(ids), dtype=_np.int32), torch.zeros(16).pin_memory(),
+                               torch.zeros(16).pin_memory(), torch.empty(16, dtype=torch.uint8, device="cuda"))
