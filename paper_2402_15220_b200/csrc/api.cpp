@@ -323,6 +323,8 @@ chunkattn_status chunkattn_create(const chunkattn_config* cfg, const chunkattn_b
   h->sopt.table_capacity = h->ws.table_cap;
   h->sopt.seg_capacity = h->ws.seg_cap;
   h->sopt.cf_target_ctas = 148;
+  h->sopt.head_dim = cfg->head_dim;
+  h->sopt.elem_bytes = (int32_t)dtype_bytes(cfg->dtype);
   if (!h->host_only) {
     if (!buf || !buf->k_pool || !buf->v_pool || !buf->workspace) {
       delete h;
@@ -656,6 +658,8 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->fused_opt = value != 0;
   } else if (k == "cf_unit_cost") {
     h->sopt.cf_unit_cost = value < 1 ? 0.1 : (double)value / 10.0;  // tenths of a seq-first unit
+  } else if (k == "cf_lane_merge") {
+    h->sopt.cf_lane_merge = value != 0;
   } else if (k == "cf_small") {
     h->cf_small = value != 0;
   } else if (k == "diag_nocompute") {

@@ -96,13 +96,22 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   for (const Run& r : runs) max_n = std::max<int64_t>(max_n, (int64_t)r.chunks.size());
   const int64_t tile_rows = opt.fused ? kFusedTileRows : kMaxCfTileRows;
   auto lanes_of = [&](const RunTiling& t) { return opt.fused ? fused_lanes(t.rows_per_tile) : 1; };
+  // partials per row: the fused kernel merges its L lanes in the stage's K/V
+  // tiles when the (4 - G) foreign lane states fit there
+  auto parts_of = [&](const RunTiling& t) {
+    const int32_t L = lanes_of(t);
+    if (L == 1 || !opt.cf_lane_merge) return L;
+    const int64_t G = 4 / L;
+    const int64_t scratch = (4 - G) * (opt.head_dim / 2 + 4) * 32 * 4;
+    return scratch <= 2LL * c * opt.head_dim * opt.elem_bytes ? 1 : L;
+  };
   auto count = [&](int64_t cpt, int64_t* tiles, int64_t* slots) {
     *tiles = 0;
     *slots = 0;
     for (const Run& r : runs) {
       RunTiling t = tile_run(r, cpt, tile_rows);
       *tiles += t.splits * t.row_tiles;
-      *slots += t.splits * (r.j - r.i + 1) * lanes_of(t);
+      *slots += t.splits * (r.j - r.i + 1) * parts_of(t);
     }
   };
   int64_t cpt = max_n, tiles = 0, slots = 0;
@@ -140,7 +149,7 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   std::vector<int32_t> mg_cnt(b + 1, 0);
   for (const Run& r : runs) {
     RunTiling t = tile_run(r, cpt, tile_rows);
-    for (int32_t row = r.i; row <= r.j; ++row) mg_cnt[row + 1] += (int32_t)(t.splits * lanes_of(t));
+    for (int32_t row = r.i; row <= r.j; ++row) mg_cnt[row + 1] += (int32_t)(t.splits * parts_of(t));
   }
   std::vector<int32_t> mg_ptr(b + 1, 0);
   for (int32_t r = 0; r < b; ++r) mg_ptr[r + 1] = mg_ptr[r] + mg_cnt[r + 1];
@@ -151,7 +160,7 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   for (size_t ri = 0; ri < runs.size(); ++ri) {
     const Run& r = runs[ri];
     RunTiling t = tile_run(r, cpt, tile_rows);
-    const int32_t L = lanes_of(t);
+    const int32_t L = lanes_of(t), P = parts_of(t);
     const int64_t n = (int64_t)r.chunks.size();
     for (int64_t s = 0; s < t.splits; ++s) {
       const int64_t k0 = s * n / t.splits, k1 = (s + 1) * n / t.splits;  // balanced split
@@ -161,13 +170,13 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
         const int32_t r0 = r.i + (int32_t)(rt * t.rows_per_tile);
         const int32_t r1 = std::min<int32_t>(r.j + 1, r0 + (int32_t)t.rows_per_tile);
         const int32_t tile_id = (int32_t)(cf_tile.size() / kCfTileInts);
-        cf_tile.insert(cf_tile.end(), {off, (int32_t)(k1 - k0), r0, r1, (int32_t)slot, (int32_t)ri, L, 0});
+        cf_tile.insert(cf_tile.end(), {off, (int32_t)(k1 - k0), r0, r1, (int32_t)slot, (int32_t)ri, L, P});
         for (int32_t row = r0; row < r1; ++row)
-          for (int32_t l = 0; l < L; ++l) {  // lane partials in lane order (fixed merge order, A12)
+          for (int32_t l = 0; l < P; ++l) {  // lane partials in lane order (fixed merge order, A12)
             mg_tile[mg_fill[row]] = tile_id;
             mg_slot[mg_fill[row]++] = (int32_t)(slot + (int64_t)l * (r1 - r0) + (row - r0));
           }
-        slot += (int64_t)(r1 - r0) * L;
+        slot += (int64_t)(r1 - r0) * P;
         max_rows = std::max(max_rows, r1 - r0);
       }
     }

@@ -16,10 +16,12 @@
 namespace pakv {
 
 // Chunk-first tile record in the blob (kCfTileInts int32 each).
-// CF_LANES: number of token-lane partials per row (1 when the chunk-first CTA
-// merges its lanes itself; L = 4 / row groups in the fused kernel, which writes
-// one partial per lane: slot = CF_SLOT + lane * rows + (row - CF_ROW0)).
-enum CfTileField { CF_CHUNK_OFF = 0, CF_NCHUNK, CF_ROW0, CF_ROW1, CF_SLOT, CF_RUN, CF_LANES, CF_PAD1 };
+// CF_LANES: token lanes of the tile (1 in the two-kernel chunk-first CTA,
+// which merges its lanes itself; L = 4 / row groups in the fused kernel).
+// CF_PARTS: partials written per row: 1 when the fused kernel merges its lanes
+// in the stage's shared memory (fits when (4 - G) lane states fit the K/V
+// tiles), else L (slot = CF_SLOT + lane * rows + (row - CF_ROW0)).
+enum CfTileField { CF_CHUNK_OFF = 0, CF_NCHUNK, CF_ROW0, CF_ROW1, CF_SLOT, CF_RUN, CF_LANES, CF_PARTS };
 constexpr int kCfTileInts = 8;
 constexpr int kMaxCfTileRows = 128;  // rows of one chunk-first tile (8 warps x 16 rows)
 constexpr int kFusedTileRows = 64;   // fused kernel: 4 consumer warps x 16 rows
@@ -55,6 +57,9 @@ struct ScheduleOptions {
   int64_t sf_ctas = 296;           // persistent seq-first grid (<= kMaxSfCtas)
   bool fused = false;              // chunk-first units run inside the persistent seq-first kernel
   double cf_unit_cost = 1.6;       // fused balance: cost of a chunk-first unit in seq-first units (swept on cfg2)
+  int32_t head_dim = 128;          // fused lane merge: scratch bytes vs the stage's K/V tiles
+  int32_t elem_bytes = 2;
+  bool cf_lane_merge = true;       // fused: merge token lanes in shared memory (one partial per row)
   int64_t slot_capacity = 0;       // partial slots available in the workspace
   int64_t table_capacity = 0;      // int32 entries available for the blob
   int64_t seg_capacity = 0;        // seq-first segment partial rows available

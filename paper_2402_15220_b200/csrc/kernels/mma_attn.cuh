@@ -8,7 +8,7 @@
 // ldmatrix of 8 consecutive tokens is bank-conflict free.
 //
 // mma.sync.m16n8k16 (fp32 accumulate):  S = Q K^T over the warp's token slice
-// [tok0, tok0 + TPW), online softmax in log2 units (P rounded to the input
+// [tok0, tok0 + NTOK), online softmax in log2 units (P rounded to the input
 // type, row sum n from the rounded P: reading A11), O = O * corr + P V.
 #pragma once
 
@@ -25,7 +25,6 @@ CA_DEV uint32_t tile_off(int row, int col) {  // byte offset of (token, element)
 template <typename T, int D, int TPW>
 struct WarpAttn {
   static constexpr int KS = D / 16;   // k-steps over d
-  static constexpr int NT = TPW / 8;  // n-tiles of S
   static constexpr int DT = D / 8;    // n-tiles of O
   float o[DT][4];
   float m_lo, m_hi, n_lo, n_hi;
@@ -37,10 +36,13 @@ struct WarpAttn {
     n_lo = n_hi = 0.f;
   }
 
-  // Tokens [tok0, tok0 + TPW) of the tile; tokens >= nvalid are masked (MASK).
-  template <bool MASK>
+  // Tokens [tok0, tok0 + NTOK) of the tile; tokens >= nvalid are masked (MASK).
+  // NTOK > 16 gives the mma chains NTOK / 8 independent accumulators (the
+  // chunk-first phase is latency-bound at 16 tokens per call).
+  template <bool MASK, int NTOK = TPW>
   CA_DEV void chunk(const uint32_t (&qa)[KS][4], uint32_t k_u32, uint32_t v_u32, int tok0, int nvalid,
                     float scale_log2, int lane) {
+    constexpr int NT = NTOK / 8;
     const int mi = lane >> 3, r8 = lane & 7;
     float sc[NT][4];
 #pragma unroll
@@ -103,7 +105,7 @@ struct WarpAttn {
       o[i][3] *= c_hi;
     }
 #pragma unroll
-    for (int kk = 0; kk < TPW / 16; ++kk) {
+    for (int kk = 0; kk < NTOK / 16; ++kk) {
       const uint32_t a[4] = {pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1]};
       // masked tokens: P = 0 there, and their V rows (stale shared memory, maybe
       // not finite) are zeroed in the B fragments so 0 * V cannot produce NaN.

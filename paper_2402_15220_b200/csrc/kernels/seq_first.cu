@@ -421,23 +421,28 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
 }
 
 // The CTA's owed merges (items whose last segment it holds), one warp per
-// item, after all its own units: wait until the item's other contributions
-// are counted (chunk-first jobs of this launch when fused, the earlier
-// segments), then merge the row's chunk-first partials in merge-list order and
-// the item's segments in CTA order (n-ary Eqn 2, fixed order).  Lane e holds
-// contribution e's row and (m, n): one round of loads for the max and the
-// weights, one for the rows (each lane 4 columns of every row).  Writes O / n
-// and resets the counter.  Deadlock-free: chunk-first work never waits and
-// every CTA counts its own contributions before it waits; the grid is one
-// wave (2 CTAs per SM).
+// item -- all five warps once the producer is done -- after all its own units:
+// wait until the item's other contributions are counted (chunk-first jobs of
+// this launch when fused, the earlier segments), then merge the row's
+// chunk-first partials in merge-list order and the item's segments in CTA
+// order (n-ary Eqn 2, fixed order).  Lane e holds contribution e's row
+// pointer (resolved before the wait) and (m, n); the (m, n) loads and the
+// first 8 rows (each lane 4 columns of every row) go out in one round.
+// Writes O / n and resets the counter.  Deadlock-free: chunk-first work never
+// waits and every CTA counts its own contributions before it waits; the grid
+// is one wave (2 CTAs per SM).
+constexpr int kMergeWarps = kProducerWarps + kConsumerWarps;
+CA_DEV void named_sync_all() { asm volatile("bar.sync 2, %0;" ::"n"(kMergeWarps * 32) : "memory"); }
+
 template <typename TO, int D, int NG>
 CA_DEV void merge_pending(SfShared<D, NG>& S, const float* __restrict__ pO, const float* __restrict__ segO,
-                          uint32_t* __restrict__ cnt, TO* __restrict__ out, const DevTables& t, int h, int ct) {
+                          uint32_t* __restrict__ cnt, TO* __restrict__ out, const DevTables& t, int h, int mt) {
   constexpr int PR = D + 4;
-  named_sync_consumers();
+  constexpr int RB = 8;  // rows per load round
+  named_sync_all();
   const int np = min(S.n_pend, kMaxPend);
-  const int lane = ct & 31;
-  for (int p = ct >> 5; p < np; p += kConsumerWarps) {
+  const int lane = mt & 31;
+  for (int p = mt >> 5; p < np; p += kMergeWarps) {
     const int item = S.pend[p];
     const int row = item / h, head = item % h;
     const int mg0 = t.mg_ptr[row], ncf = t.mg_ptr[row + 1] - mg0;
@@ -445,17 +450,32 @@ CA_DEV void merge_pending(SfShared<D, NG>& S, const float* __restrict__ pO, cons
     const int E = ncf + rec.y;
     TO* orow = out + ((size_t)t.row_caller[row] * h + head) * D;
     const uint32_t others = (uint32_t)((t.fused ? ncf : 0) + rec.y - 1);
+    const float* pr = nullptr;
+    if (E <= 32 && lane < E)
+      pr = lane < ncf ? pO + ((size_t)t.mg_slot[mg0 + lane] * h + head) * PR : segO + (size_t)(rec.x + lane - ncf) * PR;
     if (others > 0) spin_flags_warp(cnt + item, lane == 0, others, item);
     __syncwarp();
     if (E <= 32) {
-      const float* pr = nullptr;
+      const uint64_t pu = reinterpret_cast<uint64_t>(pr);
+      const bool colv = lane * 4 < D;
+      float4 v[RB];
       float me = -INFINITY, ne = 0.f;
+      auto load_rows = [&](int e0) {
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          const int e = e0 + r;
+          const uint64_t pe = (uint64_t)__shfl_sync(0xffffffffu, (uint32_t)pu, e & 31) |
+                              ((uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(pu >> 32), e & 31) << 32);
+          v[r] = (e < E && colv) ? __ldcg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(pe) + lane * 4))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
       if (lane < E) {
-        pr = lane < ncf ? pO + ((size_t)t.mg_slot[mg0 + lane] * h + head) * PR : segO + (size_t)(rec.x + lane - ncf) * PR;
         const float2 mn = __ldcg(reinterpret_cast<const float2*>(pr + D));
         me = mn.x;
         ne = mn.y;
       }
+      load_rows(0);
       float M = me;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
@@ -464,21 +484,18 @@ CA_DEV void merge_pending(SfShared<D, NG>& S, const float* __restrict__ pO, cons
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, off);
       float4 ao = make_float4(0.f, 0.f, 0.f, 0.f);
-      const uint64_t pu = reinterpret_cast<uint64_t>(pr);
-#pragma unroll 8
-      for (int e = 0; e < E; ++e) {
-        const float we = __shfl_sync(0xffffffffu, w, e);
-        const uint64_t pe = (uint64_t)__shfl_sync(0xffffffffu, (uint32_t)pu, e) |
-                            ((uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(pu >> 32), e) << 32);
-        if (lane * 4 < D) {
-          const float4 v = __ldcg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(pe) + lane * 4));
-          ao.x = fmaf(we, v.x, ao.x);
-          ao.y = fmaf(we, v.y, ao.y);
-          ao.z = fmaf(we, v.z, ao.z);
-          ao.w = fmaf(we, v.w, ao.w);
+      for (int e0 = 0; e0 < E; e0 += RB) {
+        if (e0 > 0) load_rows(e0);
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          const float we = __shfl_sync(0xffffffffu, w, (e0 + r) & 31);  // 0 past E
+          ao.x = fmaf(we, v[r].x, ao.x);
+          ao.y = fmaf(we, v[r].y, ao.y);
+          ao.z = fmaf(we, v[r].z, ao.z);
+          ao.w = fmaf(we, v[r].w, ao.w);
         }
       }
-      if (lane * 4 < D) {
+      if (colv) {
         Elem<TO>::store1(orow + lane * 4 + 0, ao.x / nsum);
         Elem<TO>::store1(orow + lane * 4 + 1, ao.y / nsum);
         Elem<TO>::store1(orow + lane * 4 + 2, ao.z / nsum);
@@ -491,14 +508,14 @@ CA_DEV void merge_pending(SfShared<D, NG>& S, const float* __restrict__ pO, cons
         for (int sg = 0; sg < rec.y; ++sg) M = fmaxf(M, __ldcg(segO + (size_t)(rec.x + sg) * PR + D));
         float4 ao = make_float4(0.f, 0.f, 0.f, 0.f);
         float an = 0.f;
-        auto add = [&](const float* pr) {
-          const float w = fast_exp2(__ldcg(pr + D) - M);
-          const float4 v = __ldcg(reinterpret_cast<const float4*>(pr + x));
+        auto add = [&](const float* prr) {
+          const float w = fast_exp2(__ldcg(prr + D) - M);
+          const float4 v = __ldcg(reinterpret_cast<const float4*>(prr + x));
           ao.x = fmaf(w, v.x, ao.x);
           ao.y = fmaf(w, v.y, ao.y);
           ao.z = fmaf(w, v.z, ao.z);
           ao.w = fmaf(w, v.w, ao.w);
-          an = fmaf(w, __ldcg(pr + D + 1), an);
+          an = fmaf(w, __ldcg(prr + D + 1), an);
         };
         for (int e = 0; e < ncf; ++e) add(pO + ((size_t)t.mg_slot[mg0 + e] * h + head) * PR);
         for (int sg = 0; sg < rec.y; ++sg) add(segO + (size_t)(rec.x + sg) * PR);
@@ -516,7 +533,7 @@ CA_DEV void merge_pending(SfShared<D, NG>& S, const float* __restrict__ pO, cons
 // tile (warp cw owns the token slice [cw TPW, (cw+1) TPW) of each chunk).
 // SIMT (fp32 and fallback): 8 groups x 16 threads own every 8th token.
 template <typename T, typename TO, int D, bool MMA, int TPW>
-__global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
+__global__ void __launch_bounds__(kSfThreads, 2) sf_persistent_kernel(
     const T* __restrict__ kpool, const T* __restrict__ vpool, const T* __restrict__ q, TO* __restrict__ out,
     float* __restrict__ pO, float* __restrict__ segO, uint32_t* __restrict__ cnt, DevTables t, int32_t h, int32_t c, float scale_log2, int32_t nst,
     uint32_t stage_bytes, uint64_t* __restrict__ trace, int32_t pf) {
@@ -553,6 +570,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     sf_produce<T, D, NG>(S, smem_raw, kpool, vpool, q, pO, t, h, c, nst, stage_bytes, u0, u1, lane, tr, pf, cf0,
                          cf1);
     if (tr && lane == 0) tr[1] = globaltimer_ns();
+    merge_pending<TO, D, NG>(S, pO, segO, cnt, out, t, h, kConsumerWarps * 32 + lane);  // fifth merge warp
     return;
   }
 
@@ -567,13 +585,13 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
     WA wa;
     wa.reset();
     // ---- fused chunk-first units (Alg 1): job = (tile, head); warp (g, l)
-    // owns rows [16 g, 16 g + 16) of the tile and the job's chunks k with
-    // k % L == l; at the job's end every lane writes its own partial rows and
-    // the job's readiness flag is released.
+    // owns rows [16 g, 16 g + 16) of the tile and lane l's token slice of
+    // the job's chunks; at the job's end every lane writes its own partial
+    // rows and the job's contribution is counted.
     {
       const int cf0 = t.fused ? t.sf_cta[blockIdx.x * kSfCtaInts + 2] : 0;
       const int cf1 = t.fused ? t.sf_cta[blockIdx.x * kSfCtaInts + 3] : 0;
-      int cfL = 1, cfg = 0, cfl = 0, crow0 = 0, crows = 0, cslot = 0;
+      int cfL = 1, cfP = 1, cfg = 0, cfl = 0, crow0 = 0, crows = 0, cslot = 0;
       bool cact = false;
       for (int u = cf0; u < cf1; ++u, ++jj) {
         const int s = jj % nst;
@@ -587,6 +605,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
           crows = rec[CF_ROW1] - crow0;
           cslot = rec[CF_SLOT];
           cfL = rec[CF_LANES];
+          cfP = rec[CF_PARTS];
           cfg = cw / cfL;
           cfl = cw % cfL;
           cact = cfg * 16 < crows;
@@ -603,20 +622,86 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
             qa[ks][3] = qhi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16 + 8 + cq) : 0u;
           }
         }
-        if (cact && (k % cfL) == cfl && !diag_nocompute) {
-          const uint32_t k_u32 = smem_u32(smem_raw + (size_t)s * stage_bytes);
-          for (int t0 = 0; t0 < c; t0 += TPW)
-            wa.template chunk<false>(qa, k_u32, k_u32 + (uint32_t)tile_bytes, t0, c, scale_log2, lane);
+        // lane l of the job: token slice l % nsl (>= 32 tokens when the chunk
+        // has them) of every alt-th chunk (k % alt == l / nsl): all warps work
+        // on each unit, and each mma call covers 32-64 tokens (independent
+        // accumulator chains; 16-token calls are latency-bound)
+        int nsl = cfL;  // slices per chunk: divides cfL and c / 16, >= 32 tokens each
+        while (nsl > 1 && (nsl * 32 > c || (c / 16) % nsl != 0)) nsl >>= 1;
+        const int alt = cfL / nsl;
+        if (cact && (k % alt) == cfl / nsl && !diag_nocompute) {
+          const uint32_t k_u32 = smem_u32(smem_raw + (size_t)s * stage_bytes), v_u32 = k_u32 + (uint32_t)tile_bytes;
+          const int span = c / nsl, tb = (cfl % nsl) * span;
+          int t0 = tb;
+          for (; t0 + 32 <= tb + span; t0 += 32) wa.template chunk<false, 32>(qa, k_u32, v_u32, t0, c, scale_log2, lane);
+          for (; t0 < tb + span; t0 += 16) wa.template chunk<false, 16>(qa, k_u32, v_u32, t0, c, scale_log2, lane);
         }
         if (md.flags & F_LAST) {
           wa.finish();
-          if (cact) {
+          if (cfP == 1 && cfL > 1) {
+            // merge the token lanes of each row group in this stage's K/V
+            // tiles (every warp is done with them; the stage is released
+            // after): lanes l > 0 store their states, lane 0 folds them in
+            // lane order (Eqn 2) and writes the job's single partial row
+            constexpr int NR = WA::DT * 4 + 4;
+            float* scr = reinterpret_cast<float*>(smem_raw + (size_t)s * stage_bytes);
+            named_sync_consumers();
+            if (cfl > 0 && cact) {
+              float* my = scr + (size_t)(cfg * (cfL - 1) + cfl - 1) * NR * 32 + lane;
+#pragma unroll
+              for (int i = 0; i < WA::DT; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) my[(i * 4 + j) * 32] = wa.o[i][j];
+              my[(NR - 4) * 32] = wa.m_lo;
+              my[(NR - 3) * 32] = wa.m_hi;
+              my[(NR - 2) * 32] = wa.n_lo;
+              my[(NR - 1) * 32] = wa.n_hi;
+              fence_proxy_async();  // generic writes before the stage's next bulk copy
+            }
+            named_sync_consumers();
+            if (cfl == 0 && cact) {
+              const float* ot = scr + (size_t)cfg * (cfL - 1) * NR * 32 + lane;
+              float M_lo = wa.m_lo, M_hi = wa.m_hi;
+              for (int l = 1; l < cfL; ++l) {
+                M_lo = fmaxf(M_lo, ot[((l - 1) * NR + NR - 4) * 32]);
+                M_hi = fmaxf(M_hi, ot[((l - 1) * NR + NR - 3) * 32]);
+              }
+              const float b_lo = M_lo == -INFINITY ? 0.f : M_lo, b_hi = M_hi == -INFINITY ? 0.f : M_hi;
+              const float w_lo = fast_exp2(wa.m_lo - b_lo), w_hi = fast_exp2(wa.m_hi - b_hi);
+              wa.n_lo *= w_lo;
+              wa.n_hi *= w_hi;
+#pragma unroll
+              for (int i = 0; i < WA::DT; ++i) {
+                wa.o[i][0] *= w_lo;
+                wa.o[i][1] *= w_lo;
+                wa.o[i][2] *= w_hi;
+                wa.o[i][3] *= w_hi;
+              }
+              for (int l = 1; l < cfL; ++l) {
+                const float* ol = ot + (size_t)(l - 1) * NR * 32;
+                const float vl = fast_exp2(ol[(NR - 4) * 32] - b_lo), vh = fast_exp2(ol[(NR - 3) * 32] - b_hi);
+                wa.n_lo = fmaf(vl, ol[(NR - 2) * 32], wa.n_lo);
+                wa.n_hi = fmaf(vh, ol[(NR - 1) * 32], wa.n_hi);
+#pragma unroll
+                for (int i = 0; i < WA::DT; ++i) {
+                  wa.o[i][0] = fmaf(vl, ol[(i * 4 + 0) * 32], wa.o[i][0]);
+                  wa.o[i][1] = fmaf(vl, ol[(i * 4 + 1) * 32], wa.o[i][1]);
+                  wa.o[i][2] = fmaf(vh, ol[(i * 4 + 2) * 32], wa.o[i][2]);
+                  wa.o[i][3] = fmaf(vh, ol[(i * 4 + 3) * 32], wa.o[i][3]);
+                }
+              }
+              wa.m_lo = M_lo;
+              wa.m_hi = M_hi;
+            }
+          }
+          if (cact && (cfP > 1 || cfl == 0)) {
             const int rl = lane >> 2, cq = (lane & 3) * 2;
+            const int pl = cfP > 1 ? cfl : 0;  // partial index of this lane
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
               const int rloc = cfg * 16 + rl + 8 * hf;
               if (rloc < crows) {
-                float* prow = pO + ((size_t)(cslot + cfl * crows + rloc) * h + head) * PR;
+                float* prow = pO + ((size_t)(cslot + pl * crows + rloc) * h + head) * PR;
 #pragma unroll
                 for (int i = 0; i < WA::DT; ++i)
                   *reinterpret_cast<float2*>(prow + i * 8 + cq) =
@@ -632,7 +717,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
           named_sync_consumers();
           if (ct < crows) {
             fence_acq_rel_gpu();
-            atomicAdd(cnt + (crow0 + ct) * h + head, (uint32_t)cfL);
+            atomicAdd(cnt + (crow0 + ct) * h + head, (uint32_t)cfP);
           }
         }
         __syncwarp();
@@ -727,6 +812,7 @@ __global__ void __launch_bounds__(kSfThreads) sf_persistent_kernel(
   }
   (void)cw;
   settle_contributions(S, cnt, ct);
+  if (tr && ct == 0) tr[kTraceStride - 1] = globaltimer_ns();  // merge phase start
   merge_pending<TO, D, NG>(S, pO, segO, cnt, out, t, h, ct);
   if (tr && ct == 0) tr[2] = globaltimer_ns();
 }

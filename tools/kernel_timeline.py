@@ -22,6 +22,7 @@ import torch  # noqa: E402
 from bench import DecodeWorkload, flush_l2, time_steps  # noqa: E402
 
 TRACE_STRIDE, TRACE_CTAS, TRACE_UNITS = 128, 2048, 31
+CF_TILE_BYTES = 2 * 64 * 128 * 2  # cfg2 chunk-first unit: K + V tile of one (chunk, head)
 
 
 def summarise(tr, name, ncta):
@@ -69,6 +70,29 @@ def summarise(tr, name, ncta):
     print(f"   consume time (done - ready) us: {q(comp)}")
     print(f"   consumer idle before unit (ready - prev done) us: {q(waitc)}")
     print(f"   gap between consecutive traced ready us: {q(gap)}")
+    # phases per CTA: chunk-first units (64 KiB K+V tiles first in the CTA's
+    # list), seq-first units, the merge phase (tr[127] = after settle, tr[2] = end)
+    cf_end, sf_end, mg_start, mg_len, n_cf = [], [], [], [], []
+    for c in range(ncta):
+        by_c = t[c, 6::4][:TRACE_UNITS]
+        done = t[c, 5::4][:TRACE_UNITS]
+        k = 0
+        while k < len(by_c) and by_c[k] == CF_TILE_BYTES and done[k] > 0:
+            k += 1
+        n_cf.append(k)
+        if k:
+            cf_end.append((done[k - 1] - t0) / 1e3)
+        dd = done[done > 0]
+        if dd.size > k:
+            sf_end.append((dd.max() - t0) / 1e3)
+        if t[c, TRACE_STRIDE - 1] > 0:
+            mg_start.append((t[c, TRACE_STRIDE - 1] - t0) / 1e3)
+            mg_len.append((ends[c] - t[c, TRACE_STRIDE - 1]) / 1e3)
+    q2 = lambda v: f"med {np.median(v):.2f} p90 {np.percentile(v, 90):.2f} max {max(v):.2f}" if v else "-"
+    print(f"   chunk-first units per CTA: {q2(n_cf)}; CTAs with any: {sum(1 for x in n_cf if x)}")
+    print(f"   chunk-first phase end us: {q2(cf_end)}")
+    print(f"   seq-first phase end us: {q2(sf_end)}")
+    print(f"   merge phase start us: {q2(mg_start)}; merge phase length us: {q2(mg_len)}")
     # aggregate data arrival rate over the kernel (bytes of each unit at its ready time)
     rd = t[:, 4:4 + 4 * TRACE_UNITS:4].ravel()
     by = t[:, 6:6 + 4 * TRACE_UNITS:4].ravel()
