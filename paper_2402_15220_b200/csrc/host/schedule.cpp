@@ -94,6 +94,14 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   // ---- split rule: chunks per tile so that heads * tiles >= target CTAs
   int64_t max_n = 1;
   for (const Run& r : runs) max_n = std::max<int64_t>(max_n, (int64_t)r.chunks.size());
+  if (opt.fused) {  // a run wider than the fused tile would re-read its K/V per 64-row tile
+    for (const Run& r : runs)
+      if (r.j - r.i + 1 > kFusedTileRows) {
+        ScheduleOptions o2 = opt;
+        o2.fused = false;
+        return build_context(tree, o2, ctx, err);
+      }
+  }
   const int64_t tile_rows = opt.fused ? kFusedTileRows : kMaxCfTileRows;
   auto lanes_of = [&](const RunTiling& t) { return opt.fused ? fused_lanes(t.rows_per_tile) : 1; };
   // partials per row: the fused kernel merges its L lanes in the stage's K/V

@@ -593,35 +593,42 @@ __global__ void __launch_bounds__(kSfThreads, 2) sf_persistent_kernel(
       const int cf1 = t.fused ? t.sf_cta[blockIdx.x * kSfCtaInts + 3] : 0;
       int cfL = 1, cfP = 1, cfg = 0, cfl = 0, crow0 = 0, crows = 0, cslot = 0;
       bool cact = false;
+      // a job's tile record and Q fragments (dependent global loads): the
+      // CTA's first job is begun at kernel start, overlapping the first copies
+      auto begin_job = [&](int tile, int head) {
+        const int32_t* rec = t.cf_tile + tile * kCfTileInts;
+        crow0 = rec[CF_ROW0];
+        crows = rec[CF_ROW1] - crow0;
+        cslot = rec[CF_SLOT];
+        cfL = rec[CF_LANES];
+        cfP = rec[CF_PARTS];
+        cfg = cw / cfL;
+        cfl = cw % cfL;
+        cact = cfg * 16 < crows;
+        wa.reset();
+        const int rlo = crow0 + cfg * 16 + (lane >> 2), rhi = rlo + 8;
+        const T* qlo = (cact && rlo < crow0 + crows) ? q + ((size_t)t.row_caller[rlo] * h + head) * D : nullptr;
+        const T* qhi = (cact && rhi < crow0 + crows) ? q + ((size_t)t.row_caller[rhi] * h + head) * D : nullptr;
+        const int cq = (lane & 3) * 2;
+#pragma unroll
+        for (int ks = 0; ks < WA::KS; ++ks) {
+          qa[ks][0] = qlo ? *reinterpret_cast<const uint32_t*>(qlo + ks * 16 + cq) : 0u;
+          qa[ks][1] = qhi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16 + cq) : 0u;
+          qa[ks][2] = qlo ? *reinterpret_cast<const uint32_t*>(qlo + ks * 16 + 8 + cq) : 0u;
+          qa[ks][3] = qhi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16 + 8 + cq) : 0u;
+        }
+      };
+      if (cf0 < cf1) {
+        const int4 d0 = *reinterpret_cast<const int4*>(t.cf_unit + (size_t)cf0 * kCfUnitInts);
+        begin_job(d0.y, d0.z);
+      }
       for (int u = cf0; u < cf1; ++u, ++jj) {
         const int s = jj % nst;
         mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
         if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 4 * jj] = globaltimer_ns();
         const StageMeta md = S.meta[s];
         const int tile = md.item, head = md.caller, k = md.seg;
-        if (md.flags & F_FIRST) {
-          const int32_t* rec = t.cf_tile + tile * kCfTileInts;
-          crow0 = rec[CF_ROW0];
-          crows = rec[CF_ROW1] - crow0;
-          cslot = rec[CF_SLOT];
-          cfL = rec[CF_LANES];
-          cfP = rec[CF_PARTS];
-          cfg = cw / cfL;
-          cfl = cw % cfL;
-          cact = cfg * 16 < crows;
-          wa.reset();
-          const int rlo = crow0 + cfg * 16 + (lane >> 2), rhi = rlo + 8;
-          const T* qlo = (cact && rlo < crow0 + crows) ? q + ((size_t)t.row_caller[rlo] * h + head) * D : nullptr;
-          const T* qhi = (cact && rhi < crow0 + crows) ? q + ((size_t)t.row_caller[rhi] * h + head) * D : nullptr;
-          const int cq = (lane & 3) * 2;
-#pragma unroll
-          for (int ks = 0; ks < WA::KS; ++ks) {
-            qa[ks][0] = qlo ? *reinterpret_cast<const uint32_t*>(qlo + ks * 16 + cq) : 0u;
-            qa[ks][1] = qhi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16 + cq) : 0u;
-            qa[ks][2] = qlo ? *reinterpret_cast<const uint32_t*>(qlo + ks * 16 + 8 + cq) : 0u;
-            qa[ks][3] = qhi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16 + 8 + cq) : 0u;
-          }
-        }
+        if ((md.flags & F_FIRST) && u != cf0) begin_job(tile, head);
         // lane l of the job: token slice l % nsl (>= 32 tokens when the chunk
         // has them) of every alt-th chunk (k % alt == l / nsl): all warps work
         // on each unit, and each mma call covers 32-64 tokens (independent

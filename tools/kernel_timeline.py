@@ -111,11 +111,14 @@ def main():
     ap.add_argument("--step", type=int, default=400)
     ap.add_argument("--opt", action="append", default=[])
     ap.add_argument("--kernel", default="sf", choices=["sf", "cf"])
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--n-shared", dest="n_shared", type=int, default=2048)
+    ap.add_argument("--question", type=int, default=0)
     ap.add_argument("--flush", default="write", choices=["write", "clean"],
                     help="clean: write then read the flush buffer (no dirty lines left in L2)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
-    wl = DecodeWorkload(dev, steps=args.step + 2)
+    wl = DecodeWorkload(dev, steps=args.step + 2, b=args.batch, n_shared=args.n_shared, question=args.question)
     for o in args.opt:
         k, v = o.split("=")
         wl.ca.set_option(k, int(v))
