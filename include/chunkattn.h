@@ -154,6 +154,24 @@ chunkattn_status chunkattn_remove_sequence(chunkattn_t h, int64_t seq_id, int64_
 chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const int64_t* seq_ids,
                                   const void* q, void* out, void* stream);
 
+/* Prefill attention with prefix lookup (§2.2/§3.1):
+ * after add_sequence matched a cached prefix and wrote the K/V of the rest,
+ * every query position p >= first_pos[k] of sequence seq_ids[k] attends
+ * causally over positions 0..p of that sequence in the pool (matched shared
+ * chunks + its own):  out_p = softmax(s q_p K[0..p]^T) V[0..p]  (PAPER.md:344
+ * per row, causal).  The projection of the matched prefix is never redone.
+ *   seq_ids    host int64[n], live sequences (any subset, any order)
+ *   first_pos  host int64[n], 0 <= first_pos[k] <= length (typically the
+ *              matched length returned by add_sequence)
+ *   q          device [Q][h][d] dtype, Q = sum(length - first_pos): the
+ *              queries of seq_ids[0] (ascending positions), then seq_ids[1], ...
+ *   out        device [Q][h][d] out_dtype, same order
+ * Needs dtype F16/BF16, d in {64, 128}, c % 16 == 0 (CA_EDTYPE otherwise).
+ * Asynchronous on `stream`; the pool must hold the K/V of every attended
+ * position (stream order after add_sequence / append_kv). */
+chunkattn_status chunkattn_prefill_attend(chunkattn_t h, int32_t layer, int64_t n, const int64_t* seq_ids,
+                                          const int64_t* first_pos, const void* q, void* out, void* stream);
+
 /* One whole decode step from HOST buffers (append_kv of the step's new K/V,
  * then attend of `layer`), with the host<->device copies inside the call:
  *   in_host   host (pinned for asynchrony) packed [q | k_new | v_new]:

@@ -9,6 +9,7 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg and
   tree_model.py  C3 prefix-tree replay model emitting the canonical tables.
   sharing.py     order-free definition of which sequences share which chunk.
   reference.py   the oracle decode step used by bench.py (CPU timing arm).
+  prefill.py     C4 causal prefill attention with prefix lookup (row f1).
 
 Every function cites the PAPER.md passage it follows; pins live in
 tests/test_oracle_*.py.

@@ -67,6 +67,7 @@ _SIGS = {
     "chunkattn_append_kv": (ctypes.c_int, [_P, ctypes.c_int64, _I64P, _I32P, _P, _P, _P]),
     "chunkattn_remove_sequence": (ctypes.c_int, [_P, ctypes.c_int64, _I64P]),
     "chunkattn_attend": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _I64P, _P, _P, _P]),
+    "chunkattn_prefill_attend": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _I64P, _I64P, _P, _P, _P]),
     "chunkattn_decode_step_host": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _I64P, _P, _P, _P, _P,
                                                   ctypes.c_size_t, _P]),
     "chunkattn_batch_order": (ctypes.c_int, [_P, _I64P, ctypes.c_int64, _I64P]),

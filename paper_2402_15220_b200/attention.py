@@ -152,6 +152,24 @@ class ChunkAttention:
         C.check(self.lib.chunkattn_attend(self._h, layer, n, _p64(ids), qp, op, self._stream()))
         return out
 
+    def prefill_attend(self, seq_ids: Sequence[int], first_pos: Sequence[int], q: torch.Tensor,
+                       layer: int = 0, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Causal prefill attention of positions first_pos[k].. of each sequence
+        over its whole context in the pool (chunkattn_prefill_attend): q [Q][h][d]
+        packed in seq_ids order, ascending positions -> out [Q][h][d]."""
+        ids = _i64(seq_ids)
+        fp = _i64(first_pos)
+        if len(fp) != len(ids):
+            raise ValueError("first_pos and seq_ids differ in length")
+        nq = q.shape[0]
+        qp = self._dev(q, (nq, self.h, self.d), "q")
+        if out is None:
+            out = torch.empty((nq, self.h, self.d), dtype=self.out_dtype, device=self.device)
+        op = self._dev(out, (nq, self.h, self.d), "out", self.out_dtype)
+        C.check(self.lib.chunkattn_prefill_attend(self._h, layer, len(ids), _p64(ids), _p64(fp), qp, op,
+                                                  self._stream()))
+        return out
+
     def decode_step_host(self, ids: np.ndarray, toks: np.ndarray, in_host: torch.Tensor, out_host: torch.Tensor,
                          staging: torch.Tensor, layer: int = 0, stream_ptr: int | None = None) -> None:
         """One decode step from host buffers (chunkattn_decode_step_host): in_host

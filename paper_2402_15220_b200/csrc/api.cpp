@@ -33,8 +33,8 @@ chunkattn_status fail(chunkattn_status s, const std::string& msg) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t attend_perm, append_row, tables, pO, segO, counters, trace, total;
-  int64_t table_cap, slot_cap, seg_cap;
+  size_t attend_perm, append_row, tables, pO, segO, counters, prefill, trace, total;
+  int64_t table_cap, slot_cap, seg_cap, pf_cap;
 };
 
 bool valid_config(const chunkattn_config* c, std::string* why) {
@@ -82,6 +82,10 @@ WsLayout ws_layout(const chunkattn_config* c) {
   o = align_up(o + (size_t)4 * w.seg_cap * (c->head_dim + 4), 256);
   w.counters = o;  // per-item contribution counters [B * h] u32 (zeroed; reset by each merge)
   o = align_up(o + (size_t)4 * B * c->num_heads, 256);
+  // prefill tables (chunkattn_prefill_attend): tile records + chunk lists
+  w.pf_cap = (int64_t)kPfTileInts * B * ((c->max_seq_len + kPfTileRows - 1) / kPfTileRows + 1) + B * msc + 16;
+  w.prefill = o;
+  o = align_up(o + (size_t)4 * w.pf_cap, 256);
   w.trace = o;  // debug timeline (option "trace"): the last kTraceCtas*kTraceStride u64 words
   o = align_up(o + (size_t)8 * kTraceCtas * kTraceStride, 256);
   w.total = o;
@@ -358,7 +362,7 @@ chunkattn_status chunkattn_create(const chunkattn_config* cfg, const chunkattn_b
     h->sopt.cf_target_ctas = h->num_sms;
     h->sopt.sf_ctas = 2 * h->num_sms;
     h->tma_ok = cf_mma_supported(h->pool);
-    const size_t pin_bytes = (size_t)4 * (h->ws.table_cap + 2 * cfg->max_batch + 64);
+    const size_t pin_bytes = (size_t)4 * (std::max(h->ws.table_cap, h->ws.pf_cap) + 2 * cfg->max_batch + 64);
     for (int k = 0; k < 2; ++k) {
       cudaError_t e = cudaHostAlloc((void**)&h->pinned[k], pin_bytes, cudaHostAllocDefault);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev[k], cudaEventDisableTiming);
@@ -488,6 +492,56 @@ chunkattn_status chunkattn_remove_sequence(chunkattn_t h, int64_t seq_id, int64_
   if (!h->tree.find(seq_id)) return fail(CA_ENOSEQ, "unknown seq id " + std::to_string(seq_id));
   const auto rel = h->tree.remove(seq_id);
   if (released) *released = (int64_t)rel.size();
+  return CA_OK;
+  CA_GUARD_END
+}
+
+chunkattn_status chunkattn_prefill_attend(chunkattn_t h, int32_t layer, int64_t n, const int64_t* seq_ids,
+                                          const int64_t* first_pos, const void* q, void* out, void* stream) {
+  CA_GUARD_BEGIN
+  if (!h || n < 0 || (n > 0 && (!seq_ids || !first_pos))) return fail(CA_EINVAL, "bad argument");
+  if (h->host_only) return fail(CA_EINVAL, "host-only handle");
+  if (h->failed) return fail(CA_ECUDA, "handle failed on an earlier CUDA error");
+  if (layer < 0 || layer >= h->cfg.num_layers) return fail(CA_EINVAL, "layer out of range");
+  if (!prefill_supported(h->pool)) return fail(CA_EDTYPE, "prefill needs F16/BF16, d in {64, 128}, c % 16 == 0");
+  // tiles of <= 64 consecutive query positions; chunk lists in path order
+  std::vector<int32_t> chunks, tiles;
+  int64_t row = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    const Sequence* sq = h->tree.find(seq_ids[k]);
+    if (!sq) return fail(CA_ENOSEQ, "unknown seq id " + std::to_string(seq_ids[k]));
+    if (first_pos[k] < 0 || first_pos[k] > sq->len) return fail(CA_EINVAL, "first_pos out of range");
+    const int32_t off = (int32_t)chunks.size();
+    chunks.insert(chunks.end(), sq->path.begin(), sq->path.end());
+    for (int64_t p = first_pos[k]; p < sq->len; p += kPfTileRows) {
+      const int32_t nq = (int32_t)std::min<int64_t>(kPfTileRows, sq->len - p);
+      tiles.insert(tiles.end(), {off, (int32_t)(row + p - first_pos[k]), nq, (int32_t)p, (int32_t)sq->len, 0, 0, 0});
+    }
+    row += sq->len - first_pos[k];
+  }
+  if (row > 0 && (!q || !out)) return fail(CA_EINVAL, "null q/out");
+  if ((int64_t)(tiles.size() + chunks.size()) > h->ws.pf_cap) return fail(CA_ENOMEM, "prefill tables exceed workspace");
+  const int32_t n_tiles = (int32_t)(tiles.size() / kPfTileInts);
+  if (n_tiles == 0) return CA_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (h->set_device() != CA_OK) return CA_ECUDA;
+  const size_t tb = tiles.size();
+  tiles.insert(tiles.end(), chunks.begin(), chunks.end());
+  chunkattn_status s = h->upload(h->wsp + h->ws.prefill, tiles.data(), tiles.size() * 4, st);
+  if (s != CA_OK) return s;
+  PrefillLaunch a{};
+  a.pool = h->pool;
+  a.layer = layer;
+  a.q = q;
+  a.out = out;
+  a.out_dtype = h->cfg.out_dtype;
+  a.tiles = reinterpret_cast<const int32_t*>(h->wsp + h->ws.prefill);
+  a.chunks = a.tiles + tb;
+  a.n_tiles = n_tiles;
+  a.scale_log2 = h->scale() * 1.4426950408889634f;
+  cudaError_t e = h->timed_launch(chunkattn::K_COPY, st, [&] { return launch_prefill(a, st); });
+  if (e != cudaSuccess) return h->cuda_fail(e, "prefill");
+  ++h->n_launches;
   return CA_OK;
   CA_GUARD_END
 }

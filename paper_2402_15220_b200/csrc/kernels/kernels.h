@@ -74,6 +74,25 @@ struct AttnLaunch {
   bool use_pdl;
 };
 
+// Prefill attention with prefix lookup (prefill.cu): tile record (kPfTileInts
+// int32) {chunk list offset, first query row, queries (<= 64), position of the
+// first query, sequence length, 0, 0, 0}; chunk lists are path order.
+constexpr int kPfTileInts = 8;
+constexpr int kPfTileRows = 64;
+struct PrefillLaunch {
+  PoolGeom pool;
+  int32_t layer;
+  const void* q;  // [total queries][h][d] dtype
+  void* out;      // [total queries][h][d] out_dtype
+  int32_t out_dtype;
+  const int32_t* tiles;
+  const int32_t* chunks;
+  int32_t n_tiles;
+  float scale_log2;
+};
+bool prefill_supported(const PoolGeom& pool);
+cudaError_t launch_prefill(const PrefillLaunch& a, cudaStream_t st);
+
 // K1: scatter one decode step's K/V into the leaf chunks and set seq_len.
 struct AppendItem {
   int32_t row, chunk, slot, new_len;

@@ -39,23 +39,35 @@ struct WarpAttn {
   // Tokens [tok0, tok0 + NTOK) of the tile; tokens >= nvalid are masked (MASK).
   // NTOK > 16 gives the mma chains NTOK / 8 independent accumulators (the
   // chunk-first phase is latency-bound at 16 tokens per call).
-  template <bool MASK, int NTOK = TPW>
+  // CAUSAL (prefill): additionally, row lo / hi (lane >> 2, + 8) sees only
+  // tokens < lim_lo / lim_hi of the tile.
+  template <bool MASK, int NTOK = TPW, bool CAUSAL = false>
   CA_DEV void chunk(const uint32_t (&qa)[KS][4], uint32_t k_u32, uint32_t v_u32, int tok0, int nvalid,
-                    float scale_log2, int lane) {
+                    float scale_log2, int lane, int lim_lo = 0, int lim_hi = 0) {
     constexpr int NT = NTOK / 8;
     const int mi = lane >> 3, r8 = lane & 7;
     float sc[NT][4];
 #pragma unroll
     for (int i = 0; i < NT; ++i) sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
+    // K fragments of k-step ks + 1 are loaded before the mma of k-step ks
+    // (ldmatrix is ordered asm: without the register double buffer every
+    // mma would wait out a full ldmatrix latency)
+    uint32_t kb[2][NT / 2][4];
+    auto load_k = [&](int ks, uint32_t (&dst)[NT / 2][4]) {
 #pragma unroll
       for (int np = 0; np < NT / 2; ++np) {
-        uint32_t b0, b1, b2, b3;
         const int tok = tok0 + np * 16 + (mi >> 1) * 8 + r8;
-        ldmatrix_x4(k_u32 + tile_off<D>(tok, ks * 16 + (mi & 1) * 8), b0, b1, b2, b3);
-        Mma<T>::run(sc[2 * np], qa[ks], b0, b1);
-        Mma<T>::run(sc[2 * np + 1], qa[ks], b2, b3);
+        ldmatrix_x4(k_u32 + tile_off<D>(tok, ks * 16 + (mi & 1) * 8), dst[np][0], dst[np][1], dst[np][2], dst[np][3]);
+      }
+    };
+    load_k(0, kb[0]);
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      if (ks + 1 < KS) load_k(ks + 1, kb[(ks + 1) & 1]);
+#pragma unroll
+      for (int np = 0; np < NT / 2; ++np) {
+        Mma<T>::run(sc[2 * np], qa[ks], kb[ks & 1][np][0], kb[ks & 1][np][1]);
+        Mma<T>::run(sc[2 * np + 1], qa[ks], kb[ks & 1][np][2], kb[ks & 1][np][3]);
       }
     }
     if (MASK) {
@@ -65,6 +77,12 @@ struct WarpAttn {
         const int t0 = cb + i * 8;
         if (t0 >= nvalid) sc[i][0] = sc[i][2] = -INFINITY;
         if (t0 + 1 >= nvalid) sc[i][1] = sc[i][3] = -INFINITY;
+        if (CAUSAL) {
+          if (t0 >= lim_lo) sc[i][0] = -INFINITY;
+          if (t0 + 1 >= lim_lo) sc[i][1] = -INFINITY;
+          if (t0 >= lim_hi) sc[i][2] = -INFINITY;
+          if (t0 + 1 >= lim_hi) sc[i][3] = -INFINITY;
+        }
       }
     }
     float mx_lo = -INFINITY, mx_hi = -INFINITY;
@@ -116,11 +134,17 @@ struct WarpAttn {
         vm0 = (tb < nvalid ? 0x0000ffffu : 0u) | (tb + 1 < nvalid ? 0xffff0000u : 0u);
         vm1 = (tb + 8 < nvalid ? 0x0000ffffu : 0u) | (tb + 9 < nvalid ? 0xffff0000u : 0u);
       }
+      // V fragments one d-pair ahead of the mma (see load_k)
+      const int vtok = tok0 + kk * 16 + (mi & 1) * 8 + r8;
+      uint32_t vb[2][4];
+      ldmatrix_x4_trans(v_u32 + tile_off<D>(vtok, (mi >> 1) * 8), vb[0][0], vb[0][1], vb[0][2], vb[0][3]);
 #pragma unroll
       for (int dp = 0; dp < DT / 2; ++dp) {
-        uint32_t b0, b1, b2, b3;
-        const int tok = tok0 + kk * 16 + (mi & 1) * 8 + r8;
-        ldmatrix_x4_trans(v_u32 + tile_off<D>(tok, dp * 16 + (mi >> 1) * 8), b0, b1, b2, b3);
+        if (dp + 1 < DT / 2) {
+          uint32_t(&nx)[4] = vb[(dp + 1) & 1];
+          ldmatrix_x4_trans(v_u32 + tile_off<D>(vtok, (dp + 1) * 16 + (mi >> 1) * 8), nx[0], nx[1], nx[2], nx[3]);
+        }
+        uint32_t b0 = vb[dp & 1][0], b1 = vb[dp & 1][1], b2 = vb[dp & 1][2], b3 = vb[dp & 1][3];
         if (MASK) {
           b0 &= vm0;
           b2 &= vm0;
