@@ -135,6 +135,11 @@ CA_DEV void prefetch_tmap(const CUtensorMap* map) {
 CA_DEV void st_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+CA_DEV uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 CA_DEV uint32_t ld_acquire_gpu(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -154,8 +159,13 @@ CA_DEV void spin_flags_warp(const uint32_t* f, bool mine, uint32_t tag, int who)
   const uint64_t t0 = globaltimer_ns();
 #endif
   for (;;) {
-    const bool ok = !mine || ld_acquire_gpu(f) == tag;
-    if (__all_sync(0xffffffffu, ok)) break;
+    // relaxed polls (an acquire load invalidates the SM's L1 every time, which
+    // stalls the co-resident CTA's memory pipe); one acquire once it matched
+    const bool ok = !mine || ld_relaxed_gpu(f) == tag;
+    if (__all_sync(0xffffffffu, ok)) {
+      if (mine) (void)ld_acquire_gpu(f);
+      break;
+    }
     __nanosleep(32);
 #ifdef CA_HANG_CHECK
     if (globaltimer_ns() - t0 > 2000000000ull) CA_HANG_TRAP("flag", who, ok ? 1 : 0);
