@@ -36,6 +36,12 @@ using namespace dev;
 namespace {
 
 constexpr int kMaxStages = 8;
+// Fused chunk-first token slice per warp and call (>= 32 tokens: 16-token
+// mma calls are latency-bound).  64-token calls are cheaper in isolation
+// (~1650 vs ~2400 cycles per 64 tokens x 16 rows, tools/warpattn_bench.cu) but
+// spill in this kernel's 168-register budget and measured slower (49.0 vs
+// 45.5 us per cfg2 step).
+constexpr int kCfSlice = 32;
 
 template <typename T, int D>
 struct Geo {
@@ -633,8 +639,8 @@ __global__ void __launch_bounds__(kSfThreads, 2) sf_persistent_kernel(
         // has them) of every alt-th chunk (k % alt == l / nsl): all warps work
         // on each unit, and each mma call covers 32-64 tokens (independent
         // accumulator chains; 16-token calls are latency-bound)
-        int nsl = cfL;  // slices per chunk: divides cfL and c / 16, >= 32 tokens each
-        while (nsl > 1 && (nsl * 32 > c || (c / 16) % nsl != 0)) nsl >>= 1;
+        int nsl = cfL;  // slices per chunk: divides cfL and c / 16, >= kCfSlice tokens each
+        while (nsl > 1 && (nsl * kCfSlice > c || (c / 16) % nsl != 0)) nsl >>= 1;
         const int alt = cfL / nsl;
         if (cact && (k % alt) == cfl / nsl && !diag_nocompute) {
           const uint32_t k_u32 = smem_u32(smem_raw + (size_t)s * stage_bytes), v_u32 = k_u32 + (uint32_t)tile_bytes;
