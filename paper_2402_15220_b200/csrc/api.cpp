@@ -112,6 +112,7 @@ struct chunkattn {
   // default -- the co-resident pair faulted intermittently with the SIMT
   // seq-first consumers; costs ~1.5% on cfg2.
   bool cf_small = false;
+  bool cf_umma = true;  // tcgen05 chunk-first kernel in the two-kernel path
   // chunk-first units inside the persistent seq-first kernel (one launch per
   // attend; falls back to two kernels when the schedule does not allow it)
   bool fused_opt = true;
@@ -594,6 +595,7 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   a.cf_tensor_cores = h->tma_ok && !h->cf_simt;
   a.sf_tensor_cores = !h->sf_simt;
   a.cf_small = h->cf_small;
+  a.cf_umma = h->cf_umma;
   a.trace = h->trace_kernel ? reinterpret_cast<uint64_t*>(h->wsp + h->ws.trace) : nullptr;
   a.trace_cf = h->trace_kernel == 2;
   a.sf_ctas_per_sm = h->sf_ctas_per_sm;
@@ -714,6 +716,8 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->sopt.cf_unit_cost = value < 1 ? 0.1 : (double)value / 10.0;  // tenths of a seq-first unit
   } else if (k == "cf_lane_merge") {
     h->sopt.cf_lane_merge = value != 0;
+  } else if (k == "cf_umma") {
+    h->cf_umma = value != 0;
   } else if (k == "cf_small") {
     h->cf_small = value != 0;
   } else if (k == "diag_nocompute") {

@@ -240,6 +240,8 @@ cudaError_t launch_chunk_first(const AttnLaunch& a, const DevTables& t, cudaStre
   int L = 1, tpw = 16;
   // small CTA (4 consumer warps, ~100 KB ring) when the tiles allow it, so a
   // seq-first CTA fits beside it; 8 warps for tiles of up to 128 rows
+  if (a.cf_tensor_cores && a.cf_umma && cf_umma_supported(a.pool, t.max_tile_rows))
+    return launch_chunk_first_umma(a, t, st);
   const bool small = a.cf_small && t.max_tile_rows <= 64;
   const int warps = small ? 4 : 8;
   if (!a.cf_tensor_cores || !cf_mma_supported(a.pool) || !pick_slices(a.pool.c, t.max_tile_rows, warps, &L, &tpw))

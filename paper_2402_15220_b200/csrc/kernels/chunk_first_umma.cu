@@ -1,0 +1,393 @@
+// K3 chunk-first phase on the 5th-generation tensor cores (tcgen05 / UMMA;
+// SURVEY §8 row f3).  Same job and output contract as cf_mma_kernel (Alg 1,
+// PAPER.md:72-91; Eqn 1): one CTA = (head, rows [r0, r1) <=
+// 128 of a shared run, chunks [k0, k1) of that run) -> one fp32 partial row
+// (o | m n, m in log2 units) per (row, head).
+//
+//   S_k = Q . K_k^T   M = 128 rows, N = c tokens, K = d   (A = Q, B = K: K-major)
+//   O  += P_k . V_k   M = 128 rows, N = d, K = c tokens   (A = P: K-major, B = V: MN-major)
+// issued by one thread (warp 5), S double-buffered and O in TMEM; the online
+// softmax (Eqn 1 + Eqn 2 rescale) runs on 4 warps, thread = row = TMEM lane,
+// concurrently with the next chunk's S.  O is rescaled lazily (only when a
+// row's max grows by more than 2^8: P <= 256 is exact enough in 16 bits and
+// the final O / n does not depend on the reference max).  K / V tiles arrive
+// by 2-D TMA (one box per 64-element d-half: the pool rows are already XOR
+// pre-swizzled within each 128-byte half, so the boxes land as canonical
+// SWIZZLE_128B atoms -- tools/umma_probe.cu validates both operand layouts).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+
+#include "../host/schedule.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pakv {
+
+using namespace dev;
+
+namespace {
+
+constexpr int kUmRows = 128;   // UMMA M
+constexpr int kUmStages = 3;   // K/V ring depth
+constexpr int kUmThreads = 192;  // warps 0-3 softmax/epilogue, 4 TMA producer, 5 MMA issuer
+constexpr float kRescaleLog2 = 8.f;  // lazy O rescale threshold (P <= 2^8)
+
+struct UmShared {
+  uint64_t kv_full[kUmStages], kv_empty[kUmStages];
+  uint64_t s_full[2], s_free[2], p_full[2], pv_done[2];
+  uint64_t q_full, o_ready;
+  uint32_t tmem_base;
+};
+
+CA_DEV uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3fff);
+  d |= (uint64_t)((lbo >> 4) & 0x3fff) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3fff) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+template <typename T>
+CA_DEV constexpr uint32_t umma_idesc(int n, bool b_mn_major) {
+  const uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((b_mn_major ? 1u : 0u) << 16) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(kUmRows >> 4) << 24);
+}
+CA_DEV void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+CA_DEV void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+CA_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+CA_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+CA_DEV void tmem_ld32(uint32_t addr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+}
+CA_DEV void tmem_st32(uint32_t addr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+CA_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+CA_DEV void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+CA_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+// byte offset of 16-byte group j (of 8) of row r inside a SWIZZLE_128B image
+CA_DEV uint32_t sw128(int r, int j) { return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4)); }
+
+template <typename T, int D, int C>
+__global__ void __launch_bounds__(kUmThreads, 1)
+    cf_umma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
+                   const T* __restrict__ q, float* __restrict__ pO, DevTables t, int32_t h, int64_t layer_rows,
+                   float scale_log2) {
+  constexpr int HALVES = D / 64;            // 128-byte d-halves of a token row
+  constexpr int PATOMS = C / 64;            // 128-byte token atoms of a P row
+  constexpr uint32_t kQBytes = HALVES * kUmRows * 128;
+  constexpr uint32_t kTileBytes = HALVES * C * 128;  // one K (or V) tile image
+  constexpr uint32_t kStageBytes = 2 * kTileBytes;
+  constexpr uint32_t kPBytes = PATOMS * kUmRows * 128;
+  constexpr uint32_t kTmemCols = 2 * C + D <= 256 ? 256 : 512;
+  constexpr int PR = D + 4;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sQ = sm;
+  unsigned char* sKV = sQ + kQBytes;
+  unsigned char* sP = sKV + kUmStages * kStageBytes;
+  __shared__ UmShared S;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int head = blockIdx.y;
+  const int32_t* tile = t.cf_tile + blockIdx.x * kCfTileInts;
+  const int chunk_off = tile[CF_CHUNK_OFF], n_chunks = tile[CF_NCHUNK], row0 = tile[CF_ROW0], row1 = tile[CF_ROW1];
+  const int slot0 = tile[CF_SLOT];
+  const int rows = row1 - row0;
+  pdl_launch_dependents();
+
+  if (tid == 0) {
+    for (int s = 0; s < kUmStages; ++s) {
+      mbar_init(&S.kv_full[s], 1);
+      mbar_init(&S.kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.s_full[b], 1);
+      mbar_init(&S.s_free[b], 4);
+      mbar_init(&S.p_full[b], 4);
+      mbar_init(&S.pv_done[b], 1);
+    }
+    mbar_init(&S.q_full, 4);
+    mbar_init(&S.o_ready, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
+                 "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+  const uint32_t tS0 = tmem, tO = tmem + 2 * C;
+
+  if (warp == 4) {
+    // ---------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      for (int k = 0; k < n_chunks; ++k) {
+        const int s = k % kUmStages;
+        if (k >= kUmStages) mbar_wait(&S.kv_empty[s], (uint32_t)(((k / kUmStages) - 1) & 1));
+        mbar_arrive_expect_tx(&S.kv_full[s], kStageBytes);
+        const int y = (int)(layer_rows + ((int64_t)t.cf_chunk[chunk_off + k] * h + head) * C);
+        unsigned char* st = sKV + s * kStageBytes;
+#pragma unroll
+        for (int hf = 0; hf < HALVES; ++hf) {
+          tma_load_2d(st + hf * C * 128, &tmap_k, hf * 64, y, &S.kv_full[s]);
+          tma_load_2d(st + kTileBytes + hf * C * 128, &tmap_v, hf * 64, y, &S.kv_full[s]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idS = umma_idesc<T>(C, false), idO = umma_idesc<T>(D, true);
+      const uint32_t qa = smem_u32(sQ), kva = smem_u32(sKV), pa = smem_u32(sP);
+      mbar_wait(&S.q_full, 0);
+      tc_fence_after();
+      auto issue_pv = [&](int j) {  // O += P_j V_j
+        const int b = j & 1, s = j % kUmStages;
+        mbar_wait(&S.p_full[b], (uint32_t)((j >> 1) & 1));
+        tc_fence_after();
+        const uint32_t va = kva + s * kStageBytes + kTileBytes, pb = pa + b * kPBytes;
+#pragma unroll
+        for (int ks = 0; ks < C / 16; ++ks)
+          umma_f16(tO, umma_sdesc(pb + (ks / 4) * kUmRows * 128 + (ks % 4) * 32, 16, 1024),
+                   umma_sdesc(va + ks * 16 * 128, C * 128, 1024), idO, (j > 0 || ks > 0) ? 1u : 0u);
+        umma_commit(&S.pv_done[b]);
+        umma_commit(&S.kv_empty[s]);
+      };
+      for (int k = 0; k < n_chunks; ++k) {
+        const int s = k % kUmStages, b = k & 1;
+        mbar_wait(&S.kv_full[s], (uint32_t)((k / kUmStages) & 1));
+        if (k >= 2) mbar_wait(&S.s_free[b], (uint32_t)(((k >> 1) - 1) & 1));
+        tc_fence_after();
+        const uint32_t ka = kva + s * kStageBytes;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {  // S_k = Q K_k^T over d
+          const uint32_t o = (ks / 4) * 0u + (ks % 4) * 32;
+          umma_f16(tS0 + b * C, umma_sdesc(qa + (ks / 4) * kUmRows * 128 + o, 16, 1024),
+                   umma_sdesc(ka + (ks / 4) * C * 128 + o, 16, 1024), idS, ks > 0 ? 1u : 0u);
+        }
+        umma_commit(&S.s_full[b]);
+        if (k >= 1) issue_pv(k - 1);
+      }
+      if (n_chunks > 0) issue_pv(n_chunks - 1);
+      umma_commit(&S.o_ready);
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------- softmax / epilogue
+    const int r = tid;  // row of the tile = TMEM lane
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    {  // Q image (SWIZZLE_128B, d-halves), rows past the tile zero
+      const T* qrow = r < rows ? q + ((size_t)t.row_caller[row0 + r] * h + head) * D : nullptr;
+#pragma unroll
+      for (int g = 0; g < D / 8; ++g) {
+        const uint4 v = qrow ? *reinterpret_cast<const uint4*>(qrow + g * 8) : make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(sQ + (g / 8) * kUmRows * 128 + sw128(r, g % 8)) = v;
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&S.q_full);
+    }
+    float m_ref = -INFINITY, n = 0.f;
+    for (int k = 0; k < n_chunks; ++k) {
+      const int b = k & 1;
+      mbar_wait(&S.s_full[b], (uint32_t)((k >> 1) & 1));
+      tc_fence_after();
+      float sv[C];
+#pragma unroll
+      for (int c0 = 0; c0 < C; c0 += 32) {
+        uint32_t u[32];
+        tmem_ld32(tS0 + b * C + lane_base + c0, u);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[c0 + i] = __uint_as_float(u[i]) * scale_log2;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&S.s_free[b]);
+      float mx = sv[0];
+#pragma unroll
+      for (int i = 1; i < C; ++i) mx = fmaxf(mx, sv[i]);
+      // lazy rescale: a new reference max only when this row's max grew by more than 2^8
+      const bool need = mx > m_ref + kRescaleLog2;
+      if (__any_sync(0xffffffffu, need)) {
+        const float m_new = need ? mx : m_ref;
+        const float f = (need && m_ref != -INFINITY) ? fast_exp2(m_ref - m_new) : 1.f;
+        if (k > 0) {  // O holds chunks 0..k-1: wait for PV_{k-1}, scale it in TMEM
+          mbar_wait(&S.pv_done[(k - 1) & 1], (uint32_t)(((k - 1) >> 1) & 1));
+          tc_fence_after();
+#pragma unroll 1
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t u[32];
+            tmem_ld32(tO + lane_base + c0, u);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * f);
+            tmem_st32(tO + lane_base + c0, u);
+          }
+          tmem_wait_st();
+          tc_fence_before();
+        }
+        n *= f;
+        m_ref = m_new;
+      }
+      // P_k = exp2(s - m_ref) rounded to T (n from the rounded P, reading A11)
+      if (k >= 2) mbar_wait(&S.pv_done[b], (uint32_t)(((k >> 1) - 1) & 1));  // PV_{k-2} read this buffer
+      unsigned char* pb = sP + b * kPBytes;
+#pragma unroll
+      for (int g = 0; g < C / 8; ++g) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          w[e] = Mma<T>::pack(fast_exp2(sv[g * 8 + 2 * e] - m_ref), fast_exp2(sv[g * 8 + 2 * e + 1] - m_ref));
+          const float2 f2 = Mma<T>::unpack(w[e]);
+          n += f2.x + f2.y;
+        }
+        *reinterpret_cast<uint4*>(pb + (g / 8) * kUmRows * 128 + sw128(r, g % 8)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&S.p_full[b]);
+    }
+    // epilogue: O (unnormalised), m (log2 units), n -> the row's partial
+    mbar_wait(&S.o_ready, 0);
+    tc_fence_after();
+    float* prow = r < rows ? pO + ((size_t)(slot0 + r) * h + head) * PR : nullptr;
+#pragma unroll 1
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      uint32_t u[32];
+      tmem_ld32(tO + lane_base + c0, u);
+      tmem_wait_ld();
+      if (prow) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(prow + c0 + i) = make_float4(__uint_as_float(u[i]), __uint_as_float(u[i + 1]),
+                                                                 __uint_as_float(u[i + 2]), __uint_as_float(u[i + 3]));
+      }
+    }
+    if (prow) *reinterpret_cast<float2*>(prow + D) = make_float2(m_ref, n);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+  pdl_wait();  // PDL chain append -> chunk-first -> seq-first (see cf_mma_kernel)
+}
+
+// 2-D views of the pools for TMA: [layers * chunks * h * c rows][d] 16-bit,
+// boxes of 64 elements x c rows (one 128-byte d-half of a (chunk, head) tile)
+struct MapKey {
+  const void* base;
+  int64_t rows;
+  int32_t d, c;
+  bool operator<(const MapKey& o) const {
+    return std::tie(base, rows, d, c) < std::tie(o.base, o.rows, o.d, o.c);
+  }
+};
+
+bool encode_map(const void* base, int64_t rows, int d, int c, CUtensorMap* out) {
+  static std::mutex mu;
+  static std::map<MapKey, CUtensorMap> cache;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  const MapKey key{base, rows, d, c};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q{};
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)c};
+  const cuuint32_t estr[2] = {1, 1};
+  if (encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  cache[key] = m;
+  *out = m;
+  return true;
+}
+
+template <typename T, int D, int C>
+cudaError_t launch_t(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
+  const PoolGeom& p = a.pool;
+  const int64_t rows = (int64_t)p.num_layers * p.max_chunks * p.h * p.c;
+  CUtensorMap mk, mv;
+  if (!encode_map(p.k, rows, D, C, &mk) || !encode_map(p.v, rows, D, C, &mv)) return cudaErrorNotSupported;
+  constexpr size_t smem = 1024 + (size_t)(D / 64) * kUmRows * 128 + (size_t)kUmStages * 2 * (D / 64) * C * 128 +
+                          (size_t)2 * (C / 64) * kUmRows * 128;
+  auto kern = cf_umma_kernel<T, D, C>;
+  cudaError_t e = set_smem_once((const void*)kern, smem);
+  if (e != cudaSuccess) return e;
+  return launch_ex(kern, dim3(t.n_cf_tiles, p.h), dim3(kUmThreads), smem, st, a.use_pdl, mk, mv, (const T*)a.q, a.pO,
+                   t, (int32_t)p.h, (int64_t)a.layer * p.max_chunks * p.h * p.c, a.scale_log2);
+}
+
+template <typename T>
+cudaError_t dispatch(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
+  if (a.pool.d == 128 && a.pool.c == 64) return launch_t<T, 128, 64>(a, t, st);
+  if (a.pool.d == 128 && a.pool.c == 128) return launch_t<T, 128, 128>(a, t, st);
+  if (a.pool.d == 64 && a.pool.c == 64) return launch_t<T, 64, 64>(a, t, st);
+  if (a.pool.d == 64 && a.pool.c == 128) return launch_t<T, 64, 128>(a, t, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+bool cf_umma_supported(const PoolGeom& p, int max_tile_rows) {
+  return (p.dtype == DT_F16 || p.dtype == DT_BF16) && (p.d == 64 || p.d == 128) && (p.c == 64 || p.c == 128) &&
+         max_tile_rows <= kUmRows;
+}
+
+cudaError_t launch_chunk_first_umma(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
+  if (t.n_cf_tiles == 0) return cudaSuccess;
+  if (a.pool.dtype == DT_F16) return dispatch<__half>(a, t, st);
+  return dispatch<__nv_bfloat16>(a, t, st);
+}
+
+}  // namespace pakv

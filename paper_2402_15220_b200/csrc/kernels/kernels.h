@@ -70,6 +70,7 @@ struct AttnLaunch {
   int sf_prefetch;       // seq-first L2 prefetch distance in units (0 = off)
   bool cf_tensor_cores;  // use the mma chunk-first kernel
   bool cf_small;         // 4-warp chunk-first CTA (co-resident with seq-first) when tiles allow
+  bool cf_umma;          // tcgen05 chunk-first kernel when supported (two-kernel path)
   bool sf_tensor_cores;  // use the mma consumers in the seq-first kernel (16-bit types)
   bool use_pdl;
 };
@@ -112,5 +113,8 @@ cudaError_t launch_chunk_first(const AttnLaunch& a, const DevTables& t, cudaStre
 cudaError_t launch_seq_first(const AttnLaunch& a, const DevTables& t, cudaStream_t st);
 
 bool cf_mma_supported(const PoolGeom& pool);
+// tcgen05 chunk-first (chunk_first_umma.cu): 16-bit, d in {64, 128}, c in {64, 128}, tiles <= 128 rows
+bool cf_umma_supported(const PoolGeom& pool, int max_tile_rows);
+cudaError_t launch_chunk_first_umma(const AttnLaunch& a, const DevTables& t, cudaStream_t st);
 
 }  // namespace pakv

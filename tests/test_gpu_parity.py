@@ -15,8 +15,9 @@ pytestmark = pytest.mark.gpu
 
 TOL = {("f32", "f32"): 1e-5, ("f16", "f16"): 2e-3, ("bf16", "f32"): 2e-3, ("f16", "f32"): 2e-3}
 # kernel variants exercised beside the default (fused single-kernel) path: the
-# two-kernel phase pair, and its 4-warp chunk-first CTA (PDL co-residency)
-VARIANTS = ["", "fused=0", "fused=0,cf_small=1"]
+# two-kernel phase pair (tcgen05 chunk-first where supported), with the
+# mma.sync chunk-first kernel, and its 4-warp CTA (PDL co-residency)
+VARIANTS = ["", "fused=0", "fused=0,cf_umma=0", "fused=0,cf_umma=0,cf_small=1"]
 
 
 # --------------------------------------------------------------- config 1 ---
