@@ -45,8 +45,11 @@ def time_attend(wl: DecodeWorkload, iters: int, flush, stream) -> list[float]:
     return [a.elapsed_time(b) * 1e3 for a, b in evs]  # us
 
 
-def run_point(dev, b, n_p, n_s, mode, iters, flush, stream, c=64):
+def run_point(dev, b, n_p, n_s, mode, iters, flush, stream, c=64, opts=()):
     wl = DecodeWorkload(dev, b=b, n_shared=n_s, question=n_p - n_s, steps=2, mode=mode)
+    for o in opts:
+        key, val = o.split("=")
+        wl.ca.set_option(key, int(val))
     wl.fill()
     with torch.cuda.stream(stream):
         wl.step(0, stream.cuda_stream)  # one decode token: context n_p + 1, attention after the append
@@ -70,6 +73,7 @@ def main():
     ap.add_argument("--points", default="all", choices=["tab", "cfg3", "cfg5", "all"])
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--opt", action="append", default=[], help="library option key=value (ChunkAttn mode only)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -92,7 +96,8 @@ def main():
     for (b, n_p, n_s) in pts:
         res = {}
         for mode in ("chunk", "b1", "b0"):
-            r = run_point(dev, b, n_p, n_s, mode, args.iters, flush, stream)
+            r = run_point(dev, b, n_p, n_s, mode, args.iters, flush, stream,
+                          opts=args.opt if mode == "chunk" else ())
             res[mode] = r
         for mode, r in res.items():
             r["speedup_vs_b0"] = res["b0"]["us_median"] / r["us_median"]
