@@ -216,6 +216,11 @@ chunkattn_status chunkattn_counters(chunkattn_t h, int64_t out[6]);
  *   "cf_simt"          1 = force the SIMT chunk-first kernel (no tensor cores;
  *                      implies fused = 0)
  *   "sf_simt"          1 = SIMT seq-first consumers (implies fused = 0)
+ *   "cf_umma"          1 (default) = tcgen05 chunk-first kernel in the two-kernel
+ *                      path when supported (16-bit, d in {64, 128}, c = 64);
+ *                      0 = the mma.sync kernel
+ *   "cf_lane_merge"    1 (default) = the fused kernel merges its token lanes in
+ *                      shared memory (one partial per row and job)
  *   "cf_small"         1 = 4-warp chunk-first CTA when tiles have <= 64 rows
  *                      (two-kernel path; default 0)
  *   "sf_ctas"          persistent grid size (default 296 = 2 per SM)

@@ -371,16 +371,15 @@ cudaError_t launch_t(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
 template <typename T>
 cudaError_t dispatch(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   if (a.pool.d == 128 && a.pool.c == 64) return launch_t<T, 128, 64>(a, t, st);
-  if (a.pool.d == 128 && a.pool.c == 128) return launch_t<T, 128, 128>(a, t, st);
   if (a.pool.d == 64 && a.pool.c == 64) return launch_t<T, 64, 64>(a, t, st);
-  if (a.pool.d == 64 && a.pool.c == 128) return launch_t<T, 64, 128>(a, t, st);
   return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
 bool cf_umma_supported(const PoolGeom& p, int max_tile_rows) {
-  return (p.dtype == DT_F16 || p.dtype == DT_BF16) && (p.d == 64 || p.d == 128) && (p.c == 64 || p.c == 128) &&
+  // c = 128 would need 2 x 32 KB P buffers and 64 KB stages: over the shared-memory budget
+  return (p.dtype == DT_F16 || p.dtype == DT_BF16) && (p.d == 64 || p.d == 128) && p.c == 64 &&
          max_tile_rows <= kUmRows;
 }
 

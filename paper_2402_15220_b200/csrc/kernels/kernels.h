@@ -113,7 +113,7 @@ cudaError_t launch_chunk_first(const AttnLaunch& a, const DevTables& t, cudaStre
 cudaError_t launch_seq_first(const AttnLaunch& a, const DevTables& t, cudaStream_t st);
 
 bool cf_mma_supported(const PoolGeom& pool);
-// tcgen05 chunk-first (chunk_first_umma.cu): 16-bit, d in {64, 128}, c in {64, 128}, tiles <= 128 rows
+// tcgen05 chunk-first (chunk_first_umma.cu): 16-bit, d in {64, 128}, c = 64, tiles <= 128 rows
 bool cf_umma_supported(const PoolGeom& pool, int max_tile_rows);
 cudaError_t launch_chunk_first_umma(const AttnLaunch& a, const DevTables& t, cudaStream_t st);
 

@@ -412,3 +412,29 @@ def test_decode_step_host_matches_device_path():
     with pytest.raises(Exception):  # staging too small
         hs.ca.decode_step_host(ida, _np.zeros(len(ids), dtype=_np.int32), torch.zeros(16).pin_memory(),
                                torch.zeros(16).pin_memory(), torch.empty(16, dtype=torch.uint8, device="cuda"))
+
+
+# ------------------------------------------------- tcgen05 chunk-first (f3) ---
+@pytest.mark.parametrize("d,c,dt,odt", [(128, 64, "f16", "f16"), (64, 64, "bf16", "f32"), (128, 128, "f16", "f32")])
+def test_tcgen05_chunk_first_wide_runs(d, c, dt, odt):
+    """Runs wider than the fused tile (130 and 70 rows) take the two-kernel
+    schedule with the tcgen05 chunk-first (c = 64; c = 128 takes the mma.sync
+    kernel): two row tiles per run, both head dims, a two-level tree (system prompt shared by
+    all rows + a group prefix shared by 70), partial private chunks."""
+    hs = Harness(2, d, c, dt, odt, seed=11, alpha=8.0, max_chunks=1024)
+    sys_p = synth.token_ids(11, synth.TAG_SYS, 0, 3 * c).tolist()
+    grp = synth.token_ids(11, synth.TAG_SYS, 1, c).tolist()
+    ids = []
+    for i in range(130):
+        pre = sys_p + (grp if i < 70 else [])
+        ids.append(hs.add(pre + synth.token_ids(11, synth.TAG_PRIV, i, i % 37).tolist())[0])
+    hs.step = 1
+    hs.append(ids, decode_tokens(hs, ids))
+    hs.check(ids, TOL[(dt, odt)])
+    hs2 = Harness(2, d, c, dt, odt, seed=11, alpha=8.0, max_chunks=1024, opts="cf_umma=0")
+    for i in range(130):
+        pre = sys_p + (grp if i < 70 else [])
+        hs2.add(pre + synth.token_ids(11, synth.TAG_PRIV, i, i % 37).tolist())
+    hs2.step = 1
+    hs2.append(ids, decode_tokens(hs2, ids))
+    hs2.check(ids, TOL[(dt, odt)])  # the mma.sync chunk-first on the same tree
