@@ -505,7 +505,9 @@ chunkattn_status chunkattn_prefill_attend(chunkattn_t h, int32_t layer, int64_t 
   if (h->failed) return fail(CA_ECUDA, "handle failed on an earlier CUDA error");
   if (layer < 0 || layer >= h->cfg.num_layers) return fail(CA_EINVAL, "layer out of range");
   if (!prefill_supported(h->pool)) return fail(CA_EDTYPE, "prefill needs F16/BF16, d in {64, 128}, c % 16 == 0");
-  // tiles of <= 64 consecutive query positions; chunk lists in path order
+  // tiles of <= 64 (mma.sync) or 128 (tcgen05) consecutive query positions; chunk lists in path order
+  const bool umma = h->cf_umma && prefill_umma_supported(h->pool);
+  const int64_t tile_rows = umma ? kPfTileRowsUmma : kPfTileRows;
   std::vector<int32_t> chunks, tiles;
   int64_t row = 0;
   for (int64_t k = 0; k < n; ++k) {
@@ -514,8 +516,8 @@ chunkattn_status chunkattn_prefill_attend(chunkattn_t h, int32_t layer, int64_t 
     if (first_pos[k] < 0 || first_pos[k] > sq->len) return fail(CA_EINVAL, "first_pos out of range");
     const int32_t off = (int32_t)chunks.size();
     chunks.insert(chunks.end(), sq->path.begin(), sq->path.end());
-    for (int64_t p = first_pos[k]; p < sq->len; p += kPfTileRows) {
-      const int32_t nq = (int32_t)std::min<int64_t>(kPfTileRows, sq->len - p);
+    for (int64_t p = first_pos[k]; p < sq->len; p += tile_rows) {
+      const int32_t nq = (int32_t)std::min<int64_t>(tile_rows, sq->len - p);
       tiles.insert(tiles.end(), {off, (int32_t)(row + p - first_pos[k]), nq, (int32_t)p, (int32_t)sq->len, 0, 0, 0});
     }
     row += sq->len - first_pos[k];
@@ -540,7 +542,8 @@ chunkattn_status chunkattn_prefill_attend(chunkattn_t h, int32_t layer, int64_t 
   a.chunks = a.tiles + tb;
   a.n_tiles = n_tiles;
   a.scale_log2 = h->scale() * 1.4426950408889634f;
-  cudaError_t e = h->timed_launch(chunkattn::K_COPY, st, [&] { return launch_prefill(a, st); });
+  cudaError_t e =
+      h->timed_launch(chunkattn::K_COPY, st, [&] { return umma ? launch_prefill_umma(a, st) : launch_prefill(a, st); });
   if (e != cudaSuccess) return h->cuda_fail(e, "prefill");
   ++h->n_launches;
   return CA_OK;

@@ -100,11 +100,15 @@ CA_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_
 // byte offset of 16-byte group j (of 8) of row r inside a SWIZZLE_128B image
 CA_DEV uint32_t sw128(int r, int j) { return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4)); }
 
-template <typename T, int D, int C>
+// PREFILL (row f1 on tcgen05): CTA = (<= 128 consecutive query positions of
+// one sequence, head); causal mask per row, stale V rows past the sequence end
+// zeroed in shared memory before PV, output O / n in TO (no partials).
+template <typename T, typename TO, int D, int C, bool PREFILL>
 __global__ void __launch_bounds__(kUmThreads, 1)
     cf_umma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                    const T* __restrict__ q, float* __restrict__ pO, DevTables t, int32_t h, int64_t layer_rows,
-                   float scale_log2) {
+                   float scale_log2, TO* __restrict__ out, const int32_t* __restrict__ pf_tiles,
+                   const int32_t* __restrict__ pf_chunks) {
   constexpr int HALVES = D / 64;            // 128-byte d-halves of a token row
   constexpr int PATOMS = C / 64;            // 128-byte token atoms of a P row
   constexpr uint32_t kQBytes = HALVES * kUmRows * 128;
@@ -122,10 +126,26 @@ __global__ void __launch_bounds__(kUmThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int head = blockIdx.y;
-  const int32_t* tile = t.cf_tile + blockIdx.x * kCfTileInts;
-  const int chunk_off = tile[CF_CHUNK_OFF], n_chunks = tile[CF_NCHUNK], row0 = tile[CF_ROW0], row1 = tile[CF_ROW1];
-  const int slot0 = tile[CF_SLOT];
-  const int rows = row1 - row0;
+  int chunk_off, n_chunks, row0, rows, slot0 = 0, pos0 = 0, seq_len = 0;
+  const int32_t* chunk_list;
+  if (PREFILL) {  // {chunk list offset, first query row, queries, first position, sequence length}
+    const int32_t* pt = pf_tiles + (size_t)blockIdx.x * kPfTileInts;
+    chunk_off = pt[0];
+    row0 = pt[1];
+    rows = pt[2];
+    pos0 = pt[3];
+    seq_len = pt[4];
+    n_chunks = (pos0 + rows - 1) / C + 1;
+    chunk_list = pf_chunks;
+  } else {
+    const int32_t* tile = t.cf_tile + blockIdx.x * kCfTileInts;
+    chunk_off = tile[CF_CHUNK_OFF];
+    n_chunks = tile[CF_NCHUNK];
+    row0 = tile[CF_ROW0];
+    rows = tile[CF_ROW1] - row0;
+    slot0 = tile[CF_SLOT];
+    chunk_list = t.cf_chunk;
+  }
   pdl_launch_dependents();
 
   if (tid == 0) {
@@ -161,7 +181,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         const int s = k % kUmStages;
         if (k >= kUmStages) mbar_wait(&S.kv_empty[s], (uint32_t)(((k / kUmStages) - 1) & 1));
         mbar_arrive_expect_tx(&S.kv_full[s], kStageBytes);
-        const int y = (int)(layer_rows + ((int64_t)t.cf_chunk[chunk_off + k] * h + head) * C);
+        const int y = (int)(layer_rows + ((int64_t)chunk_list[chunk_off + k] * h + head) * C);
         unsigned char* st = sKV + s * kStageBytes;
 #pragma unroll
         for (int hf = 0; hf < HALVES; ++hf) {
@@ -214,7 +234,9 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     const int r = tid;  // row of the tile = TMEM lane
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     {  // Q image (SWIZZLE_128B, d-halves), rows past the tile zero
-      const T* qrow = r < rows ? q + ((size_t)t.row_caller[row0 + r] * h + head) * D : nullptr;
+      const T* qrow = r >= rows ? nullptr
+                      : PREFILL ? q + ((size_t)(row0 + r) * h + head) * D
+                                : q + ((size_t)t.row_caller[row0 + r] * h + head) * D;
 #pragma unroll
       for (int g = 0; g < D / 8; ++g) {
         const uint4 v = qrow ? *reinterpret_cast<const uint4*>(qrow + g * 8) : make_uint4(0u, 0u, 0u, 0u);
@@ -236,14 +258,31 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         tmem_ld32(tS0 + b * C + lane_base + c0, u);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c0 + i] = __uint_as_float(u[i]) * scale_log2;
+        for (int i = 0; i < 32; ++i) sv[c0 + i] = __uint_as_float(u[i]);  // raw logits; scale folded below
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&S.s_free[b]);
+      if (PREFILL) {  // causal: row r (position pos0 + r) sees positions <= its own
+        const int lim = pos0 + r - k * C;  // last visible token of this chunk
+        if (lim < C - 1) {                 // only the chunks on the diagonal are masked
+#pragma unroll
+          for (int i = 0; i < C; ++i)
+            if (i > lim) sv[i] = -INFINITY;
+        }
+        const int nt = seq_len - k * C;  // valid tokens of the chunk: zero the stale V rows past them
+        if (nt < C) {
+          unsigned char* vt = sKV + (k % kUmStages) * kStageBytes + kTileBytes;
+          for (int i = r; i < (C - max(nt, 0)) * HALVES * 8; i += 128) {
+            const int row = max(nt, 0) + i / (HALVES * 8), hf = (i / 8) % HALVES, j = i % 8;
+            *reinterpret_cast<uint4*>(vt + hf * C * 128 + sw128(row, j)) = make_uint4(0u, 0u, 0u, 0u);
+          }
+        }
+      }
       float mx = sv[0];
 #pragma unroll
       for (int i = 1; i < C; ++i) mx = fmaxf(mx, sv[i]);
+      mx *= scale_log2;  // scale > 0: the max commutes with it
       // lazy rescale: a new reference max only when this row's max grew by more than 2^8
       const bool need = mx > m_ref + kRescaleLog2;
       if (__any_sync(0xffffffffu, need)) {
@@ -275,7 +314,8 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          w[e] = Mma<T>::pack(fast_exp2(sv[g * 8 + 2 * e] - m_ref), fast_exp2(sv[g * 8 + 2 * e + 1] - m_ref));
+          w[e] = Mma<T>::pack(fast_exp2(fmaf(sv[g * 8 + 2 * e], scale_log2, -m_ref)),
+                              fast_exp2(fmaf(sv[g * 8 + 2 * e + 1], scale_log2, -m_ref)));
           const float2 f2 = Mma<T>::unpack(w[e]);
           n += f2.x + f2.y;
         }
@@ -288,20 +328,35 @@ __global__ void __launch_bounds__(kUmThreads, 1)
     // epilogue: O (unnormalised), m (log2 units), n -> the row's partial
     mbar_wait(&S.o_ready, 0);
     tc_fence_after();
-    float* prow = r < rows ? pO + ((size_t)(slot0 + r) * h + head) * PR : nullptr;
+    if (PREFILL) {  // O / n straight to the output row
+      TO* orow = r < rows ? out + ((size_t)(row0 + r) * h + head) * D : nullptr;
+      const float inv = 1.f / n;
 #pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 32) {
-      uint32_t u[32];
-      tmem_ld32(tO + lane_base + c0, u);
-      tmem_wait_ld();
-      if (prow) {
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t u[32];
+        tmem_ld32(tO + lane_base + c0, u);
+        tmem_wait_ld();
+        if (orow) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(prow + c0 + i) = make_float4(__uint_as_float(u[i]), __uint_as_float(u[i + 1]),
-                                                                 __uint_as_float(u[i + 2]), __uint_as_float(u[i + 3]));
+          for (int i = 0; i < 32; ++i) Elem<TO>::store1(orow + c0 + i, __uint_as_float(u[i]) * inv);
+        }
       }
+    } else {
+      float* prow = r < rows ? pO + ((size_t)(slot0 + r) * h + head) * PR : nullptr;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t u[32];
+        tmem_ld32(tO + lane_base + c0, u);
+        tmem_wait_ld();
+        if (prow) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(prow + c0 + i) = make_float4(__uint_as_float(u[i]), __uint_as_float(u[i + 1]),
+                                                                   __uint_as_float(u[i + 2]), __uint_as_float(u[i + 3]));
+        }
+      }
+      if (prow) *reinterpret_cast<float2*>(prow + D) = make_float2(m_ref, n);
     }
-    if (prow) *reinterpret_cast<float2*>(prow + D) = make_float2(m_ref, n);
   }
   tc_fence_before();
   __syncthreads();
@@ -353,19 +408,28 @@ bool encode_map(const void* base, int64_t rows, int d, int c, CUtensorMap* out) 
   return true;
 }
 
+template <int D, int C>
+constexpr size_t um_smem() {
+  return 1024 + (size_t)(D / 64) * kUmRows * 128 + (size_t)kUmStages * 2 * (D / 64) * C * 128 +
+         (size_t)2 * (C / 64) * kUmRows * 128;
+}
+
+bool pool_maps(const PoolGeom& p, int D, int C, CUtensorMap* mk, CUtensorMap* mv) {
+  const int64_t rows = (int64_t)p.num_layers * p.max_chunks * p.h * p.c;
+  return encode_map(p.k, rows, D, C, mk) && encode_map(p.v, rows, D, C, mv);
+}
+
 template <typename T, int D, int C>
 cudaError_t launch_t(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   const PoolGeom& p = a.pool;
-  const int64_t rows = (int64_t)p.num_layers * p.max_chunks * p.h * p.c;
   CUtensorMap mk, mv;
-  if (!encode_map(p.k, rows, D, C, &mk) || !encode_map(p.v, rows, D, C, &mv)) return cudaErrorNotSupported;
-  constexpr size_t smem = 1024 + (size_t)(D / 64) * kUmRows * 128 + (size_t)kUmStages * 2 * (D / 64) * C * 128 +
-                          (size_t)2 * (C / 64) * kUmRows * 128;
-  auto kern = cf_umma_kernel<T, D, C>;
-  cudaError_t e = set_smem_once((const void*)kern, smem);
+  if (!pool_maps(p, D, C, &mk, &mv)) return cudaErrorNotSupported;
+  auto kern = cf_umma_kernel<T, T, D, C, false>;
+  cudaError_t e = set_smem_once((const void*)kern, um_smem<D, C>());
   if (e != cudaSuccess) return e;
-  return launch_ex(kern, dim3(t.n_cf_tiles, p.h), dim3(kUmThreads), smem, st, a.use_pdl, mk, mv, (const T*)a.q, a.pO,
-                   t, (int32_t)p.h, (int64_t)a.layer * p.max_chunks * p.h * p.c, a.scale_log2);
+  return launch_ex(kern, dim3(t.n_cf_tiles, p.h), dim3(kUmThreads), um_smem<D, C>(), st, a.use_pdl, mk, mv,
+                   (const T*)a.q, a.pO, t, (int32_t)p.h, (int64_t)a.layer * p.max_chunks * p.h * p.c, a.scale_log2,
+                   (T*)nullptr, (const int32_t*)nullptr, (const int32_t*)nullptr);
 }
 
 template <typename T>
@@ -375,12 +439,44 @@ cudaError_t dispatch(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
+template <typename T, typename TO, int D, int C>
+cudaError_t launch_pf(const PrefillLaunch& a, cudaStream_t st) {
+  const PoolGeom& p = a.pool;
+  CUtensorMap mk, mv;
+  if (!pool_maps(p, D, C, &mk, &mv)) return cudaErrorNotSupported;
+  auto kern = cf_umma_kernel<T, TO, D, C, true>;
+  cudaError_t e = set_smem_once((const void*)kern, um_smem<D, C>());
+  if (e != cudaSuccess) return e;
+  return launch_ex(kern, dim3(a.n_tiles, p.h), dim3(kUmThreads), um_smem<D, C>(), st, false, mk, mv, (const T*)a.q,
+                   (float*)nullptr, DevTables{}, (int32_t)p.h, (int64_t)a.layer * p.max_chunks * p.h * p.c,
+                   a.scale_log2, (TO*)a.out, a.tiles, a.chunks);
+}
+
+template <typename T, int D>
+cudaError_t dispatch_pf_out(const PrefillLaunch& a, cudaStream_t st) {
+  switch (a.out_dtype) {
+    case DT_F16: return launch_pf<T, __half, D, 64>(a, st);
+    case DT_BF16: return launch_pf<T, __nv_bfloat16, D, 64>(a, st);
+    case DT_F32: return launch_pf<T, float, D, 64>(a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 }  // namespace
 
 bool cf_umma_supported(const PoolGeom& p, int max_tile_rows) {
   // c = 128 would need 2 x 32 KB P buffers and 64 KB stages: over the shared-memory budget
   return (p.dtype == DT_F16 || p.dtype == DT_BF16) && (p.d == 64 || p.d == 128) && p.c == 64 &&
          max_tile_rows <= kUmRows;
+}
+
+bool prefill_umma_supported(const PoolGeom& p) { return cf_umma_supported(p, kUmRows); }
+
+cudaError_t launch_prefill_umma(const PrefillLaunch& a, cudaStream_t st) {
+  if (a.n_tiles == 0) return cudaSuccess;
+  if (a.pool.dtype == DT_F16)
+    return a.pool.d == 128 ? dispatch_pf_out<__half, 128>(a, st) : dispatch_pf_out<__half, 64>(a, st);
+  return a.pool.d == 128 ? dispatch_pf_out<__nv_bfloat16, 128>(a, st) : dispatch_pf_out<__nv_bfloat16, 64>(a, st);
 }
 
 cudaError_t launch_chunk_first_umma(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {

@@ -92,6 +92,10 @@ struct PrefillLaunch {
   float scale_log2;
 };
 bool prefill_supported(const PoolGeom& pool);
+// tcgen05 prefill (chunk_first_umma.cu, PREFILL mode): tiles of <= kPfTileRowsUmma queries
+constexpr int kPfTileRowsUmma = 128;
+bool prefill_umma_supported(const PoolGeom& pool);
+cudaError_t launch_prefill_umma(const PrefillLaunch& a, cudaStream_t st);
 cudaError_t launch_prefill(const PrefillLaunch& a, cudaStream_t st);
 
 // K1: scatter one decode step's K/V into the leaf chunks and set seq_len.

@@ -20,8 +20,8 @@ def _queries(seed, n, h, d):
     return torch.randn((n, h, d), generator=g, dtype=torch.float64) * 2.0
 
 
-def _run(h, d, c, dt, odt, prompts, seed=0):
-    hs = Harness(h, d, c, dt, odt, seed=seed, alpha=8.0)
+def _run(h, d, c, dt, odt, prompts, seed=0, opts=""):
+    hs = Harness(h, d, c, dt, odt, seed=seed, alpha=8.0, opts=opts)
     ids, firsts = [], []
     for toks in prompts:
         m = hs.ca.match_prefix(toks)
@@ -47,9 +47,12 @@ def _run(h, d, c, dt, odt, prompts, seed=0):
     return err, firsts
 
 
-@pytest.mark.parametrize("h,d,c,dt,odt", [(4, 128, 64, "f16", "f16"), (2, 64, 16, "bf16", "f32"),
-                                          (2, 128, 32, "f16", "f32")])
-def test_prefill_with_prefix_lookup(h, d, c, dt, odt):
+# c = 64 takes the tcgen05 kernel (128-query tiles), other chunk sizes and
+# cf_umma=0 the mma.sync kernel (64-query tiles)
+@pytest.mark.parametrize("h,d,c,dt,odt,opts", [(4, 128, 64, "f16", "f16", ""), (4, 128, 64, "f16", "f16", "cf_umma=0"),
+                                               (2, 64, 64, "bf16", "f32", ""), (2, 64, 16, "bf16", "f32", ""),
+                                               (2, 128, 32, "f16", "f32", "")])
+def test_prefill_with_prefix_lookup(h, d, c, dt, odt, opts):
     sys_prompt = synth.token_ids(3, synth.TAG_SYS, 0, 3 * c + 5).tolist()
     prompts = [
         sys_prompt + synth.token_ids(3, synth.TAG_PRIV, 0, 2 * c + 7).tolist(),   # first: full causal prefill
@@ -57,18 +60,19 @@ def test_prefill_with_prefix_lookup(h, d, c, dt, odt):
         sys_prompt[:c + 3] + synth.token_ids(3, synth.TAG_PRIV, 2, 5).tolist(),   # matches 1 chunk
         sys_prompt[:2 * c] + [11],                                                # two full chunks matched, one query
     ]
-    err, firsts = _run(h, d, c, dt, odt, prompts)
+    err, firsts = _run(h, d, c, dt, odt, prompts, opts=opts)
     assert firsts[0] == 0 and firsts[1] == 3 * c and firsts[2] == c
     assert err <= 2e-3, err
 
 
-def test_prefill_many_tiles_and_ragged_tail():
-    """A 700-token prompt (11 query tiles, ragged last tile and chunk), then two
-    sequences that reuse 10 of its chunks."""
+@pytest.mark.parametrize("opts", ["", "cf_umma=0"])
+def test_prefill_many_tiles_and_ragged_tail(opts):
+    """A 700-token prompt (6 / 11 query tiles, ragged last tile and chunk), then
+    two sequences that reuse 10 of its chunks."""
     c = 64
     base = synth.token_ids(5, synth.TAG_SYS, 0, 700).tolist()
     prompts = [base, base[:650] + [7, 8, 9], base[:640] + synth.token_ids(5, synth.TAG_PRIV, 1, 129).tolist()]
-    err, firsts = _run(2, 128, c, "f16", "f16", prompts, seed=5)
+    err, firsts = _run(2, 128, c, "f16", "f16", prompts, seed=5, opts=opts)
     assert firsts == [0, 640, 640]
     assert err <= 2e-3, err
 
