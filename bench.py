@@ -26,7 +26,10 @@ event time, against MEASURED_PEAKS.json), cpu_baseline (the fp64 oracle on the
 host, bounded sample), e2e (same metric through the C ABI with HOST buffers,
 chunkattn_decode_step_host: H2D of q/k/v and D2H of the output inside the
 call and the timed region),
-gpu_launches, clocks.
+gpu_launches, clocks, and phase_roofline: the two phases timed apart on the
+two-kernel schedule (pass D) -- the sequence-first kernel's algorithmic GB/s
+against the HBM roofline (north_star's sequence-first target) and the tcgen05
+chunk-first kernel's.
 """
 from __future__ import annotations
 
@@ -380,6 +383,30 @@ def run_ours(args):
                    "gbs": kbytes[k] / (kt[k][0] * 1e-3) / 1e9 if kt[k][0] and k in kbytes else None}
                for k in ("append", "chunk_first", "seq_first")}
     step_bytes = sum(x.unique_bytes() for x in shapes)
+    # ---- pass D: the sequence-first phase on its own (two-kernel schedule,
+    # per-kernel events): north_star's ">= 70% of HBM roofline in the
+    # sequence-first phase"; its bytes = private K/V + q + o (+ the partial
+    # rows it merges, an overhead not counted)
+    wl.ca.set_option("fused", 0)
+    wl.fill()
+    wl.ca.set_option("kernel_events", 1)
+    wl.ca.kernel_times()
+    time_steps(wl, K, flush_buf, stream)
+    ktd = wl.ca.kernel_times()
+    wl.ca.set_option("kernel_events", 0)
+    wl.ca.set_option("fused", 1)
+    sf_ms, sf_n = ktd["seq_first"]
+    cf_ms, cf_n = ktd["chunk_first"]
+    sf_bytes = sum(x.seq_first_bytes() for x in shapes)
+    cf_bytes = sum(x.chunk_first_bytes() for x in shapes)
+    sf_gbs = sf_bytes / (sf_ms * 1e-3) / 1e9 if sf_ms > 0 else None
+    phase_split = {
+        "seq_first": {"achieved": sf_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": sf_gbs / hbm_peak if sf_gbs else None,
+                      "avg_launch_us": 1e3 * sf_ms / sf_n if sf_n else None, "alg_bytes_per_launch": sf_bytes / K},
+        "chunk_first": {"achieved": cf_bytes / (cf_ms * 1e-3) / 1e9 if cf_ms > 0 else None, "peak": hbm_peak,
+                        "unit": "GB/s", "avg_launch_us": 1e3 * cf_ms / cf_n if cf_n else None,
+                        "alg_bytes_per_launch": cf_bytes / K, "kernel": "cf_umma_kernel (tcgen05)"},
+        "schedule": "two-kernel (fused=0), per-kernel CUDA events on the launch stream, same steps 1..K"}
     # ---- pass C: end to end through the C ABI with host buffers
     wl.fill()
     e2e_ms, h2d, d2h = time_e2e(wl, K, flush_buf, stream)
@@ -405,6 +432,7 @@ def run_ours(args):
                      "traffic_note": traffic_note,
                      "peak_source": peak_src, "avg_launch_us": 1e3 * dom_ms / dom_n if dom_n else None},
         "kernels": kernels,
+        "phase_roofline": phase_split,
         "step_unique_bytes_avg": step_bytes / K,
         "step_gbs_vs_unique_bytes": step_bytes / (total_ms * 1e-3) / 1e9,
         "passB_ms_per_step": sum(ms_b) / K,
