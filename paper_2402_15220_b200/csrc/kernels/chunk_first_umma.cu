@@ -35,12 +35,6 @@ constexpr int kUmStages = 3;   // K/V ring depth
 constexpr int kUmThreads = 192;  // warps 0-3 softmax/epilogue, 4 TMA producer, 5 MMA issuer
 constexpr float kRescaleLog2 = 8.f;  // lazy O rescale threshold (P <= 2^8)
 
-struct UmShared {
-  uint64_t kv_full[kUmStages], kv_empty[kUmStages];
-  uint64_t s_full[2], s_free[2], p_full[2], pv_done[2];
-  uint64_t q_full, o_ready;
-  uint32_t tmem_base;
-};
 
 CA_DEV uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = (uint64_t)((addr >> 4) & 0x3fff);
@@ -100,29 +94,38 @@ CA_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_
 // byte offset of 16-byte group j (of 8) of row r inside a SWIZZLE_128B image
 CA_DEV uint32_t sw128(int r, int j) { return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4)); }
 
-// PREFILL (row f1 on tcgen05): CTA = (<= 128 consecutive query positions of
-// one sequence, head); causal mask per row, stale V rows past the sequence end
-// zeroed in shared memory before PV, output O / n in TO (no partials).
-template <typename T, typename TO, int D, int C, bool PREFILL>
-__global__ void __launch_bounds__(kUmThreads, 1)
+// PREFILL (row f1 on tcgen05): CTA = (<= 128 NG consecutive query positions
+// of one sequence, head); causal mask per row, stale K/V rows past the
+// sequence end masked (K) and zeroed in shared memory before PV (V), output
+// O / n in TO (no partials).  NG = 2 softmax groups (two 128-row query tiles
+// of the same head) share every K/V stage and ping-pong on the tensor core.
+template <typename T, typename TO, int D, int C, bool PREFILL, int NG>
+__global__ void __launch_bounds__(NG * 128 + 64, 1)
     cf_umma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                    const T* __restrict__ q, float* __restrict__ pO, DevTables t, int32_t h, int64_t layer_rows,
                    float scale_log2, TO* __restrict__ out, const int32_t* __restrict__ pf_tiles,
                    const int32_t* __restrict__ pf_chunks) {
+  constexpr int NST = NG == 1 ? kUmStages : 2;   // K/V ring depth (shared-memory budget)
   constexpr int HALVES = D / 64;            // 128-byte d-halves of a token row
   constexpr int PATOMS = C / 64;            // 128-byte token atoms of a P row
   constexpr uint32_t kQBytes = HALVES * kUmRows * 128;
   constexpr uint32_t kTileBytes = HALVES * C * 128;  // one K (or V) tile image
   constexpr uint32_t kStageBytes = 2 * kTileBytes;
   constexpr uint32_t kPBytes = PATOMS * kUmRows * 128;
-  constexpr uint32_t kTmemCols = 2 * C + D <= 256 ? 256 : 512;
+  constexpr uint32_t kGroupCols = 2 * C + D;        // S double buffer + O per group
+  constexpr uint32_t kTmemCols = NG * kGroupCols <= 256 ? 256 : 512;
+  static_assert(NG * kGroupCols <= 512, "TMEM columns");
   constexpr int PR = D + 4;
+  constexpr int kProducer = 4 * NG, kIssuer = 4 * NG + 1;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sQ = sm;
-  unsigned char* sKV = sQ + kQBytes;
-  unsigned char* sP = sKV + kUmStages * kStageBytes;
-  __shared__ UmShared S;
+  unsigned char* sQ = sm;                       // [NG][kQBytes]
+  unsigned char* sKV = sQ + NG * kQBytes;       // [NST][kStageBytes]
+  unsigned char* sP = sKV + NST * kStageBytes;  // [NG][2][kPBytes]
+  __shared__ uint64_t kv_full[NST], kv_empty[NST];
+  __shared__ uint64_t s_full[NG][2], s_free[NG][2], p_full[NG][2], pv_done[NG][2], q_full[NG];
+  __shared__ uint64_t o_ready;
+  __shared__ uint32_t tmem_base;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int head = blockIdx.y;
@@ -149,107 +152,121 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   pdl_launch_dependents();
 
   if (tid == 0) {
-    for (int s = 0; s < kUmStages; ++s) {
-      mbar_init(&S.kv_full[s], 1);
-      mbar_init(&S.kv_empty[s], 1);
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&S.s_full[b], 1);
-      mbar_init(&S.s_free[b], 4);
-      mbar_init(&S.p_full[b], 4);
-      mbar_init(&S.pv_done[b], 1);
+    for (int g = 0; g < NG; ++g) {
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&s_full[g][b], 1);
+        mbar_init(&s_free[g][b], 4);
+        mbar_init(&p_full[g][b], 4);
+        mbar_init(&pv_done[g][b], 1);
+      }
+      mbar_init(&q_full[g], 4);
     }
-    mbar_init(&S.q_full, 4);
-    mbar_init(&S.o_ready, 1);
+    mbar_init(&o_ready, 1);
     fence_barrier_init();
   }
-  if (warp == 5) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
+  if (warp == kIssuer) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                  "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = S.tmem_base;
-  const uint32_t tS0 = tmem, tO = tmem + 2 * C;
+  const uint32_t tmem = tmem_base;
 
-  if (warp == 4) {
+  if (warp == kProducer) {
     // ---------------------------------------------------------- TMA producer
     if (lane == 0) {
       for (int k = 0; k < n_chunks; ++k) {
-        const int s = k % kUmStages;
-        if (k >= kUmStages) mbar_wait(&S.kv_empty[s], (uint32_t)(((k / kUmStages) - 1) & 1));
-        mbar_arrive_expect_tx(&S.kv_full[s], kStageBytes);
+        const int s = k % NST;
+        if (k >= NST) mbar_wait(&kv_empty[s], (uint32_t)(((k / NST) - 1) & 1));
+        mbar_arrive_expect_tx(&kv_full[s], kStageBytes);
         const int y = (int)(layer_rows + ((int64_t)chunk_list[chunk_off + k] * h + head) * C);
         unsigned char* st = sKV + s * kStageBytes;
 #pragma unroll
         for (int hf = 0; hf < HALVES; ++hf) {
-          tma_load_2d(st + hf * C * 128, &tmap_k, hf * 64, y, &S.kv_full[s]);
-          tma_load_2d(st + kTileBytes + hf * C * 128, &tmap_v, hf * 64, y, &S.kv_full[s]);
+          tma_load_2d(st + hf * C * 128, &tmap_k, hf * 64, y, &kv_full[s]);
+          tma_load_2d(st + kTileBytes + hf * C * 128, &tmap_v, hf * 64, y, &kv_full[s]);
         }
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == kIssuer) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idS = umma_idesc<T>(C, false), idO = umma_idesc<T>(D, true);
       const uint32_t qa = smem_u32(sQ), kva = smem_u32(sKV), pa = smem_u32(sP);
-      mbar_wait(&S.q_full, 0);
+      for (int g = 0; g < NG; ++g) mbar_wait(&q_full[g], 0);
       tc_fence_after();
-      auto issue_pv = [&](int j) {  // O += P_j V_j
-        const int b = j & 1, s = j % kUmStages;
-        mbar_wait(&S.p_full[b], (uint32_t)((j >> 1) & 1));
-        tc_fence_after();
-        const uint32_t va = kva + s * kStageBytes + kTileBytes, pb = pa + b * kPBytes;
+      auto issue_pv = [&](int j) {  // O_g += P_{g,j} V_j for every group, then release the stage
+        const int b = j & 1, s = j % NST;
+        const uint32_t va = kva + s * kStageBytes + kTileBytes;
 #pragma unroll
-        for (int ks = 0; ks < C / 16; ++ks)
-          umma_f16(tO, umma_sdesc(pb + (ks / 4) * kUmRows * 128 + (ks % 4) * 32, 16, 1024),
-                   umma_sdesc(va + ks * 16 * 128, C * 128, 1024), idO, (j > 0 || ks > 0) ? 1u : 0u);
-        umma_commit(&S.pv_done[b]);
-        umma_commit(&S.kv_empty[s]);
+        for (int g = 0; g < NG; ++g) {
+          mbar_wait(&p_full[g][b], (uint32_t)((j >> 1) & 1));
+          tc_fence_after();
+          const uint32_t pb = pa + (g * 2 + b) * kPBytes, tO = tmem + g * kGroupCols + 2 * C;
+#pragma unroll
+          for (int ks = 0; ks < C / 16; ++ks)
+            umma_f16(tO, umma_sdesc(pb + (ks / 4) * kUmRows * 128 + (ks % 4) * 32, 16, 1024),
+                     umma_sdesc(va + ks * 16 * 128, C * 128, 1024), idO, (j > 0 || ks > 0) ? 1u : 0u);
+          umma_commit(&pv_done[g][b]);
+        }
+        umma_commit(&kv_empty[s]);
       };
       for (int k = 0; k < n_chunks; ++k) {
-        const int s = k % kUmStages, b = k & 1;
-        mbar_wait(&S.kv_full[s], (uint32_t)((k / kUmStages) & 1));
-        if (k >= 2) mbar_wait(&S.s_free[b], (uint32_t)(((k >> 1) - 1) & 1));
-        tc_fence_after();
+        const int s = k % NST, b = k & 1;
+        mbar_wait(&kv_full[s], (uint32_t)((k / NST) & 1));
         const uint32_t ka = kva + s * kStageBytes;
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {  // S_k = Q K_k^T over d
-          const uint32_t o = (ks / 4) * 0u + (ks % 4) * 32;
-          umma_f16(tS0 + b * C, umma_sdesc(qa + (ks / 4) * kUmRows * 128 + o, 16, 1024),
-                   umma_sdesc(ka + (ks / 4) * C * 128 + o, 16, 1024), idS, ks > 0 ? 1u : 0u);
+        for (int g = 0; g < NG; ++g) {
+          if (k >= 2) mbar_wait(&s_free[g][b], (uint32_t)(((k >> 1) - 1) & 1));
+          tc_fence_after();
+          const uint32_t qg = qa + g * kQBytes, tS = tmem + g * kGroupCols + b * C;
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {  // S_{g,k} = Q_g K_k^T over d
+            const uint32_t o = (ks % 4) * 32;
+            umma_f16(tS, umma_sdesc(qg + (ks / 4) * kUmRows * 128 + o, 16, 1024),
+                     umma_sdesc(ka + (ks / 4) * C * 128 + o, 16, 1024), idS, ks > 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[g][b]);
         }
-        umma_commit(&S.s_full[b]);
         if (k >= 1) issue_pv(k - 1);
       }
       if (n_chunks > 0) issue_pv(n_chunks - 1);
-      umma_commit(&S.o_ready);
+      umma_commit(&o_ready);
     }
     __syncwarp();
   } else {
     // ------------------------------------------------- softmax / epilogue
-    const int r = tid;  // row of the tile = TMEM lane
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const int g = warp >> 2;            // query group
+    const int r = tid & 127;            // row of the group = TMEM lane
+    const int grow0 = g * kUmRows;      // first row of the group in the tile
+    const int grows = min(kUmRows, rows - grow0);  // valid rows of the group (may be <= 0)
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS0 = tmem + g * kGroupCols, tO = tS0 + 2 * C;
+    unsigned char* sQg = sQ + g * kQBytes;
     {  // Q image (SWIZZLE_128B, d-halves), rows past the tile zero
-      const T* qrow = r >= rows ? nullptr
-                      : PREFILL ? q + ((size_t)(row0 + r) * h + head) * D
-                                : q + ((size_t)t.row_caller[row0 + r] * h + head) * D;
+      const T* qrow = r >= grows ? nullptr
+                      : PREFILL ? q + ((size_t)(row0 + grow0 + r) * h + head) * D
+                                : q + ((size_t)t.row_caller[row0 + grow0 + r] * h + head) * D;
 #pragma unroll
-      for (int g = 0; g < D / 8; ++g) {
-        const uint4 v = qrow ? *reinterpret_cast<const uint4*>(qrow + g * 8) : make_uint4(0u, 0u, 0u, 0u);
-        *reinterpret_cast<uint4*>(sQ + (g / 8) * kUmRows * 128 + sw128(r, g % 8)) = v;
+      for (int gg = 0; gg < D / 8; ++gg) {
+        const uint4 v = qrow ? *reinterpret_cast<const uint4*>(qrow + gg * 8) : make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(sQg + (gg / 8) * kUmRows * 128 + sw128(r, gg % 8)) = v;
       }
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cta(&S.q_full);
+      if (lane == 0) mbar_arrive_cta(&q_full[g]);
     }
     float m_ref = -INFINITY, n = 0.f;
     for (int k = 0; k < n_chunks; ++k) {
       const int b = k & 1;
-      mbar_wait(&S.s_full[b], (uint32_t)((k >> 1) & 1));
+      mbar_wait(&s_full[g][b], (uint32_t)((k >> 1) & 1));
       tc_fence_after();
       float sv[C];
 #pragma unroll
@@ -262,17 +279,22 @@ __global__ void __launch_bounds__(kUmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cta(&S.s_free[b]);
-      if (PREFILL) {  // causal: row r (position pos0 + r) sees positions <= its own
-        const int lim = pos0 + r - k * C;  // last visible token of this chunk
-        if (lim < C - 1) {                 // only the chunks on the diagonal are masked
+      if (lane == 0) mbar_arrive_cta(&s_free[g][b]);
+      if (PREFILL) {
+        // causal: row r (position pos0 + grow0 + r) sees positions <= its own,
+        // and nothing past the sequence end (stale pool rows)
+        const int nt = seq_len - k * C;
+        const int lim = min(pos0 + grow0 + r - k * C, nt - 1);  // last visible token of this chunk
+        if (lim < C - 1) {  // only the chunks on the diagonal / at the end are masked
 #pragma unroll
           for (int i = 0; i < C; ++i)
             if (i > lim) sv[i] = -INFINITY;
         }
-        const int nt = seq_len - k * C;  // valid tokens of the chunk: zero the stale V rows past them
-        if (nt < C) {
-          unsigned char* vt = sKV + (k % kUmStages) * kStageBytes + kTileBytes;
+        // zero the stale V rows of the stage before any P . V reads them: group
+        // 0's P_k is published after this, and the issuer issues group 0's P.V
+        // of chunk k before any other group's
+        if (nt < C && g == 0) {
+          unsigned char* vt = sKV + (k % NST) * kStageBytes + kTileBytes;
           for (int i = r; i < (C - max(nt, 0)) * HALVES * 8; i += 128) {
             const int row = max(nt, 0) + i / (HALVES * 8), hf = (i / 8) % HALVES, j = i % 8;
             *reinterpret_cast<uint4*>(vt + hf * C * 128 + sw128(row, j)) = make_uint4(0u, 0u, 0u, 0u);
@@ -289,7 +311,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         const float m_new = need ? mx : m_ref;
         const float f = (need && m_ref != -INFINITY) ? fast_exp2(m_ref - m_new) : 1.f;
         if (k > 0) {  // O holds chunks 0..k-1: wait for PV_{k-1}, scale it in TMEM
-          mbar_wait(&S.pv_done[(k - 1) & 1], (uint32_t)(((k - 1) >> 1) & 1));
+          mbar_wait(&pv_done[g][(k - 1) & 1], (uint32_t)(((k - 1) >> 1) & 1));
           tc_fence_after();
 #pragma unroll 1
           for (int c0 = 0; c0 < D; c0 += 32) {
@@ -307,29 +329,29 @@ __global__ void __launch_bounds__(kUmThreads, 1)
         m_ref = m_new;
       }
       // P_k = exp2(s - m_ref) rounded to T (n from the rounded P, reading A11)
-      if (k >= 2) mbar_wait(&S.pv_done[b], (uint32_t)(((k >> 1) - 1) & 1));  // PV_{k-2} read this buffer
-      unsigned char* pb = sP + b * kPBytes;
+      if (k >= 2) mbar_wait(&pv_done[g][b], (uint32_t)(((k >> 1) - 1) & 1));  // PV_{k-2} read this buffer
+      unsigned char* pb = sP + (g * 2 + b) * kPBytes;
 #pragma unroll
-      for (int g = 0; g < C / 8; ++g) {
+      for (int gg = 0; gg < C / 8; ++gg) {
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          w[e] = Mma<T>::pack(fast_exp2(fmaf(sv[g * 8 + 2 * e], scale_log2, -m_ref)),
-                              fast_exp2(fmaf(sv[g * 8 + 2 * e + 1], scale_log2, -m_ref)));
+          w[e] = Mma<T>::pack(fast_exp2(fmaf(sv[gg * 8 + 2 * e], scale_log2, -m_ref)),
+                              fast_exp2(fmaf(sv[gg * 8 + 2 * e + 1], scale_log2, -m_ref)));
           const float2 f2 = Mma<T>::unpack(w[e]);
           n += f2.x + f2.y;
         }
-        *reinterpret_cast<uint4*>(pb + (g / 8) * kUmRows * 128 + sw128(r, g % 8)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(pb + (gg / 8) * kUmRows * 128 + sw128(r, gg % 8)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cta(&S.p_full[b]);
+      if (lane == 0) mbar_arrive_cta(&p_full[g][b]);
     }
-    // epilogue: O (unnormalised), m (log2 units), n -> the row's partial
-    mbar_wait(&S.o_ready, 0);
+    // epilogue
+    mbar_wait(&o_ready, 0);
     tc_fence_after();
     if (PREFILL) {  // O / n straight to the output row
-      TO* orow = r < rows ? out + ((size_t)(row0 + r) * h + head) * D : nullptr;
+      TO* orow = r < grows ? out + ((size_t)(row0 + grow0 + r) * h + head) * D : nullptr;
       const float inv = 1.f / n;
 #pragma unroll 1
       for (int c0 = 0; c0 < D; c0 += 32) {
@@ -341,8 +363,8 @@ __global__ void __launch_bounds__(kUmThreads, 1)
           for (int i = 0; i < 32; ++i) Elem<TO>::store1(orow + c0 + i, __uint_as_float(u[i]) * inv);
         }
       }
-    } else {
-      float* prow = r < rows ? pO + ((size_t)(slot0 + r) * h + head) * PR : nullptr;
+    } else {  // O (unnormalised), m (log2 units), n -> the row's partial
+      float* prow = r < grows ? pO + ((size_t)(slot0 + grow0 + r) * h + head) * PR : nullptr;
 #pragma unroll 1
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t u[32];
@@ -360,7 +382,7 @@ __global__ void __launch_bounds__(kUmThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+  if (warp == kIssuer) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
   pdl_wait();  // PDL chain append -> chunk-first -> seq-first (see cf_mma_kernel)
 }
 
@@ -408,11 +430,16 @@ bool encode_map(const void* base, int64_t rows, int d, int c, CUtensorMap* out) 
   return true;
 }
 
-template <int D, int C>
+template <int D, int C, int NG>
 constexpr size_t um_smem() {
-  return 1024 + (size_t)(D / 64) * kUmRows * 128 + (size_t)kUmStages * 2 * (D / 64) * C * 128 +
-         (size_t)2 * (C / 64) * kUmRows * 128;
+  return 1024 + (size_t)NG * (D / 64) * kUmRows * 128 + (size_t)(NG == 1 ? kUmStages : 2) * 2 * (D / 64) * C * 128 +
+         (size_t)NG * 2 * (C / 64) * kUmRows * 128;
 }
+// prefill: 128-query tiles per CTA.  Two groups per CTA sharing the K/V stages
+// (NG = 2, 2-deep ring) measured slower (0.78 vs 0.52 ms on bench_prefill's
+// lookup case: the issuer runs the groups in lock step and half-empty tiles
+// still pay both groups), so one group it is.
+constexpr int kPfGroups = 1;
 
 bool pool_maps(const PoolGeom& p, int D, int C, CUtensorMap* mk, CUtensorMap* mv) {
   const int64_t rows = (int64_t)p.num_layers * p.max_chunks * p.h * p.c;
@@ -424,10 +451,10 @@ cudaError_t launch_t(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   const PoolGeom& p = a.pool;
   CUtensorMap mk, mv;
   if (!pool_maps(p, D, C, &mk, &mv)) return cudaErrorNotSupported;
-  auto kern = cf_umma_kernel<T, T, D, C, false>;
-  cudaError_t e = set_smem_once((const void*)kern, um_smem<D, C>());
+  auto kern = cf_umma_kernel<T, T, D, C, false, 1>;
+  cudaError_t e = set_smem_once((const void*)kern, um_smem<D, C, 1>());
   if (e != cudaSuccess) return e;
-  return launch_ex(kern, dim3(t.n_cf_tiles, p.h), dim3(kUmThreads), um_smem<D, C>(), st, a.use_pdl, mk, mv,
+  return launch_ex(kern, dim3(t.n_cf_tiles, p.h), dim3(kUmThreads), um_smem<D, C, 1>(), st, a.use_pdl, mk, mv,
                    (const T*)a.q, a.pO, t, (int32_t)p.h, (int64_t)a.layer * p.max_chunks * p.h * p.c, a.scale_log2,
                    (T*)nullptr, (const int32_t*)nullptr, (const int32_t*)nullptr);
 }
@@ -444,10 +471,11 @@ cudaError_t launch_pf(const PrefillLaunch& a, cudaStream_t st) {
   const PoolGeom& p = a.pool;
   CUtensorMap mk, mv;
   if (!pool_maps(p, D, C, &mk, &mv)) return cudaErrorNotSupported;
-  auto kern = cf_umma_kernel<T, TO, D, C, true>;
-  cudaError_t e = set_smem_once((const void*)kern, um_smem<D, C>());
+  auto kern = cf_umma_kernel<T, TO, D, C, true, kPfGroups>;
+  cudaError_t e = set_smem_once((const void*)kern, um_smem<D, C, kPfGroups>());
   if (e != cudaSuccess) return e;
-  return launch_ex(kern, dim3(a.n_tiles, p.h), dim3(kUmThreads), um_smem<D, C>(), st, false, mk, mv, (const T*)a.q,
+  return launch_ex(kern, dim3(a.n_tiles, p.h), dim3(kPfGroups * 128 + 64), um_smem<D, C, kPfGroups>(), st, false, mk,
+                   mv, (const T*)a.q,
                    (float*)nullptr, DevTables{}, (int32_t)p.h, (int64_t)a.layer * p.max_chunks * p.h * p.c,
                    a.scale_log2, (TO*)a.out, a.tiles, a.chunks);
 }

@@ -93,7 +93,7 @@ struct PrefillLaunch {
 };
 bool prefill_supported(const PoolGeom& pool);
 // tcgen05 prefill (chunk_first_umma.cu, PREFILL mode): tiles of <= kPfTileRowsUmma queries
-constexpr int kPfTileRowsUmma = 128;
+constexpr int kPfTileRowsUmma = 128;  // one 128-row UMMA group per CTA (chunk_first_umma.cu kPfGroups)
 bool prefill_umma_supported(const PoolGeom& pool);
 cudaError_t launch_prefill_umma(const PrefillLaunch& a, cudaStream_t st);
 cudaError_t launch_prefill(const PrefillLaunch& a, cudaStream_t st);
