@@ -269,13 +269,15 @@ __global__ void __launch_bounds__(NG * 128 + 64, 1)
       mbar_wait(&s_full[g][b], (uint32_t)((k >> 1) & 1));
       tc_fence_after();
       float sv[C];
+      {  // all column blocks in flight, one wait
+        uint32_t u[C / 32][32];
 #pragma unroll
-      for (int c0 = 0; c0 < C; c0 += 32) {
-        uint32_t u[32];
-        tmem_ld32(tS0 + b * C + lane_base + c0, u);
+        for (int cb = 0; cb < C / 32; ++cb) tmem_ld32(tS0 + b * C + lane_base + cb * 32, u[cb]);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c0 + i] = __uint_as_float(u[i]);  // raw logits; scale folded below
+        for (int cb = 0; cb < C / 32; ++cb)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sv[cb * 32 + i] = __uint_as_float(u[cb][i]);  // raw logits; scale folded below
       }
       tc_fence_before();
       __syncwarp();
@@ -301,9 +303,12 @@ __global__ void __launch_bounds__(NG * 128 + 64, 1)
           }
         }
       }
-      float mx = sv[0];
+      float mx8[8];  // 8 independent max chains (a 64-deep chain is latency-bound)
 #pragma unroll
-      for (int i = 1; i < C; ++i) mx = fmaxf(mx, sv[i]);
+      for (int e = 0; e < 8; ++e) mx8[e] = sv[e];
+#pragma unroll
+      for (int i = 8; i < C; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], sv[i]);
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])), fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       mx *= scale_log2;  // scale > 0: the max commutes with it
       // lazy rescale: a new reference max only when this row's max grew by more than 2^8
       const bool need = mx > m_ref + kRescaleLog2;
@@ -331,6 +336,7 @@ __global__ void __launch_bounds__(NG * 128 + 64, 1)
       // P_k = exp2(s - m_ref) rounded to T (n from the rounded P, reading A11)
       if (k >= 2) mbar_wait(&pv_done[g][b], (uint32_t)(((k >> 1) - 1) & 1));  // PV_{k-2} read this buffer
       unsigned char* pb = sP + (g * 2 + b) * kPBytes;
+      float ns[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums of the rounded P
 #pragma unroll
       for (int gg = 0; gg < C / 8; ++gg) {
         uint32_t w[4];
@@ -339,10 +345,11 @@ __global__ void __launch_bounds__(NG * 128 + 64, 1)
           w[e] = Mma<T>::pack(fast_exp2(fmaf(sv[gg * 8 + 2 * e], scale_log2, -m_ref)),
                               fast_exp2(fmaf(sv[gg * 8 + 2 * e + 1], scale_log2, -m_ref)));
           const float2 f2 = Mma<T>::unpack(w[e]);
-          n += f2.x + f2.y;
+          ns[e] += f2.x + f2.y;
         }
         *reinterpret_cast<uint4*>(pb + (gg / 8) * kUmRows * 128 + sw128(r, gg % 8)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
+      n += (ns[0] + ns[1]) + (ns[2] + ns[3]);
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&p_full[g][b]);
