@@ -91,6 +91,26 @@ CA_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+// 32 consecutive fp32 TMEM columns x inv -> 32 output elements, 16-byte stores
+template <typename TO>
+CA_DEV void store_row32(TO* dst, const uint32_t (&u)[32], float inv) {
+  if constexpr (std::is_same<TO, float>::value) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 4)
+      *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(u[i]) * inv, __uint_as_float(u[i + 1]) * inv,
+                                                        __uint_as_float(u[i + 2]) * inv, __uint_as_float(u[i + 3]) * inv);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        w[e] = Mma<TO>::pack(__uint_as_float(u[i + 2 * e]) * inv, __uint_as_float(u[i + 2 * e + 1]) * inv);
+      *reinterpret_cast<uint4*>(dst + i) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
 // byte offset of 16-byte group j (of 8) of row r inside a SWIZZLE_128B image
 CA_DEV uint32_t sw128(int r, int j) { return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4)); }
 
@@ -365,10 +385,7 @@ __global__ void __launch_bounds__(NG * 128 + 64, 1)
         uint32_t u[32];
         tmem_ld32(tO + lane_base + c0, u);
         tmem_wait_ld();
-        if (orow) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) Elem<TO>::store1(orow + c0 + i, __uint_as_float(u[i]) * inv);
-        }
+        if (orow) store_row32<TO>(orow + c0, u, inv);
       }
     } else {  // O (unnormalised), m (log2 units), n -> the row's partial
       float* prow = r < grows ? pO + ((size_t)(slot0 + grow0 + r) * h + head) * PR : nullptr;
