@@ -438,3 +438,27 @@ def test_tcgen05_chunk_first_wide_runs(d, c, dt, odt):
     hs2.step = 1
     hs2.append(ids, decode_tokens(hs2, ids))
     hs2.check(ids, TOL[(dt, odt)])  # the mma.sync chunk-first on the same tree
+
+
+# ------------------------------------------- full-size shapes of the bench ---
+@pytest.mark.parametrize("opts", ["", "fused=0"])
+def test_config2_full_size_last_timed_step(opts):
+    """bench.py's workload at its largest timed step: b = 32, n_s = 2048, 512
+    private tokens (context 2560), 32 x 128 fp16 -- every row, sampled heads
+    checked against the fp64 oracle."""
+    hs = Harness(32, 128, 64, "f16", "f16", seed=0, alpha=8.0, max_chunks=640, opts=opts)
+    ids = build_shared(hs, 2048, [511] * 32)
+    hs.step = 1
+    hs.append(ids, decode_tokens(hs, ids))
+    hs.check(ids, 2e-3, rows=list(range(0, 32, 3)))
+
+
+def test_config5_full_size_sampled_rows():
+    """BASELINE configs[4] on one GPU: b = 256, shared prompt 4096, 64-token
+    private question + the decode token (two-kernel schedule, tcgen05
+    chunk-first): sampled rows against the fp64 oracle."""
+    hs = Harness(32, 128, 64, "f16", "f16", seed=2, alpha=8.0, max_chunks=64 + 256 * 2 + 16)
+    ids = build_shared(hs, 4096, [64] * 256)
+    hs.step = 1
+    hs.append(ids, decode_tokens(hs, ids))
+    hs.check(ids, 2e-3, rows=[0, 1, 63, 127, 128, 200, 255])
