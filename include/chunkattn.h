@@ -221,6 +221,10 @@ chunkattn_status chunkattn_counters(chunkattn_t h, int64_t out[6]);
  *                      0 = the mma.sync kernel
  *   "cf_lane_merge"    1 (default) = the fused kernel merges its token lanes in
  *                      shared memory (one partial per row and job)
+ *   "sf_unit_fixed"    seq-first range split: fixed share of a unit's cost in
+ *                      tenths (default 10 = plain unit counts; below 10 the rest
+ *                      is proportional to the unit's valid tokens)
+ *   "sf_item_cost"     ... plus this per item end, in tenths of a unit (default 0)
  *   "cf_small"         1 = 4-warp chunk-first CTA when tiles have <= 64 rows
  *                      (two-kernel path; default 0)
  *   "sf_ctas"          persistent grid size (default 296 = 2 per SM)

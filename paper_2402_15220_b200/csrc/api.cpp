@@ -719,6 +719,10 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->sopt.cf_unit_cost = value < 1 ? 0.1 : (double)value / 10.0;  // tenths of a seq-first unit
   } else if (k == "cf_lane_merge") {
     h->sopt.cf_lane_merge = value != 0;
+  } else if (k == "sf_unit_fixed") {
+    h->sopt.sf_unit_fixed = value < 0 ? 0.0 : std::min<int64_t>(value, 10) / 10.0;  // tenths
+  } else if (k == "sf_item_cost") {
+    h->sopt.sf_item_cost = value < 0 ? 0.0 : (double)value / 10.0;  // tenths of a unit
   } else if (k == "cf_umma") {
     h->cf_umma = value != 0;
   } else if (k == "cf_small") {

@@ -224,6 +224,31 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   // Fused: chunk-first jobs (tile, head) go first, by longest-processing-time
   // greedy to the least-loaded CTA; the seq-first units then fill every CTA up
   // to the common target (contiguous ranges, proportional to the room left).
+  // seq-first unit costs for the range split: a fixed share per unit plus its
+  // valid-token fraction, plus an item-end (finalize) cost; with the defaults
+  // (fixed 1, item 0) every unit weighs 1 (plain unit counts)
+  std::vector<double> ucost_pre((size_t)U + 1, 0.0);
+  {
+    const double a = opt.sf_unit_fixed, wf = opt.sf_item_cost;
+    int64_t u = 0;
+    for (int32_t r = 0; r < b; ++r) {
+      const int32_t n = sf_ptr[r + 1] - sf_ptr[r], per = std::max<int32_t>(1, n);
+      const int32_t last_tok = n > 0 ? std::min<int32_t>(c, seq_len[r] - sf_first[r] - (per - 1) * c) : 0;
+      for (int32_t hh = 0; hh < H; ++hh)
+        for (int32_t k = 0; k < per; ++k, ++u) {
+          const double frac = n == 0 ? 0.0 : (k < per - 1 ? 1.0 : (double)last_tok / c);
+          ucost_pre[u + 1] = ucost_pre[u] + a + (1.0 - a) * frac + (k == per - 1 ? wf : 0.0);
+        }
+    }
+  }
+  const double T_sf = ucost_pre[U];
+  auto unit_at = [&](double cost) -> int64_t {  // first unit whose prefix cost reaches `cost`
+    if (cost <= 0) return 0;
+    if (cost >= T_sf) return U;
+    const int64_t i = std::lower_bound(ucost_pre.begin(), ucost_pre.end(), cost) - ucost_pre.begin();
+    // round to the nearer boundary
+    return (i > 0 && cost - ucost_pre[i - 1] < ucost_pre[i] - cost) ? i - 1 : i;
+  };
   std::vector<int64_t> ubound(G + 1, 0);
   std::vector<int32_t> cf_unit;
   std::vector<int32_t> cf_range(2 * G, 0);
@@ -242,7 +267,7 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
       load[best] += (double)(-jb.first) * opt.cf_unit_cost;
       mine[best].push_back(jb.second);
     }
-    double total = (double)U;
+    double total = T_sf;
     for (double l : load) total += l;
     const double target = total / (double)G;
     std::vector<double> room(G);
@@ -250,7 +275,7 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
     for (int64_t g = 0; g < G; ++g) room_sum += (room[g] = std::max(0.0, target - load[g]));
     double acc = 0;
     for (int64_t g = 0; g < G; ++g) {
-      ubound[g] = room_sum > 0 ? (int64_t)std::llround((double)U * acc / room_sum) : U * g / G;
+      ubound[g] = room_sum > 0 ? unit_at(T_sf * acc / room_sum) : U * g / G;
       acc += room[g];
       cf_range[2 * g] = (int32_t)(cf_unit.size() / kCfUnitInts);
       for (int64_t job : mine[g]) {
@@ -265,7 +290,7 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
     }
     ubound[G] = U;
   } else {
-    for (int64_t g = 0; g <= G; ++g) ubound[g] = G > 0 ? U * g / G : 0;
+    for (int64_t g = 0; g <= G; ++g) ubound[g] = G > 0 ? unit_at(T_sf * (double)g / (double)G) : 0;
   }
   X.n_cf_units = (int32_t)(cf_unit.size() / kCfUnitInts);
   X.fused = opt.fused && X.n_cf_tiles > 0;
