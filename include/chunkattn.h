@@ -221,6 +221,7 @@ chunkattn_status chunkattn_counters(chunkattn_t h, int64_t out[6]);
  *                      0 = the mma.sync kernel
  *   "cf_lane_merge"    1 (default) = the fused kernel merges its token lanes in
  *                      shared memory (one partial per row and job)
+ *   "fused_tile_rows"  fused chunk-first tile rows, 16..64 (default 64)
  *   "sf_unit_fixed"    seq-first range split: fixed share of a unit's cost in
  *                      tenths (default 10 = plain unit counts; below 10 the rest
  *                      is proportional to the unit's valid tokens)

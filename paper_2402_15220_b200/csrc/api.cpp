@@ -719,6 +719,8 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->sopt.cf_unit_cost = value < 1 ? 0.1 : (double)value / 10.0;  // tenths of a seq-first unit
   } else if (k == "cf_lane_merge") {
     h->sopt.cf_lane_merge = value != 0;
+  } else if (k == "fused_tile_rows") {
+    h->sopt.fused_tile_rows = value;
   } else if (k == "sf_unit_fixed") {
     h->sopt.sf_unit_fixed = value < 0 ? 0.0 : std::min<int64_t>(value, 10) / 10.0;  // tenths
   } else if (k == "sf_item_cost") {

@@ -102,7 +102,8 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
         return build_context(tree, o2, ctx, err);
       }
   }
-  const int64_t tile_rows = opt.fused ? kFusedTileRows : kMaxCfTileRows;
+  const int64_t tile_rows = opt.fused ? std::min<int64_t>(kFusedTileRows, std::max<int64_t>(16, opt.fused_tile_rows))
+                                      : kMaxCfTileRows;
   auto lanes_of = [&](const RunTiling& t) { return opt.fused ? fused_lanes(t.rows_per_tile) : 1; };
   // partials per row: the fused kernel merges its L lanes in the stage's K/V
   // tiles when the (4 - G) foreign lane states fit there

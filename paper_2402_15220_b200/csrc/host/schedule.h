@@ -57,6 +57,7 @@ struct ScheduleOptions {
   int64_t sf_ctas = 296;           // persistent seq-first grid (<= kMaxSfCtas)
   bool fused = false;              // chunk-first units run inside the persistent seq-first kernel
   double cf_unit_cost = 1.6;       // fused balance: cost of a chunk-first unit in seq-first units (swept on cfg2)
+  int64_t fused_tile_rows = kFusedTileRows;  // fused chunk-first tile rows (16..64): smaller = more, lighter jobs
   double sf_unit_fixed = 1.0;       // seq-first range split: fixed share of a unit's cost (1 = unit counts)
   double sf_item_cost = 0.0;        // ... plus this per item end (finalize), in units
   int32_t head_dim = 128;          // fused lane merge: scratch bytes vs the stage's K/V tiles
