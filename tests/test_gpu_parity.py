@@ -198,9 +198,12 @@ def test_split_invariance_and_simt_chunk_first(dt, odt):
             hs.ca.set_option(opt, 0)
 
 
-def test_layers_independent():
-    hs = Harness(4, 64, 16, "f16", "f16", num_layers=2, seed=15, alpha=8.0)
-    ids = build_shared(hs, 48, [0, 5, 20])
+@pytest.mark.parametrize("c,opts", [(16, ""), (64, ""), (64, "fused=0")])
+def test_layers_independent(c, opts):
+    """Two layers share one tree; each layer's attention reads its own pool
+    slice (c = 64 with fused=0: the tcgen05 chunk-first's TMA row offset)."""
+    hs = Harness(4, 64, c, "f16", "f16", num_layers=2, seed=15, alpha=8.0, opts=opts)
+    ids = build_shared(hs, 3 * c, [0, 5, c + 20])
     for layer in (0, 1):
         hs.check(ids, 2e-3, layer=layer)
 

@@ -86,3 +86,18 @@ def test_prefill_empty_and_errors():
         hs.ca.prefill_attend([sid], [100], q)  # first_pos past the end
     with pytest.raises(Exception):
         hs.ca.prefill_attend([sid + 7], [0], torch.zeros((99, 2, 128), dtype=torch.float16, device=hs.dev))
+
+
+def test_prefill_second_layer():
+    """prefill_attend on layer 1 of a two-layer pool (tcgen05 kernel, c = 64)."""
+    from oracle.prefill import causal_prefill_fp64 as ref_fn
+    hs = Harness(2, 128, 64, "f16", "f16", num_layers=2, seed=9, alpha=8.0)
+    toks = synth.token_ids(9, synth.TAG_SYS, 0, 150).tolist()
+    sid, _ = hs.add(toks)
+    q = _queries(10, len(toks), 2, 128)
+    out = hs.ca.prefill_attend([sid], [0], q.to(hs.dev, hs.dt).contiguous(), layer=1)
+    torch.cuda.synchronize()
+    K, V = hs.kv(toks, list(range(len(toks))))
+    ref = ref_fn(q.to(hs.dt).double().numpy(), K.to(hs.dt).double().cpu().numpy()[:, 1],
+                 V.to(hs.dt).double().cpu().numpy()[:, 1], 0, default_scale(128))
+    assert float(np.abs(out.double().cpu().numpy() - ref).max()) <= 2e-3
