@@ -159,6 +159,14 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
   constexpr int PR = D + 4;
   const size_t tile_bytes = (size_t)c * D * sizeof(T);
   int jj = 0;
+  int rs = 0;         // ring slot of unit jj (jj % nst without a division per unit)
+  uint32_t rph = 0;   // its phase parity ((jj / nst) & 1)
+  auto ring_next = [&] {
+    if (++rs == nst) {
+      rs = 0;
+      rph ^= 1u;
+    }
+  };
   bool waited = false;  // PDL: append (new token, seq_len) and chunk-first (partials) complete
   // Fused chunk-first units first (shared chunks: untouched by this step's
   // append, so no PDL wait): full K and V tiles of (chunk, head).
@@ -172,8 +180,8 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
       const int i_tile = __shfl_sync(0xffffffffu, d.y, i);
       const int i_head = __shfl_sync(0xffffffffu, d.z, i);
       const int i_kf = __shfl_sync(0xffffffffu, d.w, i);
-      const int s = jj % nst;
-      if (jj >= nst) mbar_wait(&S.empty_bar[s], (uint32_t)(((jj / nst) - 1) & 1));
+      const int s = rs;
+      if (jj >= nst) mbar_wait(&S.empty_bar[s], rph ^ 1u);
       if (lane == 0) {
         const int fl = F_CF | ((i_kf & 1) ? F_FIRST : 0) | ((i_kf & 2) ? F_LAST : 0);
         S.meta[s] = StageMeta{i_tile, c, fl, i_head, 0, 0, i_kf >> 2, 0};
@@ -190,6 +198,7 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
       }
       __syncwarp();
       ++jj;
+      ring_next();
     }
   }
   for (int base = u0; base < u1; base += 32) {
@@ -265,11 +274,11 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
 #ifdef CA_HANG_CHECK
       if (i_chunk >= 0 && (i_nt <= 0 || i_nt > c)) CA_HANG_TRAP("bad token count", i_item, i_nt);
 #endif
-      const int s = jj % nst;
+      const int s = rs;
       const int head = i_item % h;
       const bool want_q = (i_flags & F_FIRST) && i_chunk >= 0;
       const int np = want_p ? min(i_mg1 - i_mg0, kMaxPrefetchSlots) : 0;
-      if (jj >= nst) mbar_wait(&S.empty_bar[s], (uint32_t)(((jj / nst) - 1) & 1));
+      if (jj >= nst) mbar_wait(&S.empty_bar[s], rph ^ 1u);
       unsigned char* st = smem_raw + (size_t)s * stage_bytes;
       const uint32_t kv_bytes = (uint32_t)(i_nt * D * (int)sizeof(T));
       const uint32_t q_bytes = want_q ? (uint32_t)(D * sizeof(T)) : 0u;
@@ -312,6 +321,7 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
         tr[6 + 4 * jj] = 2 * kv_bytes + q_bytes + p_bytes;
       }
       ++jj;
+      ring_next();
     }
   }
 }
@@ -583,6 +593,14 @@ __global__ void __launch_bounds__(kSfThreads, 2) sf_persistent_kernel(
   const int ct = tid - 32;  // 0..127
   const int cw = warp - 1;  // consumer warp 0..3
   int jj = 0;
+  int rs = 0;        // ring slot / phase of unit jj, advanced without divisions
+  uint32_t rph = 0;
+  auto ring_next = [&] {
+    if (++rs == nst) {
+      rs = 0;
+      rph ^= 1u;
+    }
+  };
   if constexpr (MMA) {
     using WA = WarpAttn<T, D, TPW>;
     constexpr int PR = D + 4;
@@ -598,6 +616,7 @@ __global__ void __launch_bounds__(kSfThreads, 2) sf_persistent_kernel(
       const int cf0 = t.fused ? t.sf_cta[blockIdx.x * kSfCtaInts + 2] : 0;
       const int cf1 = t.fused ? t.sf_cta[blockIdx.x * kSfCtaInts + 3] : 0;
       int cfL = 1, cfP = 1, cfg = 0, cfl = 0, crow0 = 0, crows = 0, cslot = 0;
+      int c_altm = 0, c_sel = 0, c_span = c, c_tb = 0;  // this warp's chunk / token slice of the job
       bool cact = false;
       // a job's tile record and Q fragments (dependent global loads): the
       // CTA's first job is begun at kernel start, overlapping the first copies
@@ -611,6 +630,14 @@ __global__ void __launch_bounds__(kSfThreads, 2) sf_persistent_kernel(
         cfg = cw / cfL;
         cfl = cw % cfL;
         cact = cfg * 16 < crows;
+        {  // lane l: token slice l % nsl of every alt-th chunk (nsl, alt powers of two)
+          int nsl = cfL;  // slices per chunk: divides cfL and c / 16, >= kCfSlice tokens each
+          while (nsl > 1 && (nsl * kCfSlice > c || (c / 16) % nsl != 0)) nsl >>= 1;
+          c_altm = cfL / nsl - 1;
+          c_sel = cfl / nsl;
+          c_span = c / nsl;
+          c_tb = (cfl % nsl) * c_span;
+        }
         wa.reset();
         const int rlo = crow0 + cfg * 16 + (lane >> 2), rhi = rlo + 8;
         const T* qlo = (cact && rlo < crow0 + crows) ? q + ((size_t)t.row_caller[rlo] * h + head) * D : nullptr;
@@ -628,9 +655,9 @@ __global__ void __launch_bounds__(kSfThreads, 2) sf_persistent_kernel(
         const int4 d0 = *reinterpret_cast<const int4*>(t.cf_unit + (size_t)cf0 * kCfUnitInts);
         begin_job(d0.y, d0.z);
       }
-      for (int u = cf0; u < cf1; ++u, ++jj) {
-        const int s = jj % nst;
-        mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
+      for (int u = cf0; u < cf1; ++u, ++jj, ring_next()) {
+        const int s = rs;
+        mbar_wait(&S.full_bar[s], rph);
         if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 4 * jj] = globaltimer_ns();
         const StageMeta md = S.meta[s];
         const int tile = md.item, head = md.caller, k = md.seg;
@@ -638,16 +665,14 @@ __global__ void __launch_bounds__(kSfThreads, 2) sf_persistent_kernel(
         // lane l of the job: token slice l % nsl (>= 32 tokens when the chunk
         // has them) of every alt-th chunk (k % alt == l / nsl): all warps work
         // on each unit, and each mma call covers 32-64 tokens (independent
-        // accumulator chains; 16-token calls are latency-bound)
-        int nsl = cfL;  // slices per chunk: divides cfL and c / 16, >= kCfSlice tokens each
-        while (nsl > 1 && (nsl * kCfSlice > c || (c / 16) % nsl != 0)) nsl >>= 1;
-        const int alt = cfL / nsl;
-        if (cact && (k % alt) == cfl / nsl && !diag_nocompute) {
+        // accumulator chains; 16-token calls are latency-bound).  Resolved once
+        // per job (begin_job): no integer division per unit.
+        if (cact && (k & c_altm) == c_sel && !diag_nocompute) {
           const uint32_t k_u32 = smem_u32(smem_raw + (size_t)s * stage_bytes), v_u32 = k_u32 + (uint32_t)tile_bytes;
-          const int span = c / nsl, tb = (cfl % nsl) * span;
-          int t0 = tb;
-          for (; t0 + 32 <= tb + span; t0 += 32) wa.template chunk<false, 32>(qa, k_u32, v_u32, t0, c, scale_log2, lane);
-          for (; t0 < tb + span; t0 += 16) wa.template chunk<false, 16>(qa, k_u32, v_u32, t0, c, scale_log2, lane);
+          int t0 = c_tb;
+          for (; t0 + 32 <= c_tb + c_span; t0 += 32)
+            wa.template chunk<false, 32>(qa, k_u32, v_u32, t0, c, scale_log2, lane);
+          for (; t0 < c_tb + c_span; t0 += 16) wa.template chunk<false, 16>(qa, k_u32, v_u32, t0, c, scale_log2, lane);
         }
         if (md.flags & F_LAST) {
           wa.finish();
@@ -739,9 +764,9 @@ __global__ void __launch_bounds__(kSfThreads, 2) sf_persistent_kernel(
       }
       wa.reset();
     }
-    for (int u = u0; u < u1; ++u, ++jj) {
-      const int s = jj % nst;
-      mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
+    for (int u = u0; u < u1; ++u, ++jj, ring_next()) {
+      const int s = rs;
+      mbar_wait(&S.full_bar[s], rph);
       if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 4 * jj] = globaltimer_ns();
       const StageMeta md = S.meta[s];
       const unsigned char* st = smem_raw + (size_t)s * stage_bytes;
@@ -785,9 +810,9 @@ __global__ void __launch_bounds__(kSfThreads, 2) sf_persistent_kernel(
     const int g = ct / G::kTpt, j = ct % G::kTpt;
     float qf[G::kVec];
     float m = -INFINITY, n = 0.f, o[G::kVec];
-    for (int u = u0; u < u1; ++u, ++jj) {
-      const int s = jj % nst;
-      mbar_wait(&S.full_bar[s], (uint32_t)((jj / nst) & 1));
+    for (int u = u0; u < u1; ++u, ++jj, ring_next()) {
+      const int s = rs;
+      mbar_wait(&S.full_bar[s], rph);
       if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 4 * jj] = globaltimer_ns();
       const StageMeta md = S.meta[s];
       const unsigned char* st = smem_raw + (size_t)s * stage_bytes;
