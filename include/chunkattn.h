@@ -154,6 +154,28 @@ chunkattn_status chunkattn_remove_sequence(chunkattn_t h, int64_t seq_id, int64_
 chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const int64_t* seq_ids,
                                   const void* q, void* out, void* stream);
 
+/* One decode step of one layer in ONE kernel launch (SURVEY §8 a4 + a5 + a6):
+ * append one token per sequence (PAPER.md:507 scenario iii: "append new
+ * tokens into leaf chunks or grow a new chunk when the leaf chunk is full")
+ * and attend (Alg 1 + Alg 2 + Eqn 2) for ALL live sequences;
+ * the query attends to its own new key (reading A8).
+ *   layer    0 advances the tree by one token per sequence (lazy context
+ *            rebuild and upload on a structural change); for
+ *            num_layers > 1 call layers 1..L-1 of the same step after layer 0
+ *            (they only scatter their K/V and attend; tokens is ignored)
+ *   seq_ids  host int64[n], n == live count, distinct, any order
+ *   tokens   host int32[n] (layer 0), the new token of seq_ids[k]
+ *   k, v     device [n][h][d] dtype: THIS layer's new K/V rows, seq_ids order
+ *   q        device [n][h][d] dtype;  out  device [n][h][d] out_dtype
+ * The K/V scatter happens inside the attention kernel (the cluster decode
+ * kernel K5): 16-bit dtype, d in {64, 128}, c in {16, 32, 48,
+ * 64, 96, 128}.  Other shapes run append_kv + attend (num_layers == 1 only,
+ * CA_EDTYPE otherwise).  Errors before the launch leave the state unchanged.
+ * Asynchronous on `stream`. */
+chunkattn_status chunkattn_append_attend(chunkattn_t h, int32_t layer, int64_t n, const int64_t* seq_ids,
+                                         const int32_t* tokens, const void* k, const void* v, const void* q,
+                                         void* out, void* stream);
+
 /* Prefill attention with prefix lookup (§2.2/§3.1):
  * after add_sequence matched a cached prefix and wrote the K/V of the rest,
  * every query position p >= first_pos[k] of sequence seq_ids[k] attends
@@ -203,9 +225,23 @@ chunkattn_status chunkattn_memory_stats(chunkattn_t h, int64_t out[6]);
  *           kernels launched, current epoch, partial slots of the context}. */
 chunkattn_status chunkattn_counters(chunkattn_t h, int64_t out[6]);
 
+/* Schedule of the current context (built by the last append / attend):
+ * out[8] = {K5 cluster decode in use (0/1), K5 cluster size, K5 groups
+ * (row blocks x head sets), K5 row blocks, K5 work units, K5 heads per
+ * group, persistent fused schedule (0/1), persistent grid CTAs}. */
+chunkattn_status chunkattn_schedule_info(chunkattn_t h, int64_t out[8]);
+
 /* Tuning / test knobs (scheduling only; any setting gives the same result
  * within rounding, and a fixed setting is bitwise reproducible).  Unknown keys
  * fail with CA_EINVAL.
+ *   "dk"               1 (default) = the cluster decode kernel K5 (one launch:
+ *                      append + both phases + the cluster merge) when the shape
+ *                      allows; 0 = the persistent-kernel paths below
+ *   "dk_cs"            0 = auto (largest cluster with all (row block, head)
+ *                      groups co-resident), else force the cluster size 1..16
+ *   "dk_max_rows"      rows per K5 row block, 16..64 (default 64)
+ *   "dk_shared_fixed", "dk_shared_row", "dk_pack_fixed"  K5 work-split unit
+ *                      costs (hundredths / thousandths; defaults 100, 10, 15)
  *   "fused"            1 (default) = both phases in one persistent launch
  *                      (chunk-first units first in each CTA, last-contributor
  *                      merges); 0 = chunk-first kernel + seq-first kernel
@@ -241,7 +277,9 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
  * stream around every kernel launch while the option "kernel_events" is 1
  * (PDL is not used between the two phases in that mode).  Synchronises on the
  * recorded events, accumulates, and resets the accumulators.
- *   ms[4]       total milliseconds of {append, chunk_first, seq_first, copy}
+ *   ms[4]       total milliseconds of {append, chunk_first, seq_first, copy};
+ *               "seq_first" = the attention kernel (persistent seq-first,
+ *               fused, or the K5 cluster decode kernel)
  *   launches[4] launches of each kind that were timed */
 chunkattn_status chunkattn_kernel_times(chunkattn_t h, double ms[4], int64_t launches[4]);
 

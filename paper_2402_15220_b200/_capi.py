@@ -67,6 +67,8 @@ _SIGS = {
     "chunkattn_append_kv": (ctypes.c_int, [_P, ctypes.c_int64, _I64P, _I32P, _P, _P, _P]),
     "chunkattn_remove_sequence": (ctypes.c_int, [_P, ctypes.c_int64, _I64P]),
     "chunkattn_attend": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _I64P, _P, _P, _P]),
+    "chunkattn_append_attend": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _I64P, _I32P, _P, _P, _P, _P,
+                                               _P]),
     "chunkattn_prefill_attend": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _I64P, _I64P, _P, _P, _P]),
     "chunkattn_decode_step_host": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int64, _I64P, _P, _P, _P, _P,
                                                   ctypes.c_size_t, _P]),
@@ -74,6 +76,7 @@ _SIGS = {
     "chunkattn_export_context": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
     "chunkattn_memory_stats": (ctypes.c_int, [_P, _I64P]),
     "chunkattn_counters": (ctypes.c_int, [_P, _I64P]),
+    "chunkattn_schedule_info": (ctypes.c_int, [_P, _I64P]),
     "chunkattn_set_option": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.c_int64]),
     "chunkattn_kernel_times": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double), _I64P]),
     "chunkattn_download_tables": (ctypes.c_int, [_P, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), _P]),

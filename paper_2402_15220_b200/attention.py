@@ -152,6 +152,35 @@ class ChunkAttention:
         C.check(self.lib.chunkattn_attend(self._h, layer, n, _p64(ids), qp, op, self._stream()))
         return out
 
+    def append_attend(self, seq_ids: Sequence[int], tokens: Sequence[int] | None, k: torch.Tensor,
+                      v: torch.Tensor, q: torch.Tensor, layer: int = 0,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+        """One decode step of one layer in one launch (chunkattn_append_attend):
+        k, v [n][h][d] this layer's new K/V rows, q [n][h][d], all in seq_ids
+        order; tokens (layer 0) the new token per sequence -> out [n][h][d]."""
+        ids = _i64(seq_ids)
+        n = len(ids)
+        t = _i32(tokens if tokens is not None else [])
+        if layer == 0 and len(t) != n:
+            raise ValueError("tokens and seq_ids differ in length")
+        kp = self._dev(k, (n, self.h, self.d), "k")
+        vp = self._dev(v, (n, self.h, self.d), "v")
+        qp = self._dev(q, (n, self.h, self.d), "q")
+        if out is None:
+            out = torch.empty((n, self.h, self.d), dtype=self.out_dtype, device=self.device)
+        op = self._dev(out, (n, self.h, self.d), "out", self.out_dtype)
+        C.check(self.lib.chunkattn_append_attend(self._h, layer, n, _p64(ids), _p32(t) if len(t) else None, kp, vp,
+                                                 qp, op, self._stream()))
+        return out
+
+    def append_attend_raw(self, ids: np.ndarray, toks: np.ndarray, k_ptr: int, v_ptr: int, q_ptr: int,
+                          out_ptr: int, stream_ptr: int, layer: int = 0) -> None:
+        """Pre-marshalled append_attend for timing loops."""
+        C.check(self.lib.chunkattn_append_attend(self._h, layer, len(ids), _p64(ids), _p32(toks),
+                                                 ctypes.c_void_p(k_ptr), ctypes.c_void_p(v_ptr),
+                                                 ctypes.c_void_p(q_ptr), ctypes.c_void_p(out_ptr),
+                                                 ctypes.c_void_p(stream_ptr)))
+
     def prefill_attend(self, seq_ids: Sequence[int], first_pos: Sequence[int], q: torch.Tensor,
                        layer: int = 0, out: torch.Tensor | None = None) -> torch.Tensor:
         """Causal prefill attention of positions first_pos[k].. of each sequence
@@ -215,6 +244,11 @@ class ChunkAttention:
         a = (ctypes.c_int64 * 6)()
         C.check(self.lib.chunkattn_counters(self._h, a))
         return dict(zip(["builds", "uploads", "upload_bytes", "launches", "epoch", "slots"], list(a)))
+
+    def schedule_info(self) -> dict:
+        a = (ctypes.c_int64 * 8)()
+        C.check(self.lib.chunkattn_schedule_info(self._h, a))
+        return dict(zip(["dk", "dk_cs", "dk_groups", "dk_blocks", "dk_units", "dk_hg", "fused", "sf_ctas"], list(a)))
 
     def set_option(self, key: str, value: int) -> None:
         C.check(self.lib.chunkattn_set_option(self._h, key.encode(), int(value)))

@@ -49,6 +49,12 @@ bool valid_config(const chunkattn_config* c, std::string* why) {
   if (c->max_seq_len < 1 || c->max_seq_len > (1LL << 30)) return (*why = "bad max_seq_len", false);
   if ((int64_t)c->num_layers * c->max_chunks * c->num_heads * c->chunk_size > (1LL << 31) - 1)
     return (*why = "pool too large for 32-bit row coordinates", false);
+  // the persistent seq-first kernel double-buffers (chunk, head) K/V tiles in
+  // shared memory: two stages must fit the per-CTA opt-in limit
+  if (seq_first_min_smem(c->dtype, c->chunk_size, c->head_dim) > kMaxSmemPerCta)
+    return (*why = "chunk_size x head_dim too large for this dtype (two K/V tile stages exceed 227 KB of shared "
+                   "memory; f32 needs chunk_size * head_dim <= 8192, 16-bit <= 16384)",
+            false);
   return true;
 }
 
@@ -63,7 +69,10 @@ WsLayout ws_layout(const chunkattn_config* c) {
                 (int64_t)kSfItemInts * B * c->num_heads + 4 +
                 (int64_t)kSfUnitInts * c->num_heads * B * (msc + 1) + 4 +
                 (w.slot_cap + 4) +                                      // mg_tile
-                (int64_t)kCfUnitInts * c->num_heads * w.slot_cap + 4;  // fused chunk-first units
+                (int64_t)kCfUnitInts * c->num_heads * w.slot_cap + 4 +  // fused chunk-first units
+                (B + 4) +                                                   // second length buffer (K5)
+                (int64_t)kDkUnitInts * (std::max<int64_t>(B, kDkMaxRows) * msc + 4) +  // K5 units
+                (int64_t)(kDkCtaInts * kDkMaxCluster + kDkBlockInts) * (B / kDkMaxRows + 2) + 8;
   size_t o = 0;
   w.attend_perm = o;
   o = align_up(o + 4 * B, 256);
@@ -123,6 +132,19 @@ struct chunkattn {
   bool use_pdl = true;
   int num_sms = 148;
   int64_t cf_cpt_forced = 0;
+  bool dk_opt = true;         // K5 cluster decode kernel when the shape allows (option "dk")
+  int len_parity = 0;         // K5: which of the two device length buffers is current
+  int64_t sf_ctas_req = 296;  // requested persistent grid (option sf_ctas / sf_ctas_per_sm)
+  int resident_cache = -1;    // occupancy x SMs of the persistent kernel (per residency setting)
+
+  int64_t resident_sf_ctas() {
+    if (host_only) return sf_ctas_req;
+    if (resident_cache < 0) {
+      const int r = seq_first_resident_ctas(pool, cfg.out_dtype, sf_ctas_per_sm, !sf_simt);
+      resident_cache = r > 0 ? r : num_sms;  // query failed: one CTA per SM is always resident
+    }
+    return resident_cache;
+  }
   // staging
   int32_t* pinned[2] = {nullptr, nullptr};
   cudaEvent_t ev[2] = {nullptr, nullptr};
@@ -205,6 +227,71 @@ struct chunkattn {
 
   float scale() const { return cfg.scale > 0.f ? cfg.scale : 1.0f / std::sqrt((float)cfg.head_dim); }
 
+  PoolGeom geom() const {
+    PoolGeom g = pool;
+    g.h = cfg.num_heads;
+    g.c = cfg.chunk_size;
+    g.d = cfg.head_dim;
+    g.num_layers = cfg.num_layers;
+    g.dtype = cfg.dtype;
+    return g;
+  }
+  int32_t* other_len() const {
+    int32_t* base = reinterpret_cast<int32_t*>(wsp + ws.tables);
+    return base + (len_parity ? ctx.lay.seq_len : ctx.lay.seq_len2);
+  }
+
+  // Attend permutation (row -> caller index), uploaded when the ids or the
+  // tree changed; validates the ids first.
+  chunkattn_status prepare_attend(int64_t n, const int64_t* seq_ids, cudaStream_t st) {
+    const bool same = attend_epoch == tree.epoch() && (int64_t)attend_ids.size() == n &&
+                      (n == 0 || std::memcmp(attend_ids.data(), seq_ids, n * sizeof(int64_t)) == 0);
+    if (!same) {
+      for (int64_t i = 0; i < n; ++i)
+        if (!tree.find(seq_ids[i])) return fail(CA_ENOSEQ, "unknown seq id " + std::to_string(seq_ids[i]));
+    }
+    chunkattn_status s = ensure_context(st);
+    if (s != CA_OK) return s;
+    if (!same) {
+      std::vector<int32_t> perm(n, -1);
+      for (int64_t i = 0; i < n; ++i) {
+        const int32_t r = ctx.row_of.at(seq_ids[i]);
+        if (perm[r] >= 0) return fail(CA_ESTATE, "duplicate seq id in attend");
+        perm[r] = (int32_t)i;
+      }
+      if (!host_only) {
+        s = upload(wsp + ws.attend_perm, perm.data(), n * 4, st);
+        if (s != CA_OK) return s;
+      }
+      attend_ids.assign(seq_ids, seq_ids + n);
+      attend_epoch = ctx.epoch;
+    }
+    return CA_OK;
+  }
+
+  AttnLaunch attn_launch(int32_t layer, const void* q, void* out) const {
+    AttnLaunch a{};
+    a.pool = pool;
+    a.layer = layer;
+    a.q = q;
+    a.out = out;
+    a.out_dtype = cfg.out_dtype;
+    a.pO = reinterpret_cast<float*>(wsp + ws.pO);
+    a.segO = reinterpret_cast<float*>(wsp + ws.segO);
+    a.counters = reinterpret_cast<uint32_t*>(wsp + ws.counters);
+    a.scale_log2 = scale() * 1.4426950408889634f;
+    a.cf_tensor_cores = tma_ok && !cf_simt;
+    a.sf_tensor_cores = !sf_simt;
+    a.cf_small = cf_small;
+    a.cf_umma = cf_umma;
+    a.trace = trace_kernel ? reinterpret_cast<uint64_t*>(wsp + ws.trace) : nullptr;
+    a.trace_cf = trace_kernel == 2;
+    a.sf_ctas_per_sm = sf_ctas_per_sm;
+    a.sf_prefetch = sf_prefetch | (diag_nocompute ? 256 : 0);
+    a.use_pdl = use_pdl && !kernel_events;
+    return a;
+  }
+
   chunkattn_status cuda_fail(cudaError_t e, const char* where) {
     failed = true;
     return fail(CA_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -241,8 +328,13 @@ struct chunkattn {
   chunkattn_status ensure_context(cudaStream_t st) {
     if (ctx.epoch == tree.epoch()) return CA_OK;
     sopt.cf_chunks_per_tile = cf_cpt_forced;
-    // fused kernel: tensor-core consumers in both phases (16-bit K/V, c % 16 == 0)
-    sopt.fused = fused_opt && !cf_simt && !sf_simt && cfg.dtype != CA_F32 && cfg.chunk_size % 16 == 0;
+    // fused kernel: the MMA seq-first kernel runs the chunk-first units (the
+    // SIMT consumers never do), so only shapes that kernel takes
+    sopt.fused = fused_opt && !cf_simt && sf_mma_tpw(cfg.dtype, cfg.chunk_size, !sf_simt) != 0;
+    // persistent grid: at most one wave (the cross-CTA merges spin on other
+    // CTAs' contributions, which must be resident)
+    sopt.sf_ctas = std::max<int64_t>(1, std::min<int64_t>(sf_ctas_req, resident_sf_ctas()));
+    sopt.dk = dk_opt && dk_supported(geom());
     Context nc;
     std::string err;
     if (!build_context(tree, sopt, &nc, &err)) return fail(CA_ENOMEM, err);
@@ -252,6 +344,7 @@ struct chunkattn {
       chunkattn_status s = upload(wsp + ws.tables, ctx.blob.data(), ctx.blob.size() * 4, st);
       if (s != CA_OK) return s;
       uploaded_epoch = ctx.epoch;
+      len_parity = 0;  // both length buffers now hold the host lengths
     }
     return CA_OK;
   }
@@ -261,7 +354,15 @@ struct chunkattn {
     const int32_t* base = reinterpret_cast<const int32_t*>(wsp + ws.tables);
     const BlobLayout& L = ctx.lay;
     t.row_caller = reinterpret_cast<const int32_t*>(wsp + ws.attend_perm);
-    t.seq_len = const_cast<int32_t*>(base + L.seq_len);
+    t.seq_len = const_cast<int32_t*>(base + (len_parity ? L.seq_len2 : L.seq_len));
+    t.dk_block = base + L.dk_block;
+    t.dk_cta = base + L.dk_cta;
+    t.dk_unit = base + L.dk_unit;
+    t.dk_cs = ctx.dk_cs;
+    t.dk_groups = ctx.dk_groups;
+    t.dk_max_rows = ctx.dk_max_rows;
+    t.dk_blocks = ctx.dk_blocks;
+    t.dk_hg = ctx.dk_hg;
     t.sf_first = base + L.sf_first;
     t.last_chunk = base + L.last_chunk;
     t.last_start = base + L.last_start;
@@ -361,8 +462,10 @@ chunkattn_status chunkattn_create(const chunkattn_config* cfg, const chunkattn_b
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device) == cudaSuccess && sms > 0)
       h->num_sms = sms;
     h->sopt.cf_target_ctas = h->num_sms;
-    h->sopt.sf_ctas = 2 * h->num_sms;
+    h->sf_ctas_req = 2 * h->num_sms;
     h->tma_ok = cf_mma_supported(h->pool);
+    if (dk_supported(h->pool))  // co-resident clusters of each size (the K5 cluster-size choice)
+      for (int k = 1; k <= kDkMaxCluster; ++k) h->sopt.dk_max_clusters[k] = dk_max_active_clusters(h->pool, cfg->out_dtype, k);
     const size_t pin_bytes = (size_t)4 * (std::max(h->ws.table_cap, h->ws.pf_cap) + 2 * cfg->max_batch + 64);
     for (int k = 0; k < 2; ++k) {
       cudaError_t e = cudaHostAlloc((void**)&h->pinned[k], pin_bytes, cudaHostAllocDefault);
@@ -561,51 +664,19 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   if (!h->host_only && n > 0 && (!q || !out)) return fail(CA_EINVAL, "null q/out");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (!h->host_only && h->set_device() != CA_OK) return CA_ECUDA;
-  const bool same = h->attend_epoch == h->tree.epoch() && (int64_t)h->attend_ids.size() == n &&
-                    (n == 0 || std::memcmp(h->attend_ids.data(), seq_ids, n * sizeof(int64_t)) == 0);
-  std::vector<int32_t> perm;
-  if (!same) {  // validate before touching any state
-    for (int64_t i = 0; i < n; ++i)
-      if (!h->tree.find(seq_ids[i])) return fail(CA_ENOSEQ, "unknown seq id " + std::to_string(seq_ids[i]));
-  }
-  chunkattn_status s = h->ensure_context(st);
+  chunkattn_status s = h->prepare_attend(n, seq_ids, st);
   if (s != CA_OK) return s;
-  if (!same) {
-    perm.assign(n, -1);
-    for (int64_t i = 0; i < n; ++i) {
-      const int32_t r = h->ctx.row_of.at(seq_ids[i]);
-      if (perm[r] >= 0) return fail(CA_ESTATE, "duplicate seq id in attend");
-      perm[r] = (int32_t)i;
-    }
-    if (!h->host_only) {
-      s = h->upload(h->wsp + h->ws.attend_perm, perm.data(), n * 4, st);
-      if (s != CA_OK) return s;
-    }
-    h->attend_ids.assign(seq_ids, seq_ids + n);
-    h->attend_epoch = h->ctx.epoch;
-  }
   if (h->host_only || n == 0) return CA_OK;
-  AttnLaunch a{};
-  a.pool = h->pool;
-  a.layer = layer;
-  a.q = q;
-  a.out = out;
-  a.out_dtype = h->cfg.out_dtype;
-  a.pO = reinterpret_cast<float*>(h->wsp + h->ws.pO);
-  a.segO = reinterpret_cast<float*>(h->wsp + h->ws.segO);
-  a.counters = reinterpret_cast<uint32_t*>(h->wsp + h->ws.counters);
-  a.scale_log2 = h->scale() * 1.4426950408889634f;
-  a.cf_tensor_cores = h->tma_ok && !h->cf_simt;
-  a.sf_tensor_cores = !h->sf_simt;
-  a.cf_small = h->cf_small;
-  a.cf_umma = h->cf_umma;
-  a.trace = h->trace_kernel ? reinterpret_cast<uint64_t*>(h->wsp + h->ws.trace) : nullptr;
-  a.trace_cf = h->trace_kernel == 2;
-  a.sf_ctas_per_sm = h->sf_ctas_per_sm;
-  a.sf_prefetch = h->sf_prefetch | (h->diag_nocompute ? 256 : 0);
-  a.use_pdl = h->use_pdl && !h->kernel_events;
+  const AttnLaunch a = h->attn_launch(layer, q, out);
   const DevTables t = h->dev_tables();
   cudaError_t e = cudaSuccess;
+  if (h->ctx.dk) {  // K5: one cluster launch (attend only: lengths from the current buffer)
+    const DkAppend ap{nullptr, nullptr, nullptr, 0};
+    e = h->timed_launch(chunkattn::K_SF, st, [&] { return launch_decode(a, t, ap, st); });
+    if (e != cudaSuccess) return h->cuda_fail(e, "decode");
+    ++h->n_launches;
+    return CA_OK;
+  }
   if (t.n_cf_tiles > 0 && !t.fused) {
     e = h->timed_launch(chunkattn::K_CF, st, [&] { return launch_chunk_first(a, t, st); });
     if (e != cudaSuccess) return h->cuda_fail(e, "chunk_first");
@@ -614,6 +685,59 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   e = h->timed_launch(chunkattn::K_SF, st, [&] { return launch_seq_first(a, t, st); });
   if (e != cudaSuccess) return h->cuda_fail(e, "seq_first");
   ++h->n_launches;
+  return CA_OK;
+  CA_GUARD_END
+}
+
+chunkattn_status chunkattn_append_attend(chunkattn_t h, int32_t layer, int64_t n, const int64_t* seq_ids,
+                                         const int32_t* tokens, const void* k, const void* v, const void* q,
+                                         void* out, void* stream) {
+  CA_GUARD_BEGIN
+  if (!h || n < 0 || (n > 0 && !seq_ids)) return fail(CA_EINVAL, "bad argument");
+  if (h->host_only) return fail(CA_EINVAL, "host-only handle");
+  if (h->failed) return fail(CA_ECUDA, "handle failed on an earlier CUDA error");
+  if (layer < 0 || layer >= h->cfg.num_layers) return fail(CA_EINVAL, "layer out of range");
+  if (n != h->tree.live_count())
+    return fail(CA_ESTATE, "append_attend needs all " + std::to_string(h->tree.live_count()) + " live sequences");
+  if (n == 0) return CA_OK;
+  if (!k || !v || !q || !out) return fail(CA_EINVAL, "null k/v/q/out");
+  if (layer == 0 && !tokens) return fail(CA_EINVAL, "null tokens");
+  const bool dk = h->dk_opt && dk_supported(h->geom());
+  if (!dk) {  // no K5 for this shape: the two-call path (one layer only)
+    if (h->cfg.num_layers != 1)
+      return fail(CA_EDTYPE, "append_attend with num_layers > 1 needs the cluster decode kernel (16-bit, d 64/128)");
+    chunkattn_status s = chunkattn_append_kv(h, n, seq_ids, tokens, k, v, stream);
+    if (s != CA_OK) return s;
+    return chunkattn_attend(h, layer, n, seq_ids, q, out, stream);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (h->set_device() != CA_OK) return CA_ECUDA;
+  if (layer == 0) {  // the tree grows once per step
+    for (int64_t i = 0; i < n; ++i) {
+      const Sequence* sq = h->tree.find(seq_ids[i]);
+      if (!sq) return fail(CA_ENOSEQ, "unknown seq id " + std::to_string(seq_ids[i]));
+      if (sq->len + 1 > h->cfg.max_seq_len) return fail(CA_EINVAL, "sequence would exceed max_seq_len");
+    }
+    h->scratch_ids.assign(seq_ids, seq_ids + n);
+    std::sort(h->scratch_ids.begin(), h->scratch_ids.end());
+    if (std::adjacent_find(h->scratch_ids.begin(), h->scratch_ids.end()) != h->scratch_ids.end())
+      return fail(CA_EINVAL, "duplicate seq id in append_attend");
+    const int64_t need = h->tree.append_needs(seq_ids, n);
+    if (need > h->tree.pool().available()) return fail(CA_ENOMEM, "chunk pool exhausted");
+    if (need > 0) h->tree.append_grow(seq_ids, n);  // structural: "chunk full" trigger
+  }
+  chunkattn_status s = h->prepare_attend(n, seq_ids, st);  // tables with pre-step lengths
+  if (s != CA_OK) return s;
+  const AttnLaunch a = h->attn_launch(layer, q, out);
+  const DevTables t = h->dev_tables();
+  const DkAppend ap{k, v, h->other_len(), layer == 0 ? 3 : 1};
+  cudaError_t e = h->timed_launch(chunkattn::K_SF, st, [&] { return launch_decode(a, t, ap, st); });
+  if (e != cudaSuccess) return h->cuda_fail(e, "decode");
+  ++h->n_launches;
+  if (layer == 0) {
+    h->len_parity ^= 1;  // the kernel wrote the advanced lengths to the other buffer
+    h->tree.append_tokens(seq_ids, tokens, n);
+  }
   return CA_OK;
   CA_GUARD_END
 }
@@ -640,10 +764,17 @@ chunkattn_status chunkattn_decode_step_host(chunkattn_t h, int32_t layer, int64_
   char* dev = static_cast<char*>(staging);
   cudaError_t e = cudaMemcpyAsync(dev, in_host, in_bytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return h->cuda_fail(e, "decode_step_host H2D");
-  chunkattn_status s = chunkattn_append_kv(h, n, seq_ids, tokens, dev + q_bytes, dev + q_bytes + kv_bytes, stream);
-  if (s != CA_OK) return s;
-  s = chunkattn_attend(h, layer, n, seq_ids, dev, dev + out_off, stream);
-  if (s != CA_OK) return s;
+  chunkattn_status s;
+  if (h->cfg.num_layers == 1 && h->dk_opt && dk_supported(h->geom())) {  // one launch: append + attend
+    s = chunkattn_append_attend(h, layer, n, seq_ids, tokens, dev + q_bytes, dev + q_bytes + kv_bytes, dev,
+                                dev + out_off, stream);
+    if (s != CA_OK) return s;
+  } else {
+    s = chunkattn_append_kv(h, n, seq_ids, tokens, dev + q_bytes, dev + q_bytes + kv_bytes, stream);
+    if (s != CA_OK) return s;
+    s = chunkattn_attend(h, layer, n, seq_ids, dev, dev + out_off, stream);
+    if (s != CA_OK) return s;
+  }
   e = cudaMemcpyAsync(out_host, dev + out_off, out_bytes, cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return h->cuda_fail(e, "decode_step_host D2H");
   return CA_OK;
@@ -700,6 +831,19 @@ chunkattn_status chunkattn_counters(chunkattn_t h, int64_t out[6]) {
   return CA_OK;
 }
 
+chunkattn_status chunkattn_schedule_info(chunkattn_t h, int64_t out[8]) {
+  if (!h || !out) return fail(CA_EINVAL, "bad argument");
+  out[0] = h->ctx.dk ? 1 : 0;
+  out[1] = h->ctx.dk_cs;
+  out[2] = h->ctx.dk_groups;
+  out[3] = h->ctx.dk_blocks;
+  out[4] = h->ctx.dk_units;
+  out[5] = h->ctx.dk_hg;
+  out[6] = h->ctx.fused ? 1 : 0;
+  out[7] = h->ctx.n_sf_ctas;
+  return CA_OK;
+}
+
 chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t value) {
   if (!h || !key) return fail(CA_EINVAL, "bad argument");
   const std::string k(key);
@@ -707,12 +851,13 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->cf_cpt_forced = value < 0 ? 0 : value;
   } else if (k == "cf_target_ctas") {
     h->sopt.cf_target_ctas = value < 1 ? 1 : value;
-  } else if (k == "sf_ctas") {
-    h->sopt.sf_ctas = value < 1 ? 1 : std::min<int64_t>(value, kMaxSfCtas);
+  } else if (k == "sf_ctas") {  // clamped to one resident wave at the next build
+    h->sf_ctas_req = value < 1 ? 1 : std::min<int64_t>(value, kMaxSfCtas);
   } else if (k == "cf_simt") {
     h->cf_simt = value != 0;
   } else if (k == "sf_simt") {
     h->sf_simt = value != 0;
+    h->resident_cache = -1;
   } else if (k == "fused") {
     h->fused_opt = value != 0;
   } else if (k == "cf_unit_cost") {
@@ -725,6 +870,20 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->sopt.sf_unit_fixed = value < 0 ? 0.0 : std::min<int64_t>(value, 10) / 10.0;  // tenths
   } else if (k == "sf_item_cost") {
     h->sopt.sf_item_cost = value < 0 ? 0.0 : (double)value / 10.0;  // tenths of a unit
+  } else if (k == "dk") {
+    h->dk_opt = value != 0;
+  } else if (k == "dk_cs") {
+    h->sopt.dk_cs_forced = (int32_t)std::max<int64_t>(0, std::min<int64_t>(value, kDkMaxCluster));
+  } else if (k == "dk_max_rows") {
+    h->sopt.dk_max_rows = (int32_t)std::max<int64_t>(16, std::min<int64_t>(value, kDkMaxRows));
+  } else if (k == "dk_shared_fixed") {  // hundredths
+    h->sopt.dk_shared_fixed = std::max<int64_t>(0, value) / 100.0;
+  } else if (k == "dk_shared_row") {  // thousandths
+    h->sopt.dk_shared_row = std::max<int64_t>(0, value) / 1000.0;
+  } else if (k == "dk_hg") {
+    h->sopt.dk_hg_forced = (int32_t)std::max<int64_t>(0, value);
+  } else if (k == "dk_pack_fixed") {  // hundredths
+    h->sopt.dk_pack_fixed = std::min<int64_t>(100, std::max<int64_t>(0, value)) / 100.0;
   } else if (k == "cf_umma") {
     h->cf_umma = value != 0;
   } else if (k == "cf_small") {
@@ -739,7 +898,8 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     return CA_OK;
   } else if (k == "sf_ctas_per_sm") {
     h->sf_ctas_per_sm = value <= 1 ? 1 : 2;
-    h->sopt.sf_ctas = (int64_t)h->sf_ctas_per_sm * h->num_sms;
+    h->sf_ctas_req = (int64_t)h->sf_ctas_per_sm * h->num_sms;
+    h->resident_cache = -1;
   } else if (k == "pdl") {
     h->use_pdl = value != 0;
   } else if (k == "kernel_events") {

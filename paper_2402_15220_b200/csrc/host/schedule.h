@@ -49,6 +49,19 @@ constexpr int kSfUnitInts = 8;
 // bit of the {nsegs} word: this CTA's segment is the item's last -- its merger
 constexpr int kSfMerger = 1 << 30;
 
+// K5 cluster decode tables (decode.cu).  Unit record (kDkUnitInts int32):
+// {chunk id, first row, rows, DK_* flags}; CTA record (kDkCtaInts): {u0, u1}
+// = units of CTA rank r of the block's clusters; block record: {row0, rows}.
+// DK_PACK: a row's last chunk packed with other rows' into one stage (one
+// row per consumer warp); DK_END: the producer's end marker (device only).
+enum DkFlags : int32_t { DK_FIRST = 1, DK_LAST = 2, DK_TAIL = 4, DK_PRIV = 8, DK_PACK = 16, DK_END = 32 };
+constexpr int kDkUnitInts = 4;
+constexpr int kDkCtaInts = 4;
+constexpr int kDkBlockInts = 4;
+constexpr int kDkMaxRows = 64;     // (head, row) states of one CTA: head-set size x block rows
+constexpr int kDkPack = 4;         // rows' last chunks dealt per pack (16-token slots of a c = 64 stage)
+constexpr int kDkMaxCluster = 16;  // cluster sizes considered (> 8: non-portable)
+
 struct ScheduleOptions {
   int32_t share_threshold = 2;
   int32_t num_heads = 1;
@@ -66,10 +79,20 @@ struct ScheduleOptions {
   int64_t slot_capacity = 0;       // partial slots available in the workspace
   int64_t table_capacity = 0;      // int32 entries available for the blob
   int64_t seg_capacity = 0;        // seq-first segment partial rows available
+  // K5 cluster decode
+  bool dk = false;
+  int32_t dk_max_rows = kDkMaxRows;
+  int32_t dk_cs_forced = 0;                        // > 0: cluster size to use
+  int32_t dk_max_clusters[kDkMaxCluster + 1] = {};  // co-resident clusters of each size (0: unsupported)
+  double dk_shared_fixed = 1.0;  // unit costs for the per-cluster split: chunk-first unit = fixed + per_row * rows
+  double dk_shared_row = 0.01;
+  double dk_pack_fixed = 1.3;    // a pack of last chunks = fixed + sum of valid / c / 2
+  int32_t dk_hg_forced = 0;      // > 0: heads per cluster group (divides num_heads)
 };
 
 // Offsets (int32 units) of the arrays inside the blob.
 struct BlobLayout {
+  int64_t seq_len2 = 0, dk_block = 0, dk_cta = 0, dk_unit = 0;
   int64_t seq_len = 0, sf_first = 0, last_chunk = 0, last_start = 0, sf_ptr = 0, mg_ptr = 0,
           sf_chunk = 0, mg_slot = 0, cf_chunk = 0, cf_tile = 0, sf_cta = 0, sf_item = 0, sf_unit = 0, mg_tile = 0,
           cf_unit = 0, total = 0;
@@ -92,6 +115,10 @@ struct Context {
   int32_t n_seg_slots = 0;  // segment partials of items split across CTAs
   int32_t n_cf_units = 0;   // fused: chunk-first units (all CTAs)
   bool fused = false;
+  // K5 cluster decode
+  bool dk = false;
+  int32_t dk_cs = 0, dk_blocks = 0, dk_groups = 0, dk_max_rows = 0, dk_hg = 1;
+  int64_t dk_units = 0;
 };
 
 // Build the context of the current tree.  Returns false (and sets *err) when

@@ -1,0 +1,807 @@
+// K5 cluster decode: one launch per decode step = K1 append (the step's new
+// K/V row) + K3 chunk-first (Alg 1, Eqn 1
+// :95-108) + K4 seq-first (Alg 2) + the Eqn 2 merge
+// + O / n.
+//
+// Work decomposition (host: schedule.cpp, "dk" tables).  The DFS rows are cut
+// into blocks of <= kDkMaxRows rows.  A GROUP = (row block, set of hg heads)
+// is computed by one thread-block CLUSTER of cs CTAs, one CTA per SM (the
+// host picks hg and cs so that all groups run in one wave and fill the SMs).
+// The group's work list -- per head of the set: every shared run clipped to
+// the block (chunk-first units: one (chunk, head) K/V tile x all the run's
+// rows of the block), then every row's full private chunks (cooperative
+// seq-first units) -- is cut into cs contiguous pieces of equal estimated
+// cost; every row's last chunk (short in decode) is dealt to the least-loaded
+// ranks in packs of up to one row per consumer warp.  Each CTA folds every job
+// it runs (a maximal stretch of one run / one row inside its piece) into a
+// per-(head, row) online-softmax state (o, m, n) in shared memory, in job
+// order (Eqn 2).  At the end the CTAs of the cluster merge the cs states of
+// every (head, row) over distributed shared memory in rank order (Eqn 2,
+// n-ary form) and write O / n.  No partials in global memory, no counters, no
+// cross-CTA waiting outside the cluster barrier: deterministic, any grid is
+// safe.
+//
+// CTA (one per SM, 12 warps) = 1 producer warp (unit descriptors -> 1-D bulk
+// copies of the valid tokens of each (chunk, head) K and V tile into an
+// NST-deep ring) + 3 idle warps + NC = 8 mma.sync consumer warps
+// (mma_attn.cuh WarpAttn):
+//   chunk-first job (rows [r0, r0 + nr) <= 64): warp (g, l) = 16 query rows x
+//     token slice of every (alt)-th chunk, so consecutive chunks are computed
+//     by different warps at once; Q fragments straight from global;
+//   cooperative seq-first job (one row, full chunks): warp w = token slice w;
+//   PACK (rows' last chunks, 16-token slots): warp w = all of row w's chunk.
+// K1 folded in: a row's last chunk reaches the stage as its old tokens (pool)
+// plus the new K/V rows copied from the caller's k / v into staging rows of
+// the stage (the MMA reads that token's ldmatrix rows from there); the
+// consumer warp that attends it writes those rows into the pool slot.
+// m is kept in log2 units (scale * log2 e folded into the logits).
+#include <algorithm>
+#include <map>
+#include <mutex>
+
+#include "../host/schedule.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "mma_attn.cuh"
+
+namespace pakv {
+
+using namespace dev;
+
+namespace {
+
+// 12 warps: warpgroup 0 = the producer warp + 3 idle warps, warpgroups 1-2 =
+// NC = 8 consumer warps.  Registers are
+// re-balanced per warpgroup with setmaxnreg (72 for warpgroup 0, 216 for the
+// consumers: 128 x 72 + 256 x 216 <= 64 K).
+constexpr int kNC = 8;                           // consumer warps
+constexpr int kConsumer0 = 4;                    // first consumer warp
+constexpr int kDkThreads = 12 * 32;
+constexpr int kRegsLow = 72, kRegsHigh = 216;
+constexpr int kDkMaxStages = 8;
+constexpr int kDkSlice = 32;                     // chunk-first token slice per warp and call (>= 32: latency)
+constexpr size_t kDkSmemBudget = 232448 - 2048;  // 227 KB opt-in, minus static shared memory
+constexpr int kStateRows = kDkMaxRows;           // (head, row) states per CTA: hg * block rows <= 64
+
+// Stage metadata: a unit (flags, valid tokens, rows, head of the set) or a
+// PACK of n rows' last chunks (row, valid tokens, first slot row, head), or END.
+struct DkMeta {
+  int flags, n, nt, row0, nrows, hh;
+  int prow[kNC], pnt[kNC], poff[kNC], phh[kNC], pchunk[kNC];
+};
+
+CA_DEV void dk_sync_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(kNC * 32) : "memory"); }
+template <int N>
+CA_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+template <int N>
+CA_DEV void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+CA_DEV void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+CA_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+CA_DEV void bulk_s2g(void* dst, const void* src, uint32_t bytes) {  // shared -> global, bulk group
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+CA_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+CA_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+CA_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+CA_DEV void cluster_sync() {
+  asm volatile(
+      "barrier.cluster.arrive.release.aligned;\n"
+      "barrier.cluster.wait.acquire.aligned;\n" ::
+          : "memory");
+}
+CA_DEV uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+CA_DEV float4 ld_cluster_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+CA_DEV float2 ld_cluster_f2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+
+// (head, row) state layout in shared memory: [hg][rows][D + 4] fp32 =
+// o[0..D), m (log2 units) at D, n at D + 1.
+template <int D>
+struct RowState {
+  static constexpr int kStride = D + 4;
+};
+
+// Eqn 2 weights of a state (ms) and a partial (mj) rebased to their common
+// max (either may be -inf: an empty side contributes nothing).
+CA_DEV void fold_weights(float ms, float mj, float& M, float& ws, float& wj) {
+  M = fmaxf(ms, mj);
+  ws = ms == -INFINITY ? 0.f : fast_exp2(ms - M);
+  wj = mj == -INFINITY ? 0.f : fast_exp2(mj - M);
+}
+
+template <typename T, typename TO, int D, int TPW>
+__global__ void __launch_bounds__(kDkThreads, 1)
+    dk_kernel(T* kpool, T* vpool, const T* __restrict__ q, TO* __restrict__ out, const T* __restrict__ knew,
+              const T* __restrict__ vnew, int32_t* __restrict__ len_out, int32_t mode, DevTables t, int32_t h,
+              int32_t c, float scale_log2, int32_t nst, uint32_t stage_bytes, int32_t cs, int32_t hg,
+              uint64_t* __restrict__ trace) {
+  using WA = WarpAttn<T, D, TPW>;
+  constexpr int SR = RowState<D>::kStride;
+  constexpr uint32_t kRowBytes = D * sizeof(T);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t full_bar[kDkMaxStages], empty_bar[kDkMaxStages];
+  __shared__ DkMeta meta[kDkMaxStages];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)(blockIdx.x % (unsigned)cs), grp = (int)(blockIdx.x / (unsigned)cs);
+  const int hsets = h / hg;
+  const int head0 = (grp % hsets) * hg, blk = grp / hsets;
+  const int4 brec = *reinterpret_cast<const int4*>(t.dk_block + 4 * blk);  // {row0, rows}
+  const int brow0 = brec.x, brows = brec.y;
+  const int2 crec = *reinterpret_cast<const int2*>(t.dk_cta + 4 * (blk * cs + rank));  // units [u0, u1)
+  const int u0 = crec.x, u1 = crec.y;
+  const uint32_t tile_bytes = (uint32_t)c * kRowBytes;
+  float* st = reinterpret_cast<float*>(smem_raw + (size_t)nst * stage_bytes);  // (head, row) states
+  auto state_row = [&](int hh, int row) { return st + (size_t)(hh * brows + row - brow0) * SR; };
+  // mode bit 0: scatter the step's new K/V row into each row's last chunk
+  // (K1 folded in); bit 1: the lengths advance by one in this launch (the
+  // step's first layer) and the new lengths go to len_out
+  const bool append = (mode & 1) != 0, bump = (mode & 2) != 0;
+  // debug timeline (option "trace"): kernel_timeline.py layout (kernels.h)
+  uint64_t* tr = trace && blockIdx.x < kTraceCtas ? trace + (size_t)blockIdx.x * kTraceStride : nullptr;
+  if (tr && tid == 0) tr[0] = globaltimer_ns();
+
+  if (tid == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full_bar[s], 1);  // producer: expected bytes per copy, then one arrive with the metadata
+      mbar_init(&empty_bar[s], kNC);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp < kConsumer0) {
+   regs_dec<kRegsLow>();
+   if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    // Stages: a chunk-first unit, a cooperative seq-first unit, or a PACK of
+    // up to NC rows' last chunks (16-token slots, one row per consumer warp),
+    // packed greedily in unit order; then an END stage.
+    int jj = 0, rs = 0;  // stages published; ring slot / phase of the next one
+    uint32_t rph = 0;
+    int pk_n = 0, pk_q = 0, pk_s = 0;  // open pack: rows, 16-token slots used, its stage
+    uint32_t pk_bytes = 0;
+    const int pk_cap = c / 16;
+    auto acquire = [&]() {
+      if (jj >= nst) mbar_wait(&empty_bar[rs], rph ^ 1u);
+      return rs;
+    };
+    auto publish = [&](int s, uint32_t bytes) {  // metadata written: complete the stage (lane 0)
+      if (lane == 0) {
+        mbar_arrive1(&full_bar[s]);
+        if (tr && jj < kTraceUnits) {
+          tr[3 + 4 * jj] = globaltimer_ns();
+          tr[6 + 4 * jj] = bytes;
+        }
+      }
+      __syncwarp();
+      ++jj;
+      if (++rs == nst) {
+        rs = 0;
+        rph ^= 1u;
+      }
+    };
+    // A pack's items are assigned in order (stage, 16-token slot, index) and
+    // their copies issued by the lanes holding their descriptors, all at once
+    // when the pack closes (packs close at the end of a 32-unit batch).
+    int my_pack = -1, my_off = 0, my_idx = 0, pk_id = 0;
+    auto close_pack = [&](const int4& d, int caller, int nt) {
+      if (pk_n == 0) return;
+      if (my_pack == pk_id) {
+        const int hh = d.w >> 8, head = head0 + hh;
+        const size_t toff = ((size_t)d.x * h + head) * c * D;
+        const uint32_t kv_bytes = (uint32_t)nt * kRowBytes;
+        const bool fresh = append && (d.w & DK_TAIL);  // its last token is this step's
+        const uint32_t old = fresh ? kv_bytes - kRowBytes : kv_bytes;
+        unsigned char* stg = smem_raw + (size_t)pk_s * stage_bytes;
+        const uint32_t off = (uint32_t)my_off * kRowBytes;  // 16-token aligned: the tile swizzle holds
+        const size_t src = ((size_t)caller * h + head) * D;
+        mbar_expect_tx(&full_bar[pk_s], 2 * kv_bytes + kRowBytes);
+        if (old) {
+          bulk_g2s(stg + off, kpool + toff, old, &full_bar[pk_s]);
+          bulk_g2s(stg + tile_bytes + off, vpool + toff, old, &full_bar[pk_s]);
+        }
+        bulk_g2s(stg + 2 * tile_bytes + my_idx * kRowBytes, q + src, kRowBytes, &full_bar[pk_s]);
+        if (fresh) {  // the new K / V rows, row-major, into the pack's staging rows
+          unsigned char* nrow = stg + 2 * tile_bytes + (kNC + 2 * my_idx) * kRowBytes;
+          bulk_g2s(nrow, knew + src, kRowBytes, &full_bar[pk_s]);
+          bulk_g2s(nrow + kRowBytes, vnew + src, kRowBytes, &full_bar[pk_s]);
+        }
+        meta[pk_s].prow[my_idx] = d.y;
+        meta[pk_s].pnt[my_idx] = nt;
+        meta[pk_s].poff[my_idx] = my_off;
+        meta[pk_s].phh[my_idx] = hh;
+        meta[pk_s].pchunk[my_idx] = d.x;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        meta[pk_s].flags = DK_PACK;
+        meta[pk_s].n = pk_n;
+      }
+      publish(pk_s, pk_bytes);
+      pk_n = pk_q = 0;
+      pk_bytes = 0;
+      ++pk_id;
+    };
+    for (int base = u0; base < u1; base += 32) {
+      const int u = base + lane;
+      int4 d = make_int4(-1, 0, 0, 0);  // {chunk, row0, rows, flags | hh << 8}
+      int caller = 0, nt = c;
+      if (u < u1) d = *reinterpret_cast<const int4*>(t.dk_unit + 4 * (size_t)u);
+      if (base == u0) pdl_wait();  // the pool, q and the lengths may come from the previous kernel (PDL)
+      if (u < u1) {
+        if (d.w & DK_PRIV) caller = t.row_caller[d.y];
+        if (d.w & DK_TAIL) {  // the row's last chunk: valid tokens from its length
+          const int len = t.seq_len[d.y] + (bump ? 1 : 0);
+          nt = len - t.last_start[d.y];
+          if (bump && head0 + (d.w >> 8) == 0) len_out[d.y] = len;  // the lengths of the next launch
+        }
+      }
+      const int cnt = min(32, u1 - base);
+      for (int i = 0; i < cnt; ++i) {
+        const int i_chunk = __shfl_sync(0xffffffffu, d.x, i);
+        const int i_row0 = __shfl_sync(0xffffffffu, d.y, i);
+        const int i_nrows = __shfl_sync(0xffffffffu, d.z, i);
+        const int i_word = __shfl_sync(0xffffffffu, d.w, i);
+        const int i_caller = __shfl_sync(0xffffffffu, caller, i);
+        const int i_nt = __shfl_sync(0xffffffffu, nt, i);
+        const int i_flags = i_word & 0xff, i_hh = i_word >> 8, head = head0 + i_hh;
+        const size_t toff = ((size_t)i_chunk * h + head) * c * D;
+        const uint32_t kv_bytes = (uint32_t)i_nt * kRowBytes;
+        const T* qrow = q + ((size_t)i_caller * h + head) * D;
+        if (i_flags & DK_PACK) {
+          const int slots = (i_nt + 15) >> 4;
+          if (pk_n > 0 && (pk_q + slots > pk_cap || pk_n == kNC)) close_pack(d, caller, nt);
+          if (pk_n == 0) pk_s = acquire();
+          if (lane == i) {
+            my_pack = pk_id;
+            my_off = pk_q * 16;
+            my_idx = pk_n;
+          }
+          ++pk_n;
+          pk_q += slots;
+          pk_bytes += 2 * kv_bytes + kRowBytes;
+          continue;
+        }
+        close_pack(d, caller, nt);
+        const int s = acquire();
+        const bool want_q = (i_flags & DK_PRIV) && (i_flags & DK_FIRST);
+        if (lane == 0) {
+          unsigned char* stg = smem_raw + (size_t)s * stage_bytes;
+          mbar_expect_tx(&full_bar[s], 2 * kv_bytes + (want_q ? kRowBytes : 0u));
+          bulk_g2s(stg, kpool + toff, kv_bytes, &full_bar[s]);
+          bulk_g2s(stg + tile_bytes, vpool + toff, kv_bytes, &full_bar[s]);
+          if (want_q) bulk_g2s(stg + 2 * tile_bytes, qrow, kRowBytes, &full_bar[s]);
+          meta[s].flags = i_flags;
+          meta[s].nt = i_nt;
+          meta[s].row0 = i_row0;
+          meta[s].nrows = i_nrows;
+          meta[s].hh = i_hh;
+        }
+        publish(s, 2 * kv_bytes);
+      }
+      close_pack(d, caller, nt);  // packs do not straddle batches (descriptors live in lanes)
+    }
+    if (u0 >= u1) pdl_wait();
+    const int s = acquire();
+    if (lane == 0) meta[s].flags = DK_END;
+    publish(s, 0);
+   }
+   cluster_sync();  // the consumers' states are final (the merge reads them)
+   cluster_sync();  // the merge is done
+  } else {
+    // ----------------------------------------------------------- consumers
+    regs_inc<kRegsHigh>();
+    const int ct = tid - kConsumer0 * 32, cw = warp - kConsumer0;
+    for (int i = ct; i < hg * brows * SR; i += kNC * 32) st[i] = (i % SR) == D ? -INFINITY : 0.f;
+    pdl_wait();  // q comes from the previous kernel
+    dk_sync_consumers();  // states initialised
+    WA wa;
+    uint32_t qa[WA::KS][4];
+    auto q_row0 = [&](const unsigned char* qrow) {  // the query in row 0 of the MMA tile (lanes 0..3)
+      const uint32_t* q32 = reinterpret_cast<const uint32_t*>(qrow);
+#pragma unroll
+      for (int ks = 0; ks < WA::KS; ++ks) {
+        qa[ks][0] = lane < 4 ? q32[ks * 8 + lane] : 0u;
+        qa[ks][2] = lane < 4 ? q32[ks * 8 + 4 + lane] : 0u;
+        qa[ks][1] = qa[ks][3] = 0u;
+      }
+    };
+    // chunk-first job geometry (begin_cf): warp (g, l), G row groups x L lanes
+    int cfL = 1, cfg = 0, cfl = 0, crow0 = 0, crows = 0, chh = 0, c_altm = 0, c_sel = 0, c_span = c, c_tb = 0;
+    bool cact = false;
+    auto begin_cf = [&](int row0, int nrows, int hh) {
+      crow0 = row0;
+      crows = nrows;
+      chh = hh;
+      int g = 1;
+      while (g * 16 < nrows) g *= 2;
+      cfL = kNC / g;
+      cfg = cw / cfL;
+      cfl = cw % cfL;
+      cact = cfg * 16 < crows;
+      int nsl = cfL;  // token slices per chunk: divides cfL and c / 16, >= kDkSlice tokens each
+      while (nsl > 1 && (nsl * kDkSlice > c || (c / 16) % nsl != 0)) nsl >>= 1;
+      c_altm = cfL / nsl - 1;  // lane l takes slice l % nsl of every alt-th chunk (k % alt == l / nsl)
+      c_sel = cfl / nsl;
+      c_span = c / nsl;
+      c_tb = (cfl % nsl) * c_span;
+      wa.reset();
+      const int head = head0 + hh;
+      const int rlo = crow0 + cfg * 16 + (lane >> 2), rhi = rlo + 8;
+      const T* qlo = (cact && rlo < crow0 + crows) ? q + ((size_t)t.row_caller[rlo] * h + head) * D : nullptr;
+      const T* qhi = (cact && rhi < crow0 + crows) ? q + ((size_t)t.row_caller[rhi] * h + head) * D : nullptr;
+      const int cq = (lane & 3) * 2;
+#pragma unroll
+      for (int ks = 0; ks < WA::KS; ++ks) {
+        qa[ks][0] = qlo ? *reinterpret_cast<const uint32_t*>(qlo + ks * 16 + cq) : 0u;
+        qa[ks][1] = qhi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16 + cq) : 0u;
+        qa[ks][2] = qlo ? *reinterpret_cast<const uint32_t*>(qlo + ks * 16 + 8 + cq) : 0u;
+        qa[ks][3] = qhi ? *reinterpret_cast<const uint32_t*>(qhi + ks * 16 + 8 + cq) : 0u;
+      }
+    };
+    // row-0 state (lanes 0..3) of this warp folded into (hh, row)'s state (Eqn 2)
+    auto fold_row0 = [&](int hh, int row) {
+      if (lane < 4) {
+        float* srow = state_row(hh, row);
+        const float ms = srow[D], ns = srow[D + 1];
+        float M, ws, wj;
+        fold_weights(ms, wa.m_lo, M, ws, wj);
+#pragma unroll
+        for (int i = 0; i < WA::DT; ++i) {
+          float2* p = reinterpret_cast<float2*>(srow + i * 8 + lane * 2);
+          const float2 o = *p;
+          *p = make_float2(fmaf(wj, wa.o[i][0], o.x * ws), fmaf(wj, wa.o[i][1], o.y * ws));
+        }
+        __syncwarp(0xfu);  // the quad read ms before lane 0 rewrites it
+        if (lane == 0) {
+          srow[D] = M;
+          srow[D + 1] = fmaf(wj, wa.n_lo, ns * ws);
+        }
+      }
+      __syncwarp();
+    };
+    int kk = 0;  // chunk index inside the current chunk-first job (lane selection)
+    int kp = 0;  // chunk index inside the current cooperative seq-first job (team selection)
+    // the CTA's first job, if chunk-first: its Q fragments (global loads)
+    // overlap the first K/V copies
+    bool pre = false;
+    if (u0 < u1) {
+      const int4 d0 = *reinterpret_cast<const int4*>(t.dk_unit + 4 * (size_t)u0);
+      if (!(d0.w & DK_PRIV)) {
+        begin_cf(d0.y, d0.z, d0.w >> 8);
+        pre = true;
+      }
+    }
+    int jj = 0, rs = 0;
+    uint32_t rph = 0;
+    for (;; ++jj) {
+      const int s = rs;
+      mbar_wait(&full_bar[s], rph);
+      if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 4 * jj] = globaltimer_ns();
+      const int flags = meta[s].flags;
+      if (flags & DK_END) break;
+      const unsigned char* stg = smem_raw + (size_t)s * stage_bytes;
+      const uint32_t k_u32 = smem_u32(stg), v_u32 = k_u32 + tile_bytes;
+      if (flags & DK_PACK) {
+        // ---- seq-first PACK (Alg 2): warp w = the whole last chunk of row w
+        if (cw < meta[s].n) {
+          const int row = meta[s].prow[cw], ntw = meta[s].pnt[cw], hh = meta[s].phh[cw];
+          const uint32_t off = (uint32_t)meta[s].poff[cw] * kRowBytes;
+          q_row0(stg + 2 * tile_bytes + cw * kRowBytes);
+          // the step's new token (append): its K / V rows are read from the
+          // pack's staging rows, not the tile
+          const unsigned char* nrow = stg + 2 * tile_bytes + (kNC + 2 * cw) * kRowBytes;
+          const int sp = append ? ntw - 1 : -1;
+          const uint32_t sp_k = smem_u32(nrow), sp_v = sp_k + kRowBytes;
+          wa.reset();
+          for (int t0 = 0; t0 < ntw; t0 += 16)
+            wa.template chunk<true, 16>(qa, k_u32 + off, v_u32 + off, t0, ntw, scale_log2, lane, 0, 0, sp, sp_k, sp_v);
+          wa.finish();
+          fold_row0(hh, row);
+          if (append) {
+            // K1: the new K / V row into its pool slot for the next steps
+            // (16-byte groups XOR-swizzled by slot % 8; lanes 0-15 K, 16-31 V)
+            constexpr int V16 = kRowBytes / 16, E16 = 16 / sizeof(T);
+            const int x = lane & 15, slot = ntw - 1;
+            if (x < V16) {
+              const size_t pofs = ((size_t)meta[s].pchunk[cw] * h + head0 + hh) * c * D + (size_t)slot * D;
+              T* to = (lane < 16 ? kpool : vpool) + pofs + (size_t)swz_chunk(slot, x) * E16;
+              *reinterpret_cast<uint4*>(to) = *reinterpret_cast<const uint4*>(nrow + (lane < 16 ? 0u : kRowBytes) + x * 16);
+            }
+          }
+        }
+      } else if (flags & DK_PRIV) {
+        // ---- cooperative seq-first unit (Alg 2): one row; two teams of four
+        // warps take alternate chunks of the job, warp (team, w) = token slice w
+        const int nt = meta[s].nt;
+        if (flags & DK_FIRST) {
+          wa.reset();
+          q_row0(stg + 2 * tile_bytes);
+          kp = 0;
+        }
+        const int team = cw >> 2, tw = cw & 3;
+        if ((kp & 1) == team && tw * TPW < nt) wa.template chunk<true>(qa, k_u32, v_u32, tw * TPW, nt, scale_log2, lane);
+        ++kp;
+        if (flags & DK_LAST) {
+          // fold the warps' row-0 states into the row's state, warp order
+          // (scratch: this stage's K tile -- every warp is done reading it)
+          wa.finish();
+          float* pw = reinterpret_cast<float*>(const_cast<unsigned char*>(stg));
+          dk_sync_consumers();
+          if (lane < 4) {
+            if (lane == 0) {
+              pw[cw * SR + D] = wa.m_lo;
+              pw[cw * SR + D + 1] = wa.n_lo;
+            }
+#pragma unroll
+            for (int i = 0; i < WA::DT; ++i)
+              *reinterpret_cast<float2*>(&pw[cw * SR + i * 8 + lane * 2]) = make_float2(wa.o[i][0], wa.o[i][1]);
+          }
+          dk_sync_consumers();
+          float* srow = state_row(meta[s].hh, meta[s].row0);
+          const float ms = srow[D], ns = srow[D + 1];
+          float M = ms;
+#pragma unroll
+          for (int w = 0; w < kNC; ++w) M = fmaxf(M, pw[w * SR + D]);
+          if (M != -INFINITY) {
+            float wgt[kNC];
+            const float wsf = ms == -INFINITY ? 0.f : fast_exp2(ms - M);
+#pragma unroll
+            for (int w = 0; w < kNC; ++w) {
+              const float mw = pw[w * SR + D];
+              wgt[w] = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
+            }
+            for (int x = ct; x < D; x += kNC * 32) {
+              float a = srow[x] * wsf;
+#pragma unroll
+              for (int w = 0; w < kNC; ++w) a = fmaf(wgt[w], pw[w * SR + x], a);
+              srow[x] = a;
+            }
+            dk_sync_consumers();  // every thread read ms before it changes
+            if (ct == 0) {
+              float nn = ns * wsf;
+#pragma unroll
+              for (int w = 0; w < kNC; ++w) nn = fmaf(wgt[w], pw[w * SR + D + 1], nn);
+              srow[D] = M;
+              srow[D + 1] = nn;
+            }
+          }
+          fence_proxy_async();  // generic writes to the stage before its next bulk copy
+          dk_sync_consumers();  // scratch / row state reuse
+        }
+      } else {
+        // ---- chunk-first unit (Alg 1): rows [row0, row0 + nrows) of a shared run
+        if (flags & DK_FIRST) {
+          if (!pre) begin_cf(meta[s].row0, meta[s].nrows, meta[s].hh);
+          pre = false;
+          kk = 0;
+        }
+        if (cact && (kk & c_altm) == c_sel) {
+          int t0 = c_tb;
+          for (; t0 + 32 <= c_tb + c_span; t0 += 32) wa.template chunk<false, 32>(qa, k_u32, v_u32, t0, c, scale_log2, lane);
+          for (; t0 < c_tb + c_span; t0 += 16) wa.template chunk<false, 16>(qa, k_u32, v_u32, t0, c, scale_log2, lane);
+        }
+        ++kk;
+        if (flags & DK_LAST) {
+          // fold lane l's 16-row partial into the rows' states, lanes in order
+          wa.finish();
+          for (int l = 0; l < cfL; ++l) {
+            dk_sync_consumers();
+            if (cfl == l && cact) {
+              const int rl = lane >> 2, cq = (lane & 3) * 2;
+#pragma unroll
+              for (int hf = 0; hf < 2; ++hf) {
+                const int rloc = cfg * 16 + rl + 8 * hf;
+                const bool ok = rloc < crows;
+                float* srow = state_row(chh, crow0 + (ok ? rloc : 0));
+                const float mj = hf ? wa.m_hi : wa.m_lo, nj = hf ? wa.n_hi : wa.n_lo;
+                const float ms = ok ? srow[D] : -INFINITY;
+                float M, ws, wj;
+                fold_weights(ms, mj, M, ws, wj);
+                if (ok) {
+#pragma unroll
+                  for (int i = 0; i < WA::DT; ++i) {
+                    float2* p = reinterpret_cast<float2*>(srow + i * 8 + cq);
+                    const float2 o = *p;
+                    *p = make_float2(fmaf(wj, wa.o[i][2 * hf], o.x * ws), fmaf(wj, wa.o[i][2 * hf + 1], o.y * ws));
+                  }
+                }
+                __syncwarp();  // the quad read ms before lane cq == 0 rewrites it
+                if (ok && (lane & 3) == 0) {
+                  const float ns = srow[D + 1];
+                  srow[D] = M;
+                  srow[D + 1] = fmaf(wj, nj, ns * ws);
+                }
+              }
+            }
+          }
+          dk_sync_consumers();
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&empty_bar[s]);
+      if (tr && ct == 0 && jj < kTraceUnits) tr[5 + 4 * jj] = globaltimer_ns();
+      if (++rs == nst) {
+        rs = 0;
+        rph ^= 1u;
+      }
+    }
+    // ------------------------------------------- cluster merge (Eqn 2), O / n
+
+    if (tr && tid == kConsumer0 * 32) tr[1] = globaltimer_ns();  // consumers done with their units
+    // the caller row of this warp's first merge state, loaded before the barrier
+    const int mw0 = rank + cs * (warp - kConsumer0);
+    int mcaller = mw0 < hg * brows ? t.row_caller[brow0 + mw0 % brows] : 0;
+    cluster_sync();
+    if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 1] = globaltimer_ns();  // merge start (after the cluster barrier)
+    {
+      // (head, row) state i: rank i % cs, consumer warp (i / cs) % NC; the loads
+      // of a batch of ranks ((m, n) and the lane's columns) in flight before any use
+      constexpr int CPL = D / 32;  // columns per lane (4 for d = 128, 2 for d = 64)
+      constexpr int MB = 8;        // ranks per load batch (registers)
+      const uint32_t st_base = smem_u32(st);
+      const int mw = warp - kConsumer0;
+      for (int i = rank + cs * mw; mw >= 0 && i < hg * brows; i += cs * kNC) {
+        const uint32_t row_addr = st_base + (uint32_t)(i * SR) * 4u;
+        float M = -INFINITY, nsum = 0.f, acc[CPL];
+  #pragma unroll
+        for (int e = 0; e < CPL; ++e) acc[e] = 0.f;
+        for (int j0 = 0; j0 < cs; j0 += MB) {
+          float2 mn[MB];
+          float ov[MB][CPL];
+  #pragma unroll
+          for (int j = 0; j < MB; ++j) {
+            if (j0 + j < cs) {
+              const uint32_t rb = mapa(row_addr, (uint32_t)(j0 + j));
+              mn[j] = ld_cluster_f2(rb + D * 4u);
+              if constexpr (CPL == 4) {
+                const float4 o = ld_cluster_f4(rb + lane * 16u);
+                ov[j][0] = o.x;
+                ov[j][1] = o.y;
+                ov[j][2] = o.z;
+                ov[j][3] = o.w;
+              } else {
+                const float2 o = ld_cluster_f2(rb + lane * 8u);
+                ov[j][0] = o.x;
+                ov[j][1] = o.y;
+              }
+            } else {
+              mn[j] = make_float2(-INFINITY, 0.f);
+  #pragma unroll
+              for (int e = 0; e < CPL; ++e) ov[j][e] = 0.f;
+            }
+          }
+          // rebase the running sum and this batch to their common max (Eqn 2), rank order
+          float Mb = M;
+  #pragma unroll
+          for (int j = 0; j < MB; ++j) Mb = fmaxf(Mb, mn[j].x);
+          if (Mb != -INFINITY) {
+            const float wr = M == -INFINITY ? 0.f : fast_exp2(M - Mb);
+            nsum *= wr;
+  #pragma unroll
+            for (int e = 0; e < CPL; ++e) acc[e] *= wr;
+  #pragma unroll
+            for (int j = 0; j < MB; ++j) {
+              const float w = mn[j].x == -INFINITY ? 0.f : fast_exp2(mn[j].x - Mb);
+              nsum = fmaf(w, mn[j].y, nsum);
+  #pragma unroll
+              for (int e = 0; e < CPL; ++e) acc[e] = fmaf(w, ov[j][e], acc[e]);
+            }
+            M = Mb;
+          }
+        }
+        const int hh = i / brows, row = brow0 + i % brows;
+        const float inv = 1.f / nsum;
+        const int caller = i == mw0 ? mcaller : t.row_caller[row];
+        TO* orow = out + ((size_t)caller * h + head0 + hh) * D + lane * CPL;
+        if constexpr (std::is_same<TO, float>::value) {
+          if constexpr (CPL == 4)
+            *reinterpret_cast<float4*>(orow) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+          else
+            *reinterpret_cast<float2*>(orow) = make_float2(acc[0] * inv, acc[1] * inv);
+        } else {
+          if constexpr (CPL == 4)
+            *reinterpret_cast<uint2*>(orow) =
+                make_uint2(Mma<TO>::pack(acc[0] * inv, acc[1] * inv), Mma<TO>::pack(acc[2] * inv, acc[3] * inv));
+          else
+            *reinterpret_cast<uint32_t*>(orow) = Mma<TO>::pack(acc[0] * inv, acc[1] * inv);
+        }
+      }
+    }
+    if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 2] = globaltimer_ns();  // merge loop done (rank's states written)
+    cluster_sync();  // no CTA leaves while another still reads its shared memory
+  }
+  if (tr && tid == 0) tr[2] = globaltimer_ns();
+}
+
+template <typename T, typename TO, int D, int TPW>
+const void* dk_kernel_ptr() {
+  return (const void*)dk_kernel<T, TO, D, TPW>;
+}
+
+template <typename T, typename TO, int D>
+const void* dk_kernel_tpw(int tpw) {
+  return tpw == 16 ? dk_kernel_ptr<T, TO, D, 16>() : dk_kernel_ptr<T, TO, D, 32>();
+}
+
+template <typename T, typename TO>
+const void* dk_kernel_d(int d, int tpw) {
+  return d == 128 ? dk_kernel_tpw<T, TO, 128>(tpw) : dk_kernel_tpw<T, TO, 64>(tpw);
+}
+
+template <typename T>
+const void* dk_kernel_out(int out_dtype, int d, int tpw) {
+  if (out_dtype == DT_F32) return dk_kernel_d<T, float>(d, tpw);
+  if (out_dtype == DT_F16) return dk_kernel_d<T, __half>(d, tpw);
+  return dk_kernel_d<T, __nv_bfloat16>(d, tpw);
+}
+
+const void* dk_kernel_for(const PoolGeom& p, int out_dtype) {
+  const int tpw = sf_mma_tpw(p.dtype, p.c, true);
+  return p.dtype == DT_F16 ? dk_kernel_out<__half>(out_dtype, p.d, tpw)
+                           : dk_kernel_out<__nv_bfloat16>(out_dtype, p.d, tpw);
+}
+
+// the kernel's shared-memory size, and (once) the non-portable cluster opt-in
+cudaError_t dk_prepare(const void* kern, size_t smem) {
+  cudaError_t e = set_smem_once(kern, smem);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, bool> done;
+  int dev = 0;
+  e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({kern, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) done[{kern, dev}] = true;
+  return e;
+}
+
+template <typename T, typename TO, int D, int TPW>
+cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend& ap, cudaStream_t st) {
+  const PoolGeom& p = a.pool;
+  const size_t stage = dk_stage_bytes(p.dtype, p.c, D);
+  const int nst = dk_stages(p.dtype, p.c, D);
+  const size_t smem = dk_smem_bytes(p.dtype, p.c, D);
+  auto kern = dk_kernel<T, TO, D, TPW>;
+  cudaError_t e = dk_prepare((const void*)kern, smem);
+  if (e != cudaSuccess) return e;
+  const int cs = t.dk_cs;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(t.dk_groups * cs));
+  cfg.blockDim = dim3(kDkThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeClusterDimension;
+  attr[na].val.clusterDim.x = (unsigned)cs;
+  attr[na].val.clusterDim.y = 1;
+  attr[na].val.clusterDim.z = 1;
+  ++na;
+  if (a.use_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  T* kp = (T*)p.k + (size_t)a.layer * p.layer_stride;
+  T* vp = (T*)p.v + (size_t)a.layer * p.layer_stride;
+  return cudaLaunchKernelEx(&cfg, kern, kp, vp, (const T*)a.q, (TO*)a.out, (const T*)ap.k, (const T*)ap.v,
+                            ap.len_out, (int32_t)ap.mode, t, (int32_t)p.h, (int32_t)p.c, a.scale_log2, (int32_t)nst,
+                            (uint32_t)stage, (int32_t)cs, (int32_t)t.dk_hg, a.trace);
+}
+
+template <typename T, typename TO, int D>
+cudaError_t dk_tpw(const AttnLaunch& a, const DevTables& t, const DkAppend& ap, cudaStream_t st) {
+  switch (sf_mma_tpw(a.pool.dtype, a.pool.c, true)) {
+    case 16: return launch_dk_t<T, TO, D, 16>(a, t, ap, st);
+    case 32: return launch_dk_t<T, TO, D, 32>(a, t, ap, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <typename T>
+cudaError_t dk_dispatch(const AttnLaunch& a, const DevTables& t, const DkAppend& ap, cudaStream_t st) {
+  const int d = a.pool.d;
+#define CA_CASE(DD, TO) \
+  if (d == DD) return dk_tpw<T, TO, DD>(a, t, ap, st);
+  if (a.out_dtype == DT_F32) {
+    CA_CASE(64, float) CA_CASE(128, float)
+  } else if (a.out_dtype == DT_F16) {
+    CA_CASE(64, __half) CA_CASE(128, __half)
+  } else {
+    CA_CASE(64, __nv_bfloat16) CA_CASE(128, __nv_bfloat16)
+  }
+#undef CA_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+size_t dk_stage_bytes(int32_t dtype, int32_t c, int32_t d) {
+  const size_t e = (size_t)dtype_bytes(dtype);
+  // K tile | V tile | NC q rows | NC new (K, V) row pairs (PACK)
+  return ((size_t)2 * c * d * e + (size_t)3 * kNC * d * e + 127) / 128 * 128;
+}
+
+size_t dk_state_bytes(int32_t d) { return (size_t)kStateRows * (d + 4) * 4; }
+
+int dk_stages(int32_t dtype, int32_t c, int32_t d) {
+  const size_t budget = kDkSmemBudget - dk_state_bytes(d);
+  return (int)std::min<size_t>(kDkMaxStages, budget / dk_stage_bytes(dtype, c, d));
+}
+
+size_t dk_smem_bytes(int32_t dtype, int32_t c, int32_t d) {
+  return (size_t)dk_stages(dtype, c, d) * dk_stage_bytes(dtype, c, d) + dk_state_bytes(d);
+}
+
+int dk_consumer_warps() { return kNC; }
+
+bool dk_supported(const PoolGeom& p) {
+  if (p.dtype == DT_F32 || (p.d != 64 && p.d != 128)) return false;
+  const int tpw = sf_mma_tpw(p.dtype, p.c, true);
+  if (tpw != 16 && tpw != 32) return false;  // c in {16, 32, 48, 64, 96, 128}
+  if (p.c % 16 != 0 || p.c / tpw > kNC) return false;
+  return dk_stages(p.dtype, p.c, p.d) >= 3;
+}
+
+cudaError_t launch_decode(const AttnLaunch& a, const DevTables& t, const DkAppend& ap, cudaStream_t st) {
+  if (t.b == 0 || t.dk_groups == 0) return cudaSuccess;
+  switch (a.pool.dtype) {
+    case DT_F16: return dk_dispatch<__half>(a, t, ap, st);
+    case DT_BF16: return dk_dispatch<__nv_bfloat16>(a, t, ap, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int dk_max_active_clusters(const PoolGeom& p, int out_dtype, int cs) {
+  if (!dk_supported(p)) return 0;
+  const void* kern = dk_kernel_for(p, out_dtype);
+  const size_t smem = dk_smem_bytes(p.dtype, p.c, p.d);
+  if (dk_prepare(kern, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(cs * 64));
+  cfg.blockDim = dim3(kDkThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+}  // namespace pakv

@@ -32,7 +32,14 @@ struct DevTables {
   int32_t n_cf_units;
   int32_t fused;              // chunk-first runs inside the persistent seq-first kernel
   int32_t b, n_cf_tiles, max_tile_rows, n_sf_ctas;
+  // K5 cluster decode (decode.cu, schedule.h "dk" tables)
+  const int32_t* dk_block;    // [blocks][4] {first row, rows}
+  const int32_t* dk_cta;      // [blocks * cs][4] {u0, u1}: units of CTA rank r of the block's clusters
+  const int32_t* dk_unit;     // [units][4] {chunk, row0, rows, DK_* flags}
+  int32_t dk_cs, dk_groups, dk_max_rows, dk_blocks, dk_hg;
 };
+
+
 
 // Trace record per CTA (debug timing, option "trace"): words
 //   [0] kernel entry, [1] producer done, [2] consumers done,
@@ -75,6 +82,25 @@ struct AttnLaunch {
   bool use_pdl;
 };
 
+// K5 cluster decode launch: the step's append (mode bit 0: scatter k/v, the
+// caller-order [n][h][d] rows of this layer; bit 1: lengths advance by one and
+// are written to len_out, the other length buffer) folded into the attend.
+struct DkAppend {
+  const void* k;
+  const void* v;
+  int32_t* len_out;
+  int32_t mode;
+};
+bool dk_supported(const PoolGeom& pool);
+size_t dk_stage_bytes(int32_t dtype, int32_t c, int32_t d);
+size_t dk_state_bytes(int32_t d);
+int dk_stages(int32_t dtype, int32_t c, int32_t d);
+size_t dk_smem_bytes(int32_t dtype, int32_t c, int32_t d);
+int dk_consumer_warps();
+// clusters of cs CTAs that can be co-resident (cudaOccupancyMaxActiveClusters), 0 if unsupported
+int dk_max_active_clusters(const PoolGeom& pool, int out_dtype, int cs);
+cudaError_t launch_decode(const AttnLaunch& a, const DevTables& t, const DkAppend& ap, cudaStream_t st);
+
 // Prefill attention with prefix lookup (prefill.cu): tile record (kPfTileInts
 // int32) {chunk list offset, first query row, queries (<= 64), position of the
 // first query, sequence length, 0, 0, 0}; chunk lists are path order.
@@ -110,6 +136,28 @@ cudaError_t launch_append_kv(const PoolGeom& pool, const DevTables& t, const App
 // (chunk of position p = chunks[p/c - first_pos/c]); src [m][L][h][d].
 cudaError_t launch_copy_rows(const PoolGeom& pool, const int32_t* chunks, int32_t n_chunks, int64_t first_pos,
                              int64_t m, const void* k, const void* v, cudaStream_t st);
+
+// Tokens per consumer warp of the MMA seq-first kernel for (dtype, chunk size),
+// 0 when that kernel does not take the shape (fp32, or no tpw in {16, 32, 64}
+// with c % tpw == 0 and c / tpw <= 4 consumer warps) and the SIMT consumers
+// run instead.  The fused schedule (chunk-first units inside the persistent
+// kernel) needs the MMA kernel: the SIMT consumers never run chunk-first units.
+inline int sf_mma_tpw(int32_t dtype, int32_t c, bool sf_tensor_cores) {
+  if (dtype == DT_F32 || !sf_tensor_cores) return 0;
+  for (int tpw : {16, 32, 64})
+    if (c % tpw == 0 && c / tpw <= 4) return tpw;
+  return 0;
+}
+// Shared memory of one persistent seq-first CTA at its minimum ring depth (2
+// stages) and whether it fits the 227 KB opt-in limit (valid_config rejects
+// shapes that do not).
+size_t seq_first_min_smem(int32_t dtype, int32_t c, int32_t d);
+constexpr size_t kMaxSmemPerCta = 227 * 1024;
+// CTAs of the persistent seq-first kernel that can be resident at once on the
+// current device for this launch configuration (occupancy x SMs), 0 on error.
+// The fused schedule's cross-CTA merges assume the grid is one wave: the
+// host clamps the grid to this.
+int seq_first_resident_ctas(const PoolGeom& pool, int out_dtype, int sf_ctas_per_sm, bool sf_tensor_cores);
 
 // K3: chunk-first phase (Alg 1) -> partial slots.
 cudaError_t launch_chunk_first(const AttnLaunch& a, const DevTables& t, cudaStream_t st);

@@ -41,9 +41,13 @@ struct WarpAttn {
   // chunk-first phase is latency-bound at 16 tokens per call).
   // CAUSAL (prefill): additionally, row lo / hi (lane >> 2, + 8) sees only
   // tokens < lim_lo / lim_hi of the tile.
+  // sp_tok >= 0: that token's K and V rows are not in the tile but at sp_k /
+  // sp_v (row-major, unswizzled) -- the decode step's new row, read straight
+  // from where it was staged (each lane addresses its own ldmatrix row).
   template <bool MASK, int NTOK = TPW, bool CAUSAL = false>
   CA_DEV void chunk(const uint32_t (&qa)[KS][4], uint32_t k_u32, uint32_t v_u32, int tok0, int nvalid,
-                    float scale_log2, int lane, int lim_lo = 0, int lim_hi = 0) {
+                    float scale_log2, int lane, int lim_lo = 0, int lim_hi = 0, int sp_tok = -1,
+                    uint32_t sp_k = 0, uint32_t sp_v = 0) {
     constexpr int NT = NTOK / 8;
     const int mi = lane >> 3, r8 = lane & 7;
     float sc[NT][4];
@@ -57,7 +61,9 @@ struct WarpAttn {
 #pragma unroll
       for (int np = 0; np < NT / 2; ++np) {
         const int tok = tok0 + np * 16 + (mi >> 1) * 8 + r8;
-        ldmatrix_x4(k_u32 + tile_off<D>(tok, ks * 16 + (mi & 1) * 8), dst[np][0], dst[np][1], dst[np][2], dst[np][3]);
+        const int col = ks * 16 + (mi & 1) * 8;
+        const uint32_t a = tok == sp_tok ? sp_k + col * 2 : k_u32 + tile_off<D>(tok, col);
+        ldmatrix_x4(a, dst[np][0], dst[np][1], dst[np][2], dst[np][3]);
       }
     };
     load_k(0, kb[0]);
@@ -136,13 +142,15 @@ struct WarpAttn {
       }
       // V fragments one d-pair ahead of the mma (see load_k)
       const int vtok = tok0 + kk * 16 + (mi & 1) * 8 + r8;
+      const bool vsp = vtok == sp_tok;
+      auto vaddr = [&](int col) { return vsp ? sp_v + col * 2 : v_u32 + tile_off<D>(vtok, col); };
       uint32_t vb[2][4];
-      ldmatrix_x4_trans(v_u32 + tile_off<D>(vtok, (mi >> 1) * 8), vb[0][0], vb[0][1], vb[0][2], vb[0][3]);
+      ldmatrix_x4_trans(vaddr((mi >> 1) * 8), vb[0][0], vb[0][1], vb[0][2], vb[0][3]);
 #pragma unroll
       for (int dp = 0; dp < DT / 2; ++dp) {
         if (dp + 1 < DT / 2) {
           uint32_t(&nx)[4] = vb[(dp + 1) & 1];
-          ldmatrix_x4_trans(v_u32 + tile_off<D>(vtok, (dp + 1) * 16 + (mi >> 1) * 8), nx[0], nx[1], nx[2], nx[3]);
+          ldmatrix_x4_trans(vaddr((dp + 1) * 16 + (mi >> 1) * 8), nx[0], nx[1], nx[2], nx[3]);
         }
         uint32_t b0 = vb[dp & 1][0], b1 = vb[dp & 1][1], b2 = vb[dp & 1][2], b3 = vb[dp & 1][3];
         if (MASK) {

@@ -239,12 +239,15 @@ CA_DEV void sf_produce(SfShared<D, NG>& S, unsigned char* smem_raw, const T* __r
       const int4 d2 = *reinterpret_cast<const int4*>(t.sf_unit + (size_t)(u + pf) * kSfUnitInts);
       if (d2.x >= 0) {
         const int row2 = d2.y / h;
-        const int nt2 = min(c, t.seq_len[row2] - (t.sf_first[row2] + d2.z * c));
-        pf_k = kpool + ((size_t)d2.x * h + (d2.y % h)) * c * D;
-        pf_bytes = (uint32_t)(nt2 * D * (int)sizeof(T));
+        // only full non-last chunks: a last chunk's length is written by this
+        // step's append (read before the PDL wait it would race)
+        if (d2.z < d2.w - 1) {
+          pf_k = kpool + ((size_t)d2.x * h + (d2.y % h)) * c * D;
+          pf_bytes = (uint32_t)(c * D * (int)sizeof(T));
+        }
       }
     }
-    if (base == u0 && lane < pf && u < u1 && chunk >= 0) {  // the first pf units of the CTA
+    if (base == u0 && lane < pf && u < u1 && chunk >= 0 && nt > 0) {  // the first pf units of the CTA (known length)
       const size_t off = ((size_t)chunk * h + (item % h)) * c * D;
       bulk_prefetch_l2(kpool + off, (uint32_t)(nt * D * (int)sizeof(T)));
       bulk_prefetch_l2(vpool + off, (uint32_t)(nt * D * (int)sizeof(T)));
@@ -938,14 +941,26 @@ __global__ void __launch_bounds__(128) cf_simt_kernel(const T* __restrict__ kpoo
 
 cudaError_t set_smem(const void* kern, size_t smem) { return set_smem_once(kern, smem); }
 
+size_t sf_stage_bytes(int32_t dtype, int32_t c, int32_t d) {
+  const size_t e = (size_t)dtype_bytes(dtype);
+  const size_t kv = (size_t)2 * c * d * e;
+  return (kv + d * e + (size_t)kMaxPrefetchSlots * (d + 4) * 4 + 127) / 128 * 128;
+}
+
+// ring depth for the per-CTA shared-memory budget (>= 2; valid_config
+// guarantees two stages fit the opt-in limit)
+int sf_stages(int32_t dtype, int32_t c, int32_t d, int sf_ctas_per_sm) {
+  const size_t stage = sf_stage_bytes(dtype, c, d);
+  const size_t budget = sf_ctas_per_sm == 1 ? (size_t)216 * 1024 : (size_t)108 * 1024;  // per CTA
+  int nst = (int)std::min<size_t>(kMaxStages, budget / stage);
+  return std::max(2, nst);
+}
+
 template <typename T, typename TO, int D, bool MMA, int TPW>
 cudaError_t launch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   const PoolGeom& p = a.pool;
-  const size_t kv = (size_t)2 * p.c * D * sizeof(T);
-  const size_t stage = (kv + D * sizeof(T) + (size_t)kMaxPrefetchSlots * (D + 4) * 4 + 127) / 128 * 128;
-  const size_t budget = a.sf_ctas_per_sm == 1 ? (size_t)216 * 1024 : (size_t)108 * 1024;  // per CTA
-  int nst = (int)std::min<size_t>(kMaxStages, budget / stage);
-  nst = std::max(2, nst);
+  const size_t stage = sf_stage_bytes(p.dtype, p.c, D);
+  const int nst = sf_stages(p.dtype, p.c, D, a.sf_ctas_per_sm);
   const size_t smem = nst * stage;
   auto kern = sf_persistent_kernel<T, TO, D, MMA, TPW>;
   cudaError_t e = set_smem((const void*)kern, smem);
@@ -976,12 +991,7 @@ cudaError_t launch_cf_simt(const AttnLaunch& a, const DevTables& t, cudaStream_t
 }
 
 // tokens per consumer warp of the MMA seq-first kernel (0 = use SIMT)
-int sf_tpw(const AttnLaunch& a) {
-  if (a.pool.dtype == DT_F32 || !a.sf_tensor_cores) return 0;
-  for (int tpw : {16, 32, 64})
-    if (a.pool.c % tpw == 0 && a.pool.c / tpw <= kConsumerWarps) return tpw;
-  return 0;
-}
+int sf_tpw(const AttnLaunch& a) { return sf_mma_tpw(a.pool.dtype, a.pool.c, a.sf_tensor_cores); }
 
 template <typename T, typename TO, int D>
 cudaError_t dispatch_sf_tpw(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
@@ -1014,6 +1024,35 @@ cudaError_t dispatch_sf(const AttnLaunch& a, const DevTables& t, cudaStream_t st
   return cudaErrorInvalidValue;
 }
 
+template <typename T, typename TO, int D>
+const void* sf_kernel_tpw(int tpw) {
+  if constexpr (std::is_same<T, float>::value) {
+    return (const void*)sf_persistent_kernel<T, TO, D, false, 16>;
+  } else {
+    switch (tpw) {
+      case 16: return (const void*)sf_persistent_kernel<T, TO, D, true, 16>;
+      case 32: return (const void*)sf_persistent_kernel<T, TO, D, true, 32>;
+      case 64: return (const void*)sf_persistent_kernel<T, TO, D, true, 64>;
+      default: return (const void*)sf_persistent_kernel<T, TO, D, false, 16>;
+    }
+  }
+}
+
+template <typename T>
+const void* sf_kernel_ptr(int d, int od, int tpw) {
+#define CA_CASE(DD, TO) \
+  if (d == DD) return sf_kernel_tpw<T, TO, DD>(tpw);
+  if (od == DT_F32) {
+    CA_CASE(64, float) CA_CASE(128, float)
+  } else if (od == DT_F16) {
+    CA_CASE(64, __half) CA_CASE(128, __half)
+  } else {
+    CA_CASE(64, __nv_bfloat16) CA_CASE(128, __nv_bfloat16)
+  }
+#undef CA_CASE
+  return nullptr;
+}
+
 template <typename T>
 cudaError_t dispatch_cf(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   if (a.pool.d == 64) return launch_cf_simt<T, 64>(a, t, st);
@@ -1022,6 +1061,24 @@ cudaError_t dispatch_cf(const AttnLaunch& a, const DevTables& t, cudaStream_t st
 }
 
 }  // namespace
+
+size_t seq_first_min_smem(int32_t dtype, int32_t c, int32_t d) { return 2 * sf_stage_bytes(dtype, c, d); }
+
+int seq_first_resident_ctas(const PoolGeom& p, int out_dtype, int sf_ctas_per_sm, bool sf_tensor_cores) {
+  const int tpw = sf_mma_tpw(p.dtype, p.c, sf_tensor_cores);
+  const void* kern = p.dtype == DT_F32   ? sf_kernel_ptr<float>(p.d, out_dtype, tpw)
+                     : p.dtype == DT_F16 ? sf_kernel_ptr<__half>(p.d, out_dtype, tpw)
+                                         : sf_kernel_ptr<__nv_bfloat16>(p.d, out_dtype, tpw);
+  if (!kern) return 0;
+  const size_t smem = (size_t)sf_stages(p.dtype, p.c, p.d, sf_ctas_per_sm) * sf_stage_bytes(p.dtype, p.c, p.d);
+  if (set_smem(kern, smem) != cudaSuccess) return 0;
+  int dev = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSfThreads, smem) != cudaSuccess)
+    return 0;
+  return per_sm * sms;
+}
 
 cudaError_t launch_seq_first(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {
   if (t.b == 0) return cudaSuccess;

@@ -67,6 +67,33 @@ class Harness:
         for s, t in zip(ids, toks):
             self.seqs[s].append(int(t))
 
+    def append_attend(self, ids, toks, tol=None, rows=None):
+        """One fused decode step (chunkattn_append_attend: append + attend in one
+        launch), every layer in order; checked against the oracle when tol is
+        given.  Returns (max abs err or None, out of the last layer)."""
+        pos = [len(self.seqs[s]) for s in ids]
+        k, v = self.kv(toks, pos)
+        for s, t in zip(ids, toks):
+            self.seqs[s].append(int(t))
+        err, out = None, None
+        for layer in range(self.L):
+            q64 = self.queries(ids, layer)
+            out = self.ca.append_attend(ids, toks if layer == 0 else None,
+                                        k[:, layer].to(self.dev, self.dt).contiguous(),
+                                        v[:, layer].to(self.dev, self.dt).contiguous(),
+                                        q64.to(self.dev, self.dt).contiguous(), layer=layer)
+            torch.cuda.synchronize()
+            if tol is not None:
+                ref = self.oracle(ids, q64, layer, rows=rows)
+                got = out.double().cpu().numpy()
+                if rows is not None:
+                    got, ref = got[rows], ref[rows]
+                e = float(np.abs(got - ref).max()) if got.size else 0.0
+                assert np.isfinite(got).all(), "non-finite output"
+                assert e <= tol, f"layer {layer}: max abs err {e} > {tol}"
+                err = e if err is None else max(err, e)
+        return err, out
+
     def queries(self, ids, layer=0):
         q = synth.q_values(self.seed, torch.as_tensor(ids), self.step, self.L, self.h, self.d, alpha=self.alpha)
         return q[:, layer].contiguous()  # [n][h][d] fp64 (exact in dtype)

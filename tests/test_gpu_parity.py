@@ -14,10 +14,11 @@ from tests.gpu_workload import Harness, build_shared, decode_tokens
 pytestmark = pytest.mark.gpu
 
 TOL = {("f32", "f32"): 1e-5, ("f16", "f16"): 2e-3, ("bf16", "f32"): 2e-3, ("f16", "f32"): 2e-3}
-# kernel variants exercised beside the default (fused single-kernel) path: the
-# two-kernel phase pair (tcgen05 chunk-first where supported), with the
-# mma.sync chunk-first kernel, and its 4-warp CTA (PDL co-residency)
-VARIANTS = ["", "fused=0", "fused=0,cf_umma=0", "fused=0,cf_umma=0,cf_small=1"]
+# kernel variants exercised beside the default path (the K5 cluster decode
+# kernel where the shape allows): the persistent fused kernel, the two-kernel
+# phase pair (tcgen05 chunk-first where supported), with the mma.sync
+# chunk-first kernel, and its 4-warp CTA (PDL co-residency)
+VARIANTS = ["", "dk=0", "dk=0,fused=0", "dk=0,fused=0,cf_umma=0", "dk=0,fused=0,cf_umma=0,cf_small=1"]
 
 
 # --------------------------------------------------------------- config 1 ---
@@ -180,7 +181,7 @@ def test_determinism_permutation_idempotence():
 
 @pytest.mark.parametrize("dt,odt", [("f16", "f16"), ("bf16", "f32")])
 def test_split_invariance_and_simt_chunk_first(dt, odt):
-    hs = Harness(4, 128, 64, dt, odt, seed=13, alpha=8.0)
+    hs = Harness(4, 128, 64, dt, odt, seed=13, alpha=8.0, opts="dk=0")
     ids = build_shared(hs, 2048, [2, 40, 65, 1, 0, 77, 128, 5, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18])
     q64 = hs.queries(ids)
     ref = hs.oracle(ids, q64)
@@ -198,7 +199,7 @@ def test_split_invariance_and_simt_chunk_first(dt, odt):
             hs.ca.set_option(opt, 0)
 
 
-@pytest.mark.parametrize("c,opts", [(16, ""), (64, ""), (64, "fused=0")])
+@pytest.mark.parametrize("c,opts", [(16, ""), (64, ""), (64, "dk=0"), (64, "dk=0,fused=0")])
 def test_layers_independent(c, opts):
     """Two layers share one tree; each layer's attention reads its own pool
     slice (c = 64 with fused=0: the tcgen05 chunk-first's TMA row offset)."""
@@ -319,13 +320,13 @@ def test_head_sharded_handles_match_single_gpu():
     single-handle output (the chunk-first split is forced equal; the seq-first
     CTA ranges differ with the head count, so agreement is within rounding)."""
     H, d, c, seed = 8, 128, 64, 23
-    full = Harness(H, d, c, "f16", "f16", seed=seed, alpha=8.0)
+    full = Harness(H, d, c, "f16", "f16", seed=seed, alpha=8.0, opts="dk=0")
     ids = build_shared(full, 640, [3, 70, 0, 129])
     halves = []
     for h0 in (0, 4):
         def kv_fn(which, toks, pos, h0=h0):
             return synth.kv_values(seed, which, toks, pos, 1, 4, d, head_offset=h0)
-        hs = Harness(4, d, c, "f16", "f16", seed=seed, alpha=8.0, kv_fn=kv_fn)
+        hs = Harness(4, d, c, "f16", "f16", seed=seed, alpha=8.0, kv_fn=kv_fn, opts="dk=0")
         build_shared(hs, 640, [3, 70, 0, 129])
         halves.append(hs)
     q64 = full.queries(ids)
@@ -424,7 +425,7 @@ def test_tcgen05_chunk_first_wide_runs(d, c, dt, odt):
     schedule with the tcgen05 chunk-first (c = 64; c = 128 takes the mma.sync
     kernel): two row tiles per run, both head dims, a two-level tree (system prompt shared by
     all rows + a group prefix shared by 70), partial private chunks."""
-    hs = Harness(2, d, c, dt, odt, seed=11, alpha=8.0, max_chunks=1024)
+    hs = Harness(2, d, c, dt, odt, seed=11, alpha=8.0, max_chunks=1024, opts="dk=0")
     sys_p = synth.token_ids(11, synth.TAG_SYS, 0, 3 * c).tolist()
     grp = synth.token_ids(11, synth.TAG_SYS, 1, c).tolist()
     ids = []
@@ -434,17 +435,18 @@ def test_tcgen05_chunk_first_wide_runs(d, c, dt, odt):
     hs.step = 1
     hs.append(ids, decode_tokens(hs, ids))
     hs.check(ids, TOL[(dt, odt)])
-    hs2 = Harness(2, d, c, dt, odt, seed=11, alpha=8.0, max_chunks=1024, opts="cf_umma=0")
-    for i in range(130):
-        pre = sys_p + (grp if i < 70 else [])
-        hs2.add(pre + synth.token_ids(11, synth.TAG_PRIV, i, i % 37).tolist())
-    hs2.step = 1
-    hs2.append(ids, decode_tokens(hs2, ids))
-    hs2.check(ids, TOL[(dt, odt)])  # the mma.sync chunk-first on the same tree
+    for opts in ("dk=0,cf_umma=0", ""):  # the mma.sync chunk-first, then K5 (three row blocks), same tree
+        hs2 = Harness(2, d, c, dt, odt, seed=11, alpha=8.0, max_chunks=1024, opts=opts)
+        for i in range(130):
+            pre = sys_p + (grp if i < 70 else [])
+            hs2.add(pre + synth.token_ids(11, synth.TAG_PRIV, i, i % 37).tolist())
+        hs2.step = 1
+        hs2.append(ids, decode_tokens(hs2, ids))
+        hs2.check(ids, TOL[(dt, odt)])
 
 
 # ------------------------------------------- full-size shapes of the bench ---
-@pytest.mark.parametrize("opts", ["", "fused=0"])
+@pytest.mark.parametrize("opts", ["", "dk=0", "dk=0,fused=0"])
 def test_config2_full_size_last_timed_step(opts):
     """bench.py's workload at its largest timed step: b = 32, n_s = 2048, 512
     private tokens (context 2560), 32 x 128 fp16 -- every row, sampled heads
@@ -456,11 +458,13 @@ def test_config2_full_size_last_timed_step(opts):
     hs.check(ids, 2e-3, rows=list(range(0, 32, 3)))
 
 
-def test_config5_full_size_sampled_rows():
+@pytest.mark.parametrize("opts", ["", "dk=0"])
+def test_config5_full_size_sampled_rows(opts):
     """BASELINE configs[4] on one GPU: b = 256, shared prompt 4096, 64-token
-    private question + the decode token (two-kernel schedule, tcgen05
-    chunk-first): sampled rows against the fp64 oracle."""
-    hs = Harness(32, 128, 64, "f16", "f16", seed=2, alpha=8.0, max_chunks=64 + 256 * 2 + 16)
+    private question + the decode token (K5: four 64-row blocks; dk=0: the
+    two-kernel schedule, tcgen05 chunk-first): sampled rows against the fp64
+    oracle."""
+    hs = Harness(32, 128, 64, "f16", "f16", seed=2, alpha=8.0, max_chunks=64 + 256 * 2 + 16, opts=opts)
     ids = build_shared(hs, 4096, [64] * 256)
     hs.step = 1
     hs.append(ids, decode_tokens(hs, ids))

@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests/test_gpu_decode.py -x -q 2>&1 | tail -15 > gpurun_out/exp7_decode_tests.txt
+timeout 300 python tools/kernel_timeline.py --step 10 --flush clean > gpurun_out/exp7_tl_dk.txt 2>&1
+timeout 300 python tools/kernel_timeline.py --step 300 --flush clean > gpurun_out/exp7_tl_dk300.txt 2>&1
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu > gpurun_out/exp7_bench20.json 2> gpurun_out/exp7_bench.err
+timeout 300 python bench.py --steps 512 --warmup 5 --no-cpu > gpurun_out/exp7_bench512.json 2>> gpurun_out/exp7_bench.err
+timeout 300 python bench.py --steps 512 --warmup 5 --no-cpu --opt dk=0 > gpurun_out/exp7_bench512_old.json 2>> gpurun_out/exp7_bench.err

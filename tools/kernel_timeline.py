@@ -140,7 +140,32 @@ def main():
     stream.synchronize()
     tr = tr_t.view(TRACE_CTAS, TRACE_STRIDE).cpu().numpy()
     ncta = int((tr[:, 0] > 0).sum())
+    info = wl.ca.schedule_info()
+    print("schedule:", info)
     summarise(tr, args.kernel, ncta)
+    if info["dk"]:  # K5: per cluster rank (blockIdx = group * cs + rank)
+        cs = info["dk_cs"]
+        t = tr[:ncta].astype(np.int64)
+        t0 = t[:, 0][t[:, 0] > 0].min()
+        for r in range(cs):
+            sel = t[r::cs]
+            nun = [(x[5::4][:TRACE_UNITS] > 0).sum() for x in sel]
+            cdone = (sel[:, 1] - t0) / 1e3
+            mstart = (sel[:, TRACE_STRIDE - 1] - t0) / 1e3
+            end = (sel[:, 2] - t0) / 1e3
+            mloop = (sel[:, TRACE_STRIDE - 2] - t0) / 1e3
+            x = sel[0]
+            seq = []
+            for u in range(TRACE_UNITS):
+                if x[3 + 4 * u] == 0 and x[4 + 4 * u] == 0:
+                    break
+                seq.append(f"[{(x[3 + 4 * u] - t0) / 1e3:.1f}/{(x[4 + 4 * u] - t0) / 1e3:.1f}/"
+                           f"{(x[5 + 4 * u] - t0) / 1e3:.1f} {x[6 + 4 * u] // 1024}K]")
+            print(f"   rank {r} CTA 0 units issue/ready/done: " + " ".join(seq))
+            print(f"   rank {r}: traced units med {np.median(nun):.0f}; consumers done med {np.median(cdone):.2f} "
+                  f"max {cdone.max():.2f}; merge start med {np.median(mstart):.2f}; loop done med {np.median(mloop):.2f}; "
+                  f"end med {np.median(end):.2f} "
+                  f"max {end.max():.2f} us")
 
 
 if __name__ == "__main__":
