@@ -84,7 +84,10 @@ def test_config2_llama_b32_s2048(p, dt, odt, opts):
     hs.append(ids, decode_tokens(hs, ids))
     err, _ = hs.check(ids, TOL[(dt, odt)])
     ctr = hs.ca.counters()
-    assert ctr["slots"] > 0
+    info = hs.ca.schedule_info()
+    # the shared prompt runs as chunk-first work: partial slots (persistent
+    # kernels) or chunk-first units in the K5 cluster schedule
+    assert ctr["slots"] > 0 or (info["dk"] == 1 and info["dk_units"] >= 32 * info["dk_hg"])
 
 
 @pytest.mark.parametrize("mode", ["b0", "b1"])
