@@ -119,6 +119,7 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
             break;
           }
       }
+      if (groups * k > kDkXchgCtas) k = std::max<int32_t>(1, (int32_t)(kDkXchgCtas / groups));  // exchange capacity
       const int64_t ctas = groups * k;
       if (ctas > best) {
         best = ctas;
@@ -221,9 +222,14 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
           const bool last = u == cut[rk + 1] - 1 || !same(u + 1);
           dk_unit.insert(dk_unit.end(), {d[0], d[1], d[2], d[3] | (first ? DK_FIRST : 0) | (last ? DK_LAST : 0)});
         }
-        for (const auto& tl : rank_tails[rk])
+        int32_t nhelp = 0;
+        for (const auto& tl : rank_tails[rk]) {
+          const bool help = opt.dk_help && nhelp < kDkHelpTails;
+          nhelp += help ? 1 : 0;
           dk_unit.insert(dk_unit.end(), {sf_chunk[sf_ptr[tl.second + 1] - 1], tl.second, 1,
-                                         DK_PRIV | DK_TAIL | DK_PACK | DK_FIRST | DK_LAST | (tl.first << 8)});
+                                         DK_PRIV | DK_TAIL | (help ? DK_HELP : DK_PACK) | DK_FIRST | DK_LAST |
+                                             (tl.first << 8)});
+        }
         dk_cta.insert(dk_cta.end(), {(int32_t)g0, (int32_t)(dk_unit.size() / kDkUnitInts), 0, 0});
       }
     }

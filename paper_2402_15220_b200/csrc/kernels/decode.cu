@@ -56,6 +56,7 @@ namespace {
 // consumers: 128 x 72 + 256 x 216 <= 64 K).
 constexpr int kNC = 8;                           // consumer warps
 constexpr int kConsumer0 = 4;                    // first consumer warp
+constexpr int kHelpWarps = 3;                    // warps 1-3: rows' last chunks (DK_HELP)
 constexpr int kDkThreads = 12 * 32;
 constexpr int kRegsLow = 72, kRegsHigh = 216;
 constexpr int kDkMaxStages = 8;
@@ -133,13 +134,15 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     dk_kernel(T* kpool, T* vpool, const T* __restrict__ q, TO* __restrict__ out, const T* __restrict__ knew,
               const T* __restrict__ vnew, int32_t* __restrict__ len_out, int32_t mode, DevTables t, int32_t h,
               int32_t c, float scale_log2, int32_t nst, uint32_t stage_bytes, int32_t cs, int32_t hg,
-              uint64_t* __restrict__ trace) {
+              float* __restrict__ xbuf, uint64_t* __restrict__ trace) {
   using WA = WarpAttn<T, D, TPW>;
   constexpr int SR = RowState<D>::kStride;
   constexpr uint32_t kRowBytes = D * sizeof(T);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[kDkMaxStages], empty_bar[kDkMaxStages];
   __shared__ DkMeta meta[kDkMaxStages];
+  __shared__ uint64_t cons_done, help_done;  // consumers' states final / helpers' last chunks folded in
+  __shared__ int help_state[kDkHelpTails];   // state index of each helper-attended last chunk
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rank = (int)(blockIdx.x % (unsigned)cs), grp = (int)(blockIdx.x / (unsigned)cs);
@@ -151,6 +154,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   const int u0 = crec.x, u1 = crec.y;
   const uint32_t tile_bytes = (uint32_t)c * kRowBytes;
   float* st = reinterpret_cast<float*>(smem_raw + (size_t)nst * stage_bytes);  // (head, row) states
+  float* hstate = st + (size_t)kStateRows * SR;                                 // helpers' last-chunk partials
   auto state_row = [&](int hh, int row) { return st + (size_t)(hh * brows + row - brow0) * SR; };
   // mode bit 0: scatter the step's new K/V row into each row's last chunk
   // (K1 folded in); bit 1: the lengths advance by one in this launch (the
@@ -165,6 +169,8 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       mbar_init(&full_bar[s], 1);  // producer: expected bytes per copy, then one arrive with the metadata
       mbar_init(&empty_bar[s], kNC);
     }
+    mbar_init(&cons_done, 1);
+    mbar_init(&help_done, kHelpWarps);
     fence_barrier_init();
   }
   __syncthreads();
@@ -180,7 +186,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     uint32_t rph = 0;
     int pk_n = 0, pk_q = 0, pk_s = 0;  // open pack: rows, 16-token slots used, its stage
     uint32_t pk_bytes = 0;
-    const int pk_cap = c / 16;
+    const int pk_cap = c / 16;  // 16-token slots = rows of a PACK (<= NC: c <= 128); staging rows after V
     auto acquire = [&]() {
       if (jj >= nst) mbar_wait(&empty_bar[rs], rph ^ 1u);
       return rs;
@@ -222,7 +228,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         }
         bulk_g2s(stg + 2 * tile_bytes + my_idx * kRowBytes, q + src, kRowBytes, &full_bar[pk_s]);
         if (fresh) {  // the new K / V rows, row-major, into the pack's staging rows
-          unsigned char* nrow = stg + 2 * tile_bytes + (kNC + 2 * my_idx) * kRowBytes;
+          unsigned char* nrow = stg + 2 * tile_bytes + (pk_cap + 2 * my_idx) * kRowBytes;
           bulk_g2s(nrow, knew + src, kRowBytes, &full_bar[pk_s]);
           bulk_g2s(nrow + kRowBytes, vnew + src, kRowBytes, &full_bar[pk_s]);
         }
@@ -268,6 +274,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         const size_t toff = ((size_t)i_chunk * h + head) * c * D;
         const uint32_t kv_bytes = (uint32_t)i_nt * kRowBytes;
         const T* qrow = q + ((size_t)i_caller * h + head) * D;
+        if (i_flags & DK_HELP) continue;  // a helper warp attends it
         if (i_flags & DK_PACK) {
           const int slots = (i_nt + 15) >> 4;
           if (pk_n > 0 && (pk_q + slots > pk_cap || pk_n == kNC)) close_pack(d, caller, nt);
@@ -305,9 +312,138 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     const int s = acquire();
     if (lane == 0) meta[s].flags = DK_END;
     publish(s, 0);
+   } else {
+    // ------------------------------------------------------- helper warps
+    // Rows' last chunks flagged DK_HELP (Alg 2 on the CUDA cores), ordinal % 3
+    // = helper: lane = D / 32 consecutive dims, tokens in batches of 4 (K and V
+    // loads of a batch in flight together, straight from the pool's swizzled
+    // rows; this step's new row from the caller's k / v), online softmax in
+    // fp32 -> a partial per last chunk; K1: the new row into its pool slot.
+    // Folded into the (head, row) states after the consumers are done.
+    constexpr int CPL = D / 32;
+    const int hw = warp - 1, x0 = lane * CPL;
+    int ord = 0;
+    pdl_wait();
+    for (int base = u0; base < u1; base += 32) {
+      const int u = base + lane;
+      int4 d = make_int4(-1, 0, 0, 0);
+      if (u < u1) d = *reinterpret_cast<const int4*>(t.dk_unit + 4 * (size_t)u);
+      unsigned m = __ballot_sync(0xffffffffu, u < u1 && (d.w & DK_HELP));
+      while (m) {
+        const int i = __ffs(m) - 1;
+        m &= m - 1;
+        const int k = ord++;
+        if (k % kHelpWarps != hw) continue;
+        const int chunk = __shfl_sync(0xffffffffu, d.x, i), row = __shfl_sync(0xffffffffu, d.y, i);
+        const int hh = __shfl_sync(0xffffffffu, d.w, i) >> 8, head = head0 + hh;
+        const int len = t.seq_len[row] + (bump ? 1 : 0);
+        const int nt = len - t.last_start[row];
+        const size_t qoff = ((size_t)t.row_caller[row] * h + head) * D + x0;
+        const T* kb = kpool + ((size_t)chunk * h + head) * c * D;
+        const T* vb = vpool + ((size_t)chunk * h + head) * c * D;
+        float qf[CPL], o[CPL], mx = -INFINITY, n = 0.f;
+#pragma unroll
+        for (int x = 0; x < CPL / 2; ++x) {
+          const float2 qq = Mma<T>::unpack(reinterpret_cast<const uint32_t*>(q + qoff)[x]);
+          qf[2 * x] = qq.x * scale_log2;
+          qf[2 * x + 1] = qq.y * scale_log2;
+          o[2 * x] = o[2 * x + 1] = 0.f;
+        }
+        // element x0 of token tk: 16-byte group (x0 / 8) ^ (tk % 8) of its row
+        auto addr = [&](int tk) { return (size_t)tk * D + (size_t)(((x0 >> 3) ^ (tk & 7)) << 3) + (x0 & 7); };
+        for (int t0 = 0; t0 < nt; t0 += 4) {
+          uint32_t kr[4][CPL / 2], vr[4][CPL / 2];  // raw 16-bit pairs, converted at use
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int tk = t0 + e;
+            const bool fresh = append && tk == nt - 1;
+            const T* kp = fresh ? knew + qoff : kb + addr(tk);
+            const T* vp = fresh ? vnew + qoff : vb + addr(tk);
+#pragma unroll
+            for (int x = 0; x < CPL / 2; ++x) kr[e][x] = vr[e][x] = 0u;
+            if (tk < nt) {
+#pragma unroll
+              for (int x = 0; x < CPL / 2; ++x) {
+                kr[e][x] = reinterpret_cast<const uint32_t*>(kp)[x];
+                vr[e][x] = reinterpret_cast<const uint32_t*>(vp)[x];
+              }
+            }
+          }
+          float sc[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float acc = 0.f;
+#pragma unroll
+            for (int x = 0; x < CPL / 2; ++x) {
+              const float2 kv = Mma<T>::unpack(kr[e][x]);
+              acc = fmaf(qf[2 * x], kv.x, fmaf(qf[2 * x + 1], kv.y, acc));
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            sc[e] = t0 + e < nt ? acc : -INFINITY;
+          }
+          const float mn = fmaxf(mx, fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3])));
+          const float corr = mx == -INFINITY ? 0.f : fast_exp2(mx - mn);
+          n *= corr;
+#pragma unroll
+          for (int x = 0; x < CPL; ++x) o[x] *= corr;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (t0 + e < nt) {  // select, not multiply: tokens past the end never enter
+              const float p = fast_exp2(sc[e] - mn);
+              n += p;
+#pragma unroll
+              for (int x = 0; x < CPL / 2; ++x) {
+                const float2 vv = Mma<T>::unpack(vr[e][x]);
+                o[2 * x] = fmaf(p, vv.x, o[2 * x]);
+                o[2 * x + 1] = fmaf(p, vv.y, o[2 * x + 1]);
+              }
+            }
+          }
+          mx = mn;
+        }
+        float* hs = hstate + (size_t)k * SR;
+#pragma unroll
+        for (int x = 0; x < CPL; ++x) hs[x0 + x] = o[x];
+        if (lane == 0) {
+          hs[D] = mx;
+          hs[D + 1] = n;
+          help_state[k] = hh * brows + row - brow0;
+        }
+        if (append) {  // K1: this step's K / V row into its pool slot
+          const int slot = nt - 1;
+          T* kd = kpool + ((size_t)chunk * h + head) * c * D + addr(slot);
+          T* vd = vpool + ((size_t)chunk * h + head) * c * D + addr(slot);
+          if constexpr (CPL == 4) {
+            *reinterpret_cast<uint2*>(kd) = *reinterpret_cast<const uint2*>(knew + qoff);
+            *reinterpret_cast<uint2*>(vd) = *reinterpret_cast<const uint2*>(vnew + qoff);
+          } else {
+            *reinterpret_cast<uint32_t*>(kd) = *reinterpret_cast<const uint32_t*>(knew + qoff);
+            *reinterpret_cast<uint32_t*>(vd) = *reinterpret_cast<const uint32_t*>(vnew + qoff);
+          }
+        }
+      }
+    }
+    // after the consumers' last fold: this warp's partials into the states
+    mbar_wait(&cons_done, 0);
+    for (int k = hw; k < ord; k += kHelpWarps) {
+      const float* hs = hstate + (size_t)k * SR;
+      float* srow = st + (size_t)help_state[k] * SR;
+      float M, ws, wj;
+      const float ms = srow[D], ns = srow[D + 1];
+      fold_weights(ms, hs[D], M, ws, wj);
+#pragma unroll
+      for (int x = 0; x < CPL; ++x) srow[x0 + x] = fmaf(wj, hs[x0 + x], srow[x0 + x] * ws);
+      __syncwarp();
+      if (lane == 0) {
+        srow[D] = M;
+        srow[D + 1] = fmaf(wj, hs[D + 1], ns * ws);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) mbar_arrive1(&help_done);
    }
-   cluster_sync();  // the consumers' states are final (the merge reads them)
-   cluster_sync();  // the merge is done
+   if (cs > 1) cluster_sync();  // the states are published (the merge reads them)
   } else {
     // ----------------------------------------------------------- consumers
     regs_inc<kRegsHigh>();
@@ -410,7 +546,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
           q_row0(stg + 2 * tile_bytes + cw * kRowBytes);
           // the step's new token (append): its K / V rows are read from the
           // pack's staging rows, not the tile
-          const unsigned char* nrow = stg + 2 * tile_bytes + (kNC + 2 * cw) * kRowBytes;
+          const unsigned char* nrow = stg + 2 * tile_bytes + (c / 16 + 2 * cw) * kRowBytes;
           const int sp = append ? ntw - 1 : -1;
           const uint32_t sp_k = smem_u32(nrow), sp_v = sp_k + kRowBytes;
           wa.reset();
@@ -547,89 +683,97 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       }
     }
     // ------------------------------------------- cluster merge (Eqn 2), O / n
-
+    // Each CTA publishes its (head, row) states through L2 (xbuf[cta][i], 16-byte
+    // stores), one cluster barrier (release / acquire at cluster scope orders
+    // them), then state i is merged by rank i % cs, consumer warp (i / cs) % NC,
+    // over the cs ranks in rank order.  A cluster of one merges nothing.
     if (tr && tid == kConsumer0 * 32) tr[1] = globaltimer_ns();  // consumers done with their units
-    // the caller row of this warp's first merge state, loaded before the barrier
-    const int mw0 = rank + cs * (warp - kConsumer0);
-    int mcaller = mw0 < hg * brows ? t.row_caller[brow0 + mw0 % brows] : 0;
-    cluster_sync();
+    constexpr int CPL = D / 32;  // columns per lane (4 for d = 128, 2 for d = 64)
+    const int nstate = hg * brows;
+    const int mw = warp - kConsumer0;
+    const int mw0 = rank + cs * mw;
+    const int mcaller = mw0 < nstate ? t.row_caller[brow0 + mw0 % brows] : 0;  // before the barrier
+    float* xb = xbuf + (size_t)(grp * cs) * kStateRows * SR;                    // rank j's states at j * 64 * SR
+    dk_sync_consumers();  // every warp's last fold is in the states
+    if (ct == 0) mbar_arrive1(&cons_done);
+    mbar_wait(&help_done, 0);  // the helpers' last chunks are folded in
+    if (cs > 1) {
+      const float4* src = reinterpret_cast<const float4*>(st);
+      float4* dst = reinterpret_cast<float4*>(xb + (size_t)rank * kStateRows * SR);
+      for (int v = ct; v < nstate * SR / 4; v += kNC * 32) __stcg(dst + v, src[v]);
+      cluster_sync();
+    }
     if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 1] = globaltimer_ns();  // merge start (after the cluster barrier)
-    {
-      // (head, row) state i: rank i % cs, consumer warp (i / cs) % NC; the loads
-      // of a batch of ranks ((m, n) and the lane's columns) in flight before any use
-      constexpr int CPL = D / 32;  // columns per lane (4 for d = 128, 2 for d = 64)
-      constexpr int MB = 8;        // ranks per load batch (registers)
-      const uint32_t st_base = smem_u32(st);
-      const int mw = warp - kConsumer0;
-      for (int i = rank + cs * mw; mw >= 0 && i < hg * brows; i += cs * kNC) {
-        const uint32_t row_addr = st_base + (uint32_t)(i * SR) * 4u;
-        float M = -INFINITY, nsum = 0.f, acc[CPL];
-  #pragma unroll
-        for (int e = 0; e < CPL; ++e) acc[e] = 0.f;
-        for (int j0 = 0; j0 < cs; j0 += MB) {
-          float2 mn[MB];
-          float ov[MB][CPL];
-  #pragma unroll
-          for (int j = 0; j < MB; ++j) {
-            if (j0 + j < cs) {
-              const uint32_t rb = mapa(row_addr, (uint32_t)(j0 + j));
-              mn[j] = ld_cluster_f2(rb + D * 4u);
-              if constexpr (CPL == 4) {
-                const float4 o = ld_cluster_f4(rb + lane * 16u);
-                ov[j][0] = o.x;
-                ov[j][1] = o.y;
-                ov[j][2] = o.z;
-                ov[j][3] = o.w;
-              } else {
-                const float2 o = ld_cluster_f2(rb + lane * 8u);
-                ov[j][0] = o.x;
-                ov[j][1] = o.y;
-              }
+    for (int i = mw0; i < nstate; i += cs * kNC) {
+      constexpr int MB = 8;  // ranks per load batch (registers): all of a batch's loads in flight at once
+      float M = -INFINITY, nsum = 0.f, acc[CPL];
+#pragma unroll
+      for (int e = 0; e < CPL; ++e) acc[e] = 0.f;
+      for (int j0 = 0; j0 < cs; j0 += MB) {
+        float2 mn[MB];
+        float ov[MB][CPL];
+#pragma unroll
+        for (int jb = 0; jb < MB; ++jb) {
+          const int j = j0 + jb;
+          mn[jb] = make_float2(-INFINITY, 0.f);
+#pragma unroll
+          for (int e = 0; e < CPL; ++e) ov[jb][e] = 0.f;
+          if (j < cs) {
+            const float* row = j == rank ? st + (size_t)i * SR : xb + ((size_t)j * kStateRows + i) * SR;
+            mn[jb] = j == rank ? *reinterpret_cast<const float2*>(row + D) : __ldcg(reinterpret_cast<const float2*>(row + D));
+            if constexpr (CPL == 4) {
+              const float4 o = j == rank ? *reinterpret_cast<const float4*>(row + lane * 4)
+                                         : __ldcg(reinterpret_cast<const float4*>(row + lane * 4));
+              ov[jb][0] = o.x;
+              ov[jb][1] = o.y;
+              ov[jb][2] = o.z;
+              ov[jb][3] = o.w;
             } else {
-              mn[j] = make_float2(-INFINITY, 0.f);
-  #pragma unroll
-              for (int e = 0; e < CPL; ++e) ov[j][e] = 0.f;
+              const float2 o = j == rank ? *reinterpret_cast<const float2*>(row + lane * 2)
+                                         : __ldcg(reinterpret_cast<const float2*>(row + lane * 2));
+              ov[jb][0] = o.x;
+              ov[jb][1] = o.y;
             }
           }
-          // rebase the running sum and this batch to their common max (Eqn 2), rank order
-          float Mb = M;
-  #pragma unroll
-          for (int j = 0; j < MB; ++j) Mb = fmaxf(Mb, mn[j].x);
-          if (Mb != -INFINITY) {
-            const float wr = M == -INFINITY ? 0.f : fast_exp2(M - Mb);
-            nsum *= wr;
-  #pragma unroll
-            for (int e = 0; e < CPL; ++e) acc[e] *= wr;
-  #pragma unroll
-            for (int j = 0; j < MB; ++j) {
-              const float w = mn[j].x == -INFINITY ? 0.f : fast_exp2(mn[j].x - Mb);
-              nsum = fmaf(w, mn[j].y, nsum);
-  #pragma unroll
-              for (int e = 0; e < CPL; ++e) acc[e] = fmaf(w, ov[j][e], acc[e]);
-            }
-            M = Mb;
+        }
+        // rebase the running sum and this batch to their common max (Eqn 2), rank order
+        float Mb = M;
+#pragma unroll
+        for (int jb = 0; jb < MB; ++jb) Mb = fmaxf(Mb, mn[jb].x);
+        if (tr && tid == kConsumer0 * 32 && i == mw0 && j0 == 0) tr[kTraceStride - 8] = globaltimer_ns() + (Mb > 1e30f);
+        if (Mb != -INFINITY) {
+          const float wr = M == -INFINITY ? 0.f : fast_exp2(M - Mb);
+          nsum *= wr;
+#pragma unroll
+          for (int e = 0; e < CPL; ++e) acc[e] *= wr;
+#pragma unroll
+          for (int jb = 0; jb < MB; ++jb) {
+            const float w = mn[jb].x == -INFINITY ? 0.f : fast_exp2(mn[jb].x - Mb);
+            nsum = fmaf(w, mn[jb].y, nsum);
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) acc[e] = fmaf(w, ov[jb][e], acc[e]);
           }
+          M = Mb;
         }
-        const int hh = i / brows, row = brow0 + i % brows;
-        const float inv = 1.f / nsum;
-        const int caller = i == mw0 ? mcaller : t.row_caller[row];
-        TO* orow = out + ((size_t)caller * h + head0 + hh) * D + lane * CPL;
-        if constexpr (std::is_same<TO, float>::value) {
-          if constexpr (CPL == 4)
-            *reinterpret_cast<float4*>(orow) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-          else
-            *reinterpret_cast<float2*>(orow) = make_float2(acc[0] * inv, acc[1] * inv);
-        } else {
-          if constexpr (CPL == 4)
-            *reinterpret_cast<uint2*>(orow) =
-                make_uint2(Mma<TO>::pack(acc[0] * inv, acc[1] * inv), Mma<TO>::pack(acc[2] * inv, acc[3] * inv));
-          else
-            *reinterpret_cast<uint32_t*>(orow) = Mma<TO>::pack(acc[0] * inv, acc[1] * inv);
-        }
+      }
+      const int hh = i / brows, row = brow0 + i % brows;
+      const float inv = 1.f / nsum;
+      const int caller = i == mw0 ? mcaller : t.row_caller[row];
+      TO* orow = out + ((size_t)caller * h + head0 + hh) * D + lane * CPL;
+      if constexpr (std::is_same<TO, float>::value) {
+        if constexpr (CPL == 4)
+          *reinterpret_cast<float4*>(orow) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+        else
+          *reinterpret_cast<float2*>(orow) = make_float2(acc[0] * inv, acc[1] * inv);
+      } else {
+        if constexpr (CPL == 4)
+          *reinterpret_cast<uint2*>(orow) =
+              make_uint2(Mma<TO>::pack(acc[0] * inv, acc[1] * inv), Mma<TO>::pack(acc[2] * inv, acc[3] * inv));
+        else
+          *reinterpret_cast<uint32_t*>(orow) = Mma<TO>::pack(acc[0] * inv, acc[1] * inv);
       }
     }
     if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 2] = globaltimer_ns();  // merge loop done (rank's states written)
-    cluster_sync();  // no CTA leaves while another still reads its shared memory
   }
   if (tr && tid == 0) tr[2] = globaltimer_ns();
 }
@@ -711,7 +855,7 @@ cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend&
   T* vp = (T*)p.v + (size_t)a.layer * p.layer_stride;
   return cudaLaunchKernelEx(&cfg, kern, kp, vp, (const T*)a.q, (TO*)a.out, (const T*)ap.k, (const T*)ap.v,
                             ap.len_out, (int32_t)ap.mode, t, (int32_t)p.h, (int32_t)p.c, a.scale_log2, (int32_t)nst,
-                            (uint32_t)stage, (int32_t)cs, (int32_t)t.dk_hg, a.trace);
+                            (uint32_t)stage, (int32_t)cs, (int32_t)t.dk_hg, ap.xbuf, a.trace);
 }
 
 template <typename T, typename TO, int D>
@@ -743,11 +887,13 @@ cudaError_t dk_dispatch(const AttnLaunch& a, const DevTables& t, const DkAppend&
 
 size_t dk_stage_bytes(int32_t dtype, int32_t c, int32_t d) {
   const size_t e = (size_t)dtype_bytes(dtype);
-  // K tile | V tile | NC q rows | NC new (K, V) row pairs (PACK)
-  return ((size_t)2 * c * d * e + (size_t)3 * kNC * d * e + 127) / 128 * 128;
+  const size_t pk = (size_t)std::min(kNC, std::max(1, c / 16));  // rows of one PACK
+  // K tile | V tile | pk q rows | pk new (K, V) row pairs (PACK)
+  return ((size_t)2 * c * d * e + 3 * pk * d * e + 127) / 128 * 128;
 }
 
-size_t dk_state_bytes(int32_t d) { return (size_t)kStateRows * (d + 4) * 4; }
+// (head, row) states + the helpers' last-chunk partials
+size_t dk_state_bytes(int32_t d) { return (size_t)(kStateRows + kDkHelpTails) * (d + 4) * 4; }
 
 int dk_stages(int32_t dtype, int32_t c, int32_t d) {
   const size_t budget = kDkSmemBudget - dk_state_bytes(d);

@@ -90,6 +90,7 @@ struct DkAppend {
   const void* v;
   int32_t* len_out;
   int32_t mode;
+  float* xbuf;  // cluster-merge exchange: [kDkXchgCtas][64][d + 4] fp32 (workspace)
 };
 bool dk_supported(const PoolGeom& pool);
 size_t dk_stage_bytes(int32_t dtype, int32_t c, int32_t d);

@@ -154,6 +154,7 @@ def main():
             mstart = (sel[:, TRACE_STRIDE - 1] - t0) / 1e3
             end = (sel[:, 2] - t0) / 1e3
             mloop = (sel[:, TRACE_STRIDE - 2] - t0) / 1e3
+            mload = (sel[:, TRACE_STRIDE - 8] - t0) / 1e3
             x = sel[0]
             seq = []
             for u in range(TRACE_UNITS):
@@ -163,7 +164,8 @@ def main():
                            f"{(x[5 + 4 * u] - t0) / 1e3:.1f} {x[6 + 4 * u] // 1024}K]")
             print(f"   rank {r} CTA 0 units issue/ready/done: " + " ".join(seq))
             print(f"   rank {r}: traced units med {np.median(nun):.0f}; consumers done med {np.median(cdone):.2f} "
-                  f"max {cdone.max():.2f}; merge start med {np.median(mstart):.2f}; loop done med {np.median(mloop):.2f}; "
+                  f"max {cdone.max():.2f}; merge start med {np.median(mstart):.2f}; first loads med {np.median(mload):.2f}; "
+                  f"loop done med {np.median(mloop):.2f}; "
                   f"end med {np.median(end):.2f} "
                   f"max {end.max():.2f} us")
 
