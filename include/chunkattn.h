@@ -240,9 +240,6 @@ chunkattn_status chunkattn_schedule_info(chunkattn_t h, int64_t out[8]);
  *   "dk_cs"            0 = auto (largest cluster with all (row block, head)
  *                      groups co-resident), else force the cluster size 1..16
  *   "dk_max_rows"      rows per K5 row block, 16..64 (default 64)
- *   "dk_help"          1 = rows' last chunks on the K5 helper warps (SIMT,
- *                      concurrent with the consumers); 0 (default) = in the
- *                      consumers' PACK stages
  *   "dk_hg"            0 = auto, else heads per K5 cluster group
  *   "dk_shared_fixed", "dk_shared_row", "dk_pack_fixed"  K5 work-split unit
  *                      costs (hundredths / thousandths; defaults 100, 10, 15)

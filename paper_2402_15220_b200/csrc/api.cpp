@@ -33,7 +33,7 @@ chunkattn_status fail(chunkattn_status s, const std::string& msg) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t attend_perm, append_row, tables, pO, segO, counters, prefill, dk_xchg, trace, total;
+  size_t attend_perm, append_row, tables, pO, segO, counters, prefill, trace, total;
   int64_t table_cap, slot_cap, seg_cap, pf_cap;
 };
 
@@ -95,9 +95,6 @@ WsLayout ws_layout(const chunkattn_config* c) {
   w.pf_cap = (int64_t)kPfTileInts * B * ((c->max_seq_len + kPfTileRows - 1) / kPfTileRows + 1) + B * msc + 16;
   w.prefill = o;
   o = align_up(o + (size_t)4 * w.pf_cap, 256);
-  // K5 cluster-merge exchange: the (head, row) states of every CTA of one launch
-  w.dk_xchg = o;
-  o = align_up(o + (size_t)4 * kDkXchgCtas * kDkMaxRows * (c->head_dim + 4), 256);
   w.trace = o;  // debug timeline (option "trace"): the last kTraceCtas*kTraceStride u64 words
   o = align_up(o + (size_t)8 * kTraceCtas * kTraceStride, 256);
   w.total = o;
@@ -674,7 +671,7 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
   const DevTables t = h->dev_tables();
   cudaError_t e = cudaSuccess;
   if (h->ctx.dk) {  // K5: one cluster launch (attend only: lengths from the current buffer)
-    const DkAppend ap{nullptr, nullptr, nullptr, 0, reinterpret_cast<float*>(h->wsp + h->ws.dk_xchg)};
+    const DkAppend ap{nullptr, nullptr, nullptr, 0};
     e = h->timed_launch(chunkattn::K_SF, st, [&] { return launch_decode(a, t, ap, st); });
     if (e != cudaSuccess) return h->cuda_fail(e, "decode");
     ++h->n_launches;
@@ -733,7 +730,7 @@ chunkattn_status chunkattn_append_attend(chunkattn_t h, int32_t layer, int64_t n
   if (s != CA_OK) return s;
   const AttnLaunch a = h->attn_launch(layer, q, out);
   const DevTables t = h->dev_tables();
-  const DkAppend ap{k, v, h->other_len(), layer == 0 ? 3 : 1, reinterpret_cast<float*>(h->wsp + h->ws.dk_xchg)};
+  const DkAppend ap{k, v, h->other_len(), layer == 0 ? 3 : 1};
   cudaError_t e = h->timed_launch(chunkattn::K_SF, st, [&] { return launch_decode(a, t, ap, st); });
   if (e != cudaSuccess) return h->cuda_fail(e, "decode");
   ++h->n_launches;
@@ -883,8 +880,6 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->sopt.dk_shared_fixed = std::max<int64_t>(0, value) / 100.0;
   } else if (k == "dk_shared_row") {  // thousandths
     h->sopt.dk_shared_row = std::max<int64_t>(0, value) / 1000.0;
-  } else if (k == "dk_help") {
-    h->sopt.dk_help = value != 0;
   } else if (k == "dk_hg") {
     h->sopt.dk_hg_forced = (int32_t)std::max<int64_t>(0, value);
   } else if (k == "dk_pack_fixed") {  // hundredths

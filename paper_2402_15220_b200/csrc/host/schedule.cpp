@@ -119,7 +119,6 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
             break;
           }
       }
-      if (groups * k > kDkXchgCtas) k = std::max<int32_t>(1, (int32_t)(kDkXchgCtas / groups));  // exchange capacity
       const int64_t ctas = groups * k;
       if (ctas > best) {
         best = ctas;
@@ -222,15 +221,15 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
           const bool last = u == cut[rk + 1] - 1 || !same(u + 1);
           dk_unit.insert(dk_unit.end(), {d[0], d[1], d[2], d[3] | (first ? DK_FIRST : 0) | (last ? DK_LAST : 0)});
         }
-        int32_t nhelp = 0;
-        for (const auto& tl : rank_tails[rk]) {
-          const bool help = opt.dk_help && nhelp < kDkHelpTails;
-          nhelp += help ? 1 : 0;
+        for (const auto& tl : rank_tails[rk])
           dk_unit.insert(dk_unit.end(), {sf_chunk[sf_ptr[tl.second + 1] - 1], tl.second, 1,
-                                         DK_PRIV | DK_TAIL | (help ? DK_HELP : DK_PACK) | DK_FIRST | DK_LAST |
-                                             (tl.first << 8)});
-        }
-        dk_cta.insert(dk_cta.end(), {(int32_t)g0, (int32_t)(dk_unit.size() / kDkUnitInts), 0, 0});
+                                         DK_PRIV | DK_TAIL | DK_PACK | DK_FIRST | DK_LAST | (tl.first << 8)});
+        const int64_t g1 = (int64_t)dk_unit.size() / kDkUnitInts;
+        const int32_t npre = (int32_t)std::min<int64_t>(kDkCtaPre, g1 - g0);
+        dk_cta.insert(dk_cta.end(), {(int32_t)g0, (int32_t)g1, npre, 0});
+        for (int32_t k = 0; k < kDkCtaPre; ++k)
+          for (int32_t f = 0; f < kDkUnitInts; ++f)
+            dk_cta.push_back(k < npre ? dk_unit[(size_t)kDkUnitInts * (g0 + k) + f] : 0);
       }
     }
     X.dk_units = (int64_t)dk_unit.size() / kDkUnitInts;

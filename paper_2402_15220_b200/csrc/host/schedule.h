@@ -54,16 +54,13 @@ constexpr int kSfMerger = 1 << 30;
 // = units of CTA rank r of the block's clusters; block record: {row0, rows}.
 // DK_PACK: a row's last chunk packed with other rows' into one stage (one
 // row per consumer warp); DK_END: the producer's end marker (device only).
-// DK_HELP: a row's last chunk attended by a helper warp (SIMT) concurrently
-// with the consumers (the first kDkHelpTails of a CTA's last chunks).
-enum DkFlags : int32_t { DK_FIRST = 1, DK_LAST = 2, DK_TAIL = 4, DK_PRIV = 8, DK_PACK = 16, DK_END = 32, DK_HELP = 64 };
+enum DkFlags : int32_t { DK_FIRST = 1, DK_LAST = 2, DK_TAIL = 4, DK_PRIV = 8, DK_PACK = 16, DK_END = 32 };
 constexpr int kDkUnitInts = 4;
-constexpr int kDkCtaInts = 4;
+constexpr int kDkCtaInts = 16;    // {u0, u1, npre, 0, descriptors of the first npre <= kDkCtaPre units}
+constexpr int kDkCtaPre = 3;
 constexpr int kDkBlockInts = 4;
 constexpr int kDkMaxRows = 64;     // (head, row) states of one CTA: head-set size x block rows
-constexpr int kDkXchgCtas = 160;   // CTAs of one K5 launch whose states fit the merge exchange buffer
 constexpr int kDkPack = 4;         // rows' last chunks dealt per pack (16-token slots of a c = 64 stage)
-constexpr int kDkHelpTails = 24;   // last chunks per CTA attended by the helper warps (shared-memory budget)
 constexpr int kDkMaxCluster = 16;  // cluster sizes considered (> 8: non-portable)
 
 struct ScheduleOptions {
@@ -92,7 +89,6 @@ struct ScheduleOptions {
   double dk_shared_row = 0.01;
   double dk_pack_fixed = 1.3;    // a pack of last chunks = fixed + sum of valid / c / 2
   int32_t dk_hg_forced = 0;      // > 0: heads per cluster group (divides num_heads)
-  bool dk_help = false;          // last chunks on the helper warps (else all in consumer PACK stages)
 };
 
 // Offsets (int32 units) of the arrays inside the blob.

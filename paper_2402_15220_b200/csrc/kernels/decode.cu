@@ -56,7 +56,6 @@ namespace {
 // consumers: 128 x 72 + 256 x 216 <= 64 K).
 constexpr int kNC = 8;                           // consumer warps
 constexpr int kConsumer0 = 4;                    // first consumer warp
-constexpr int kHelpWarps = 3;                    // warps 1-3: rows' last chunks (DK_HELP)
 constexpr int kDkThreads = 12 * 32;
 constexpr int kRegsLow = 72, kRegsHigh = 216;
 constexpr int kDkMaxStages = 8;
@@ -89,11 +88,13 @@ CA_DEV void bulk_s2g(void* dst, const void* src, uint32_t bytes) {  // shared ->
 CA_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 CA_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 CA_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-CA_DEV void cluster_sync() {
-  asm volatile(
-      "barrier.cluster.arrive.release.aligned;\n"
-      "barrier.cluster.wait.acquire.aligned;\n" ::
-          : "memory");
+CA_DEV void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+CA_DEV void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+// 16 bytes into another CTA's shared memory, completing bytes on its mbarrier
+CA_DEV void st_async_f4(uint32_t addr, float4 v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(bar)
+               : "memory");
 }
 CA_DEV uint32_t mapa(uint32_t addr, uint32_t rank) {
   uint32_t r;
@@ -134,15 +135,14 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     dk_kernel(T* kpool, T* vpool, const T* __restrict__ q, TO* __restrict__ out, const T* __restrict__ knew,
               const T* __restrict__ vnew, int32_t* __restrict__ len_out, int32_t mode, DevTables t, int32_t h,
               int32_t c, float scale_log2, int32_t nst, uint32_t stage_bytes, int32_t cs, int32_t hg,
-              float* __restrict__ xbuf, uint64_t* __restrict__ trace) {
+              uint64_t* __restrict__ trace) {
   using WA = WarpAttn<T, D, TPW>;
   constexpr int SR = RowState<D>::kStride;
   constexpr uint32_t kRowBytes = D * sizeof(T);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[kDkMaxStages], empty_bar[kDkMaxStages];
   __shared__ DkMeta meta[kDkMaxStages];
-  __shared__ uint64_t cons_done, help_done;  // consumers' states final / helpers' last chunks folded in
-  __shared__ int help_state[kDkHelpTails];   // state index of each helper-attended last chunk
+  __shared__ uint64_t recv_bar;  // the other ranks' copies of this rank's merge states have arrived
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rank = (int)(blockIdx.x % (unsigned)cs), grp = (int)(blockIdx.x / (unsigned)cs);
@@ -150,11 +150,13 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   const int head0 = (grp % hsets) * hg, blk = grp / hsets;
   const int4 brec = *reinterpret_cast<const int4*>(t.dk_block + 4 * blk);  // {row0, rows}
   const int brow0 = brec.x, brows = brec.y;
-  const int2 crec = *reinterpret_cast<const int2*>(t.dk_cta + 4 * (blk * cs + rank));  // units [u0, u1)
-  const int u0 = crec.x, u1 = crec.y;
+  // CTA record: units [u0, u1), then the descriptors of its first kDkCtaPre units
+  const int32_t* crp = t.dk_cta + (size_t)kDkCtaInts * (blk * cs + rank);
+  const int4 crec = *reinterpret_cast<const int4*>(crp);
+  const int u0 = crec.x, u1 = crec.y, npre = crec.z;
   const uint32_t tile_bytes = (uint32_t)c * kRowBytes;
   float* st = reinterpret_cast<float*>(smem_raw + (size_t)nst * stage_bytes);  // (head, row) states
-  float* hstate = st + (size_t)kStateRows * SR;                                 // helpers' last-chunk partials
+  float* recv = st + (size_t)kStateRows * SR;  // [owned state][other rank][SR]: pushed by the other ranks
   auto state_row = [&](int hh, int row) { return st + (size_t)(hh * brows + row - brow0) * SR; };
   // mode bit 0: scatter the step's new K/V row into each row's last chunk
   // (K1 folded in); bit 1: the lengths advance by one in this launch (the
@@ -169,11 +171,13 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       mbar_init(&full_bar[s], 1);  // producer: expected bytes per copy, then one arrive with the metadata
       mbar_init(&empty_bar[s], kNC);
     }
-    mbar_init(&cons_done, 1);
-    mbar_init(&help_done, kHelpWarps);
+    mbar_init(&recv_bar, 1);
     fence_barrier_init();
   }
   __syncthreads();
+  // cluster barrier phase: every CTA's recv_bar is initialised before any
+  // rank pushes into it (waited for just before the pushes, at the end)
+  if (cs > 1) cluster_arrive();
 
   if (warp < kConsumer0) {
    regs_dec<kRegsLow>();
@@ -210,7 +214,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     // their copies issued by the lanes holding their descriptors, all at once
     // when the pack closes (packs close at the end of a 32-unit batch).
     int my_pack = -1, my_off = 0, my_idx = 0, pk_id = 0;
-    auto close_pack = [&](const int4& d, int caller, int nt) {
+    auto close_pack = [&](const int4& d, int caller, int nt, int lenv) {
       if (pk_n == 0) return;
       if (my_pack == pk_id) {
         const int hh = d.w >> 8, head = head0 + hh;
@@ -232,6 +236,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
           bulk_g2s(nrow, knew + src, kRowBytes, &full_bar[pk_s]);
           bulk_g2s(nrow + kRowBytes, vnew + src, kRowBytes, &full_bar[pk_s]);
         }
+        if (bump && head == 0) len_out[d.y] = lenv;  // the lengths of the next launch
         meta[pk_s].prow[my_idx] = d.y;
         meta[pk_s].pnt[my_idx] = nt;
         meta[pk_s].poff[my_idx] = my_off;
@@ -248,18 +253,49 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       pk_bytes = 0;
       ++pk_id;
     };
-    for (int base = u0; base < u1; base += 32) {
+    // a chunk-first or cooperative seq-first unit into the next stage
+    auto issue_unit = [&](int i_chunk, int i_row0, int i_nrows, int i_flags, int i_hh, int i_caller, int i_nt) {
+      const int head = head0 + i_hh;
+      const size_t toff = ((size_t)i_chunk * h + head) * c * D;
+      const uint32_t kv_bytes = (uint32_t)i_nt * kRowBytes;
+      const int s = acquire();
+      const bool want_q = (i_flags & DK_PRIV) && (i_flags & DK_FIRST);
+      if (lane == 0) {
+        unsigned char* stg = smem_raw + (size_t)s * stage_bytes;
+        mbar_expect_tx(&full_bar[s], 2 * kv_bytes + (want_q ? kRowBytes : 0u));
+        bulk_g2s(stg, kpool + toff, kv_bytes, &full_bar[s]);
+        bulk_g2s(stg + tile_bytes, vpool + toff, kv_bytes, &full_bar[s]);
+        if (want_q) bulk_g2s(stg + 2 * tile_bytes, q + ((size_t)i_caller * h + head) * D, kRowBytes, &full_bar[s]);
+        meta[s].flags = i_flags;
+        meta[s].nt = i_nt;
+        meta[s].row0 = i_row0;
+        meta[s].nrows = i_nrows;
+        meta[s].hh = i_hh;
+      }
+      publish(s, 2 * kv_bytes);
+    };
+    pdl_wait();  // the pool, q and the lengths may come from the previous kernel (PDL)
+    // the leading chunk-first units straight from the CTA record (one
+    // dependent load less before the first copy)
+    int upre = u0;
+    for (int k = 0; k < npre; ++k) {
+      const int4 dd = *reinterpret_cast<const int4*>(crp + 4 + 4 * k);
+      if (dd.w & DK_PRIV) break;
+      issue_unit(dd.x, dd.y, dd.z, dd.w & 0xff, dd.w >> 8, 0, c);
+      ++upre;
+    }
+    for (int base = upre; base < u1; base += 32) {
       const int u = base + lane;
       int4 d = make_int4(-1, 0, 0, 0);  // {chunk, row0, rows, flags | hh << 8}
-      int caller = 0, nt = c;
+      int caller = 0, nt = c, lenv = 0;
       if (u < u1) d = *reinterpret_cast<const int4*>(t.dk_unit + 4 * (size_t)u);
-      if (base == u0) pdl_wait();  // the pool, q and the lengths may come from the previous kernel (PDL)
+      // dependent loads of private units (caller row, length): consumed only
+      // when their unit comes up, so chunk-first units issue without waiting
       if (u < u1) {
         if (d.w & DK_PRIV) caller = t.row_caller[d.y];
-        if (d.w & DK_TAIL) {  // the row's last chunk: valid tokens from its length
-          const int len = t.seq_len[d.y] + (bump ? 1 : 0);
-          nt = len - t.last_start[d.y];
-          if (bump && head0 + (d.w >> 8) == 0) len_out[d.y] = len;  // the lengths of the next launch
+        if (d.w & DK_TAIL) {  // the row's last chunk
+          lenv = t.seq_len[d.y] + (bump ? 1 : 0);
+          nt = lenv - t.last_start[d.y];
         }
       }
       const int cnt = min(32, u1 - base);
@@ -268,16 +304,16 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         const int i_row0 = __shfl_sync(0xffffffffu, d.y, i);
         const int i_nrows = __shfl_sync(0xffffffffu, d.z, i);
         const int i_word = __shfl_sync(0xffffffffu, d.w, i);
-        const int i_caller = __shfl_sync(0xffffffffu, caller, i);
-        const int i_nt = __shfl_sync(0xffffffffu, nt, i);
         const int i_flags = i_word & 0xff, i_hh = i_word >> 8, head = head0 + i_hh;
-        const size_t toff = ((size_t)i_chunk * h + head) * c * D;
+        int i_caller = 0, i_nt = c;
+        if (i_flags & DK_PRIV) {  // warp-uniform
+          i_caller = __shfl_sync(0xffffffffu, caller, i);
+          i_nt = __shfl_sync(0xffffffffu, nt, i);
+        }
         const uint32_t kv_bytes = (uint32_t)i_nt * kRowBytes;
-        const T* qrow = q + ((size_t)i_caller * h + head) * D;
-        if (i_flags & DK_HELP) continue;  // a helper warp attends it
         if (i_flags & DK_PACK) {
           const int slots = (i_nt + 15) >> 4;
-          if (pk_n > 0 && (pk_q + slots > pk_cap || pk_n == kNC)) close_pack(d, caller, nt);
+          if (pk_n > 0 && (pk_q + slots > pk_cap || pk_n == kNC)) close_pack(d, caller, nt, lenv);
           if (pk_n == 0) pk_s = acquire();
           if (lane == i) {
             my_pack = pk_id;
@@ -289,165 +325,21 @@ __global__ void __launch_bounds__(kDkThreads, 1)
           pk_bytes += 2 * kv_bytes + kRowBytes;
           continue;
         }
-        close_pack(d, caller, nt);
-        const int s = acquire();
-        const bool want_q = (i_flags & DK_PRIV) && (i_flags & DK_FIRST);
-        if (lane == 0) {
-          unsigned char* stg = smem_raw + (size_t)s * stage_bytes;
-          mbar_expect_tx(&full_bar[s], 2 * kv_bytes + (want_q ? kRowBytes : 0u));
-          bulk_g2s(stg, kpool + toff, kv_bytes, &full_bar[s]);
-          bulk_g2s(stg + tile_bytes, vpool + toff, kv_bytes, &full_bar[s]);
-          if (want_q) bulk_g2s(stg + 2 * tile_bytes, qrow, kRowBytes, &full_bar[s]);
-          meta[s].flags = i_flags;
-          meta[s].nt = i_nt;
-          meta[s].row0 = i_row0;
-          meta[s].nrows = i_nrows;
-          meta[s].hh = i_hh;
-        }
-        publish(s, 2 * kv_bytes);
+        close_pack(d, caller, nt, lenv);
+        issue_unit(i_chunk, i_row0, i_nrows, i_flags, i_hh, i_caller, i_nt);
       }
-      close_pack(d, caller, nt);  // packs do not straddle batches (descriptors live in lanes)
+      close_pack(d, caller, nt, lenv);  // packs do not straddle batches (descriptors live in lanes)
     }
-    if (u0 >= u1) pdl_wait();
     const int s = acquire();
     if (lane == 0) meta[s].flags = DK_END;
     publish(s, 0);
-   } else {
-    // ------------------------------------------------------- helper warps
-    // Rows' last chunks flagged DK_HELP (Alg 2 on the CUDA cores), ordinal % 3
-    // = helper: lane = D / 32 consecutive dims, tokens in batches of 4 (K and V
-    // loads of a batch in flight together, straight from the pool's swizzled
-    // rows; this step's new row from the caller's k / v), online softmax in
-    // fp32 -> a partial per last chunk; K1: the new row into its pool slot.
-    // Folded into the (head, row) states after the consumers are done.
-    constexpr int CPL = D / 32;
-    const int hw = warp - 1, x0 = lane * CPL;
-    int ord = 0;
-    pdl_wait();
-    for (int base = u0; base < u1; base += 32) {
-      const int u = base + lane;
-      int4 d = make_int4(-1, 0, 0, 0);
-      if (u < u1) d = *reinterpret_cast<const int4*>(t.dk_unit + 4 * (size_t)u);
-      unsigned m = __ballot_sync(0xffffffffu, u < u1 && (d.w & DK_HELP));
-      while (m) {
-        const int i = __ffs(m) - 1;
-        m &= m - 1;
-        const int k = ord++;
-        if (k % kHelpWarps != hw) continue;
-        const int chunk = __shfl_sync(0xffffffffu, d.x, i), row = __shfl_sync(0xffffffffu, d.y, i);
-        const int hh = __shfl_sync(0xffffffffu, d.w, i) >> 8, head = head0 + hh;
-        const int len = t.seq_len[row] + (bump ? 1 : 0);
-        const int nt = len - t.last_start[row];
-        const size_t qoff = ((size_t)t.row_caller[row] * h + head) * D + x0;
-        const T* kb = kpool + ((size_t)chunk * h + head) * c * D;
-        const T* vb = vpool + ((size_t)chunk * h + head) * c * D;
-        float qf[CPL], o[CPL], mx = -INFINITY, n = 0.f;
-#pragma unroll
-        for (int x = 0; x < CPL / 2; ++x) {
-          const float2 qq = Mma<T>::unpack(reinterpret_cast<const uint32_t*>(q + qoff)[x]);
-          qf[2 * x] = qq.x * scale_log2;
-          qf[2 * x + 1] = qq.y * scale_log2;
-          o[2 * x] = o[2 * x + 1] = 0.f;
-        }
-        // element x0 of token tk: 16-byte group (x0 / 8) ^ (tk % 8) of its row
-        auto addr = [&](int tk) { return (size_t)tk * D + (size_t)(((x0 >> 3) ^ (tk & 7)) << 3) + (x0 & 7); };
-        for (int t0 = 0; t0 < nt; t0 += 4) {
-          uint32_t kr[4][CPL / 2], vr[4][CPL / 2];  // raw 16-bit pairs, converted at use
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int tk = t0 + e;
-            const bool fresh = append && tk == nt - 1;
-            const T* kp = fresh ? knew + qoff : kb + addr(tk);
-            const T* vp = fresh ? vnew + qoff : vb + addr(tk);
-#pragma unroll
-            for (int x = 0; x < CPL / 2; ++x) kr[e][x] = vr[e][x] = 0u;
-            if (tk < nt) {
-#pragma unroll
-              for (int x = 0; x < CPL / 2; ++x) {
-                kr[e][x] = reinterpret_cast<const uint32_t*>(kp)[x];
-                vr[e][x] = reinterpret_cast<const uint32_t*>(vp)[x];
-              }
-            }
-          }
-          float sc[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float acc = 0.f;
-#pragma unroll
-            for (int x = 0; x < CPL / 2; ++x) {
-              const float2 kv = Mma<T>::unpack(kr[e][x]);
-              acc = fmaf(qf[2 * x], kv.x, fmaf(qf[2 * x + 1], kv.y, acc));
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-            sc[e] = t0 + e < nt ? acc : -INFINITY;
-          }
-          const float mn = fmaxf(mx, fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3])));
-          const float corr = mx == -INFINITY ? 0.f : fast_exp2(mx - mn);
-          n *= corr;
-#pragma unroll
-          for (int x = 0; x < CPL; ++x) o[x] *= corr;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if (t0 + e < nt) {  // select, not multiply: tokens past the end never enter
-              const float p = fast_exp2(sc[e] - mn);
-              n += p;
-#pragma unroll
-              for (int x = 0; x < CPL / 2; ++x) {
-                const float2 vv = Mma<T>::unpack(vr[e][x]);
-                o[2 * x] = fmaf(p, vv.x, o[2 * x]);
-                o[2 * x + 1] = fmaf(p, vv.y, o[2 * x + 1]);
-              }
-            }
-          }
-          mx = mn;
-        }
-        float* hs = hstate + (size_t)k * SR;
-#pragma unroll
-        for (int x = 0; x < CPL; ++x) hs[x0 + x] = o[x];
-        if (lane == 0) {
-          hs[D] = mx;
-          hs[D + 1] = n;
-          help_state[k] = hh * brows + row - brow0;
-        }
-        if (append) {  // K1: this step's K / V row into its pool slot
-          const int slot = nt - 1;
-          T* kd = kpool + ((size_t)chunk * h + head) * c * D + addr(slot);
-          T* vd = vpool + ((size_t)chunk * h + head) * c * D + addr(slot);
-          if constexpr (CPL == 4) {
-            *reinterpret_cast<uint2*>(kd) = *reinterpret_cast<const uint2*>(knew + qoff);
-            *reinterpret_cast<uint2*>(vd) = *reinterpret_cast<const uint2*>(vnew + qoff);
-          } else {
-            *reinterpret_cast<uint32_t*>(kd) = *reinterpret_cast<const uint32_t*>(knew + qoff);
-            *reinterpret_cast<uint32_t*>(vd) = *reinterpret_cast<const uint32_t*>(vnew + qoff);
-          }
-        }
-      }
-    }
-    // after the consumers' last fold: this warp's partials into the states
-    mbar_wait(&cons_done, 0);
-    for (int k = hw; k < ord; k += kHelpWarps) {
-      const float* hs = hstate + (size_t)k * SR;
-      float* srow = st + (size_t)help_state[k] * SR;
-      float M, ws, wj;
-      const float ms = srow[D], ns = srow[D + 1];
-      fold_weights(ms, hs[D], M, ws, wj);
-#pragma unroll
-      for (int x = 0; x < CPL; ++x) srow[x0 + x] = fmaf(wj, hs[x0 + x], srow[x0 + x] * ws);
-      __syncwarp();
-      if (lane == 0) {
-        srow[D] = M;
-        srow[D + 1] = fmaf(wj, hs[D + 1], ns * ws);
-      }
-      __syncwarp();
-    }
-    if (lane == 0) mbar_arrive1(&help_done);
    }
-   if (cs > 1) cluster_sync();  // the states are published (the merge reads them)
+   if (cs > 1) cluster_wait();  // the cluster barrier phase begun at entry
   } else {
     // ----------------------------------------------------------- consumers
     regs_inc<kRegsHigh>();
     const int ct = tid - kConsumer0 * 32, cw = warp - kConsumer0;
+#pragma unroll 1
     for (int i = ct; i < hg * brows * SR; i += kNC * 32) st[i] = (i % SR) == D ? -INFINITY : 0.f;
     pdl_wait();  // q comes from the previous kernel
     dk_sync_consumers();  // states initialised
@@ -521,8 +413,8 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     // the CTA's first job, if chunk-first: its Q fragments (global loads)
     // overlap the first K/V copies
     bool pre = false;
-    if (u0 < u1) {
-      const int4 d0 = *reinterpret_cast<const int4*>(t.dk_unit + 4 * (size_t)u0);
+    if (npre > 0) {
+      const int4 d0 = *reinterpret_cast<const int4*>(crp + 4);
       if (!(d0.w & DK_PRIV)) {
         begin_cf(d0.y, d0.z, d0.w >> 8);
         pre = true;
@@ -683,78 +575,61 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       }
     }
     // ------------------------------------------- cluster merge (Eqn 2), O / n
-    // Each CTA publishes its (head, row) states through L2 (xbuf[cta][i], 16-byte
-    // stores), one cluster barrier (release / acquire at cluster scope orders
-    // them), then state i is merged by rank i % cs, consumer warp (i / cs) % NC,
-    // over the cs ranks in rank order.  A cluster of one merges nothing.
+    // State i is merged by rank i % cs (consumer warp (i / cs) % NC): every
+    // other rank pushes its copy of state i into the owner's recv area with
+    // st.async (bytes completing on the owner's recv_bar), the owner merges
+    // the cs copies in rank order.  No barrier after the pushes; a cluster of
+    // one merges nothing.
     if (tr && tid == kConsumer0 * 32) tr[1] = globaltimer_ns();  // consumers done with their units
     constexpr int CPL = D / 32;  // columns per lane (4 for d = 128, 2 for d = 64)
+    constexpr int Q4 = SR / 4;   // float4 per state
     const int nstate = hg * brows;
     const int mw = warp - kConsumer0;
     const int mw0 = rank + cs * mw;
-    const int mcaller = mw0 < nstate ? t.row_caller[brow0 + mw0 % brows] : 0;  // before the barrier
-    float* xb = xbuf + (size_t)(grp * cs) * kStateRows * SR;                    // rank j's states at j * 64 * SR
+    const int mcaller = mw0 < nstate ? t.row_caller[brow0 + mw0 % brows] : 0;
     dk_sync_consumers();  // every warp's last fold is in the states
-    if (ct == 0) mbar_arrive1(&cons_done);
-    mbar_wait(&help_done, 0);  // the helpers' last chunks are folded in
+    if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 3] = globaltimer_ns();  // all consumer warps done
     if (cs > 1) {
-      const float4* src = reinterpret_cast<const float4*>(st);
-      float4* dst = reinterpret_cast<float4*>(xb + (size_t)rank * kStateRows * SR);
-      for (int v = ct; v < nstate * SR / 4; v += kNC * 32) __stcg(dst + v, src[v]);
-      cluster_sync();
+      cluster_wait();  // the other ranks' recv_bar are initialised
+      if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 4] = globaltimer_ns();
+      const uint32_t rbase = smem_u32(recv);
+#pragma unroll 1
+      for (int v = ct; v < nstate * Q4; v += kNC * 32) {
+        const int i = v / Q4, q4 = v - i * Q4, owner = i % cs;
+        if (owner == rank) continue;
+        const int slot = (i / cs) * (cs - 1) + (rank < owner ? rank : rank - 1);
+        const float4 x = reinterpret_cast<const float4*>(st + (size_t)i * SR)[q4];
+        st_async_f4(mapa(rbase + (uint32_t)(slot * SR + q4 * 4) * 4u, (uint32_t)owner), x,
+                    mapa(smem_u32(&recv_bar), (uint32_t)owner));
+      }
+      if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 5] = globaltimer_ns();  // pushes issued
+      if (ct == 0) {
+        const int owned = (nstate - rank + cs - 1) / cs;
+        mbar_arrive_expect_tx(&recv_bar, (uint32_t)(owned * (cs - 1) * SR * 4));
+      }
+      mbar_wait(&recv_bar, 0);
     }
-    if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 1] = globaltimer_ns();  // merge start (after the cluster barrier)
+    if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 1] = globaltimer_ns();  // merge start (copies arrived)
+    // compact code on purpose: this runs once per CTA from a cold instruction
+    // cache (ncu: the merge phase was bound by no_instruction stalls)
+    auto copy_of = [&](int i, int j) -> const float* {
+      return j == rank ? st + (size_t)i * SR : recv + (size_t)((i / cs) * (cs - 1) + (j < rank ? j : j - 1)) * SR;
+    };
+#pragma unroll 1
     for (int i = mw0; i < nstate; i += cs * kNC) {
-      constexpr int MB = 8;  // ranks per load batch (registers): all of a batch's loads in flight at once
       float M = -INFINITY, nsum = 0.f, acc[CPL];
+#pragma unroll 1
+      for (int j = 0; j < cs; ++j) M = fmaxf(M, copy_of(i, j)[D]);
+      if (tr && tid == kConsumer0 * 32 && i == mw0) tr[kTraceStride - 8] = globaltimer_ns() + (M > 1e30f);
 #pragma unroll
       for (int e = 0; e < CPL; ++e) acc[e] = 0.f;
-      for (int j0 = 0; j0 < cs; j0 += MB) {
-        float2 mn[MB];
-        float ov[MB][CPL];
+#pragma unroll 1
+      for (int j = 0; j < cs; ++j) {  // Eqn 2, rank order
+        const float* r = copy_of(i, j);
+        const float w = r[D] == -INFINITY ? 0.f : fast_exp2(r[D] - M);
+        nsum = fmaf(w, r[D + 1], nsum);
 #pragma unroll
-        for (int jb = 0; jb < MB; ++jb) {
-          const int j = j0 + jb;
-          mn[jb] = make_float2(-INFINITY, 0.f);
-#pragma unroll
-          for (int e = 0; e < CPL; ++e) ov[jb][e] = 0.f;
-          if (j < cs) {
-            const float* row = j == rank ? st + (size_t)i * SR : xb + ((size_t)j * kStateRows + i) * SR;
-            mn[jb] = j == rank ? *reinterpret_cast<const float2*>(row + D) : __ldcg(reinterpret_cast<const float2*>(row + D));
-            if constexpr (CPL == 4) {
-              const float4 o = j == rank ? *reinterpret_cast<const float4*>(row + lane * 4)
-                                         : __ldcg(reinterpret_cast<const float4*>(row + lane * 4));
-              ov[jb][0] = o.x;
-              ov[jb][1] = o.y;
-              ov[jb][2] = o.z;
-              ov[jb][3] = o.w;
-            } else {
-              const float2 o = j == rank ? *reinterpret_cast<const float2*>(row + lane * 2)
-                                         : __ldcg(reinterpret_cast<const float2*>(row + lane * 2));
-              ov[jb][0] = o.x;
-              ov[jb][1] = o.y;
-            }
-          }
-        }
-        // rebase the running sum and this batch to their common max (Eqn 2), rank order
-        float Mb = M;
-#pragma unroll
-        for (int jb = 0; jb < MB; ++jb) Mb = fmaxf(Mb, mn[jb].x);
-        if (tr && tid == kConsumer0 * 32 && i == mw0 && j0 == 0) tr[kTraceStride - 8] = globaltimer_ns() + (Mb > 1e30f);
-        if (Mb != -INFINITY) {
-          const float wr = M == -INFINITY ? 0.f : fast_exp2(M - Mb);
-          nsum *= wr;
-#pragma unroll
-          for (int e = 0; e < CPL; ++e) acc[e] *= wr;
-#pragma unroll
-          for (int jb = 0; jb < MB; ++jb) {
-            const float w = mn[jb].x == -INFINITY ? 0.f : fast_exp2(mn[jb].x - Mb);
-            nsum = fmaf(w, mn[jb].y, nsum);
-#pragma unroll
-            for (int e = 0; e < CPL; ++e) acc[e] = fmaf(w, ov[jb][e], acc[e]);
-          }
-          M = Mb;
-        }
+        for (int e = 0; e < CPL; ++e) acc[e] = fmaf(w, r[lane * CPL + e], acc[e]);
       }
       const int hh = i / brows, row = brow0 + i % brows;
       const float inv = 1.f / nsum;
@@ -825,13 +700,14 @@ cudaError_t dk_prepare(const void* kern, size_t smem) {
 template <typename T, typename TO, int D, int TPW>
 cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend& ap, cudaStream_t st) {
   const PoolGeom& p = a.pool;
-  const size_t stage = dk_stage_bytes(p.dtype, p.c, D);
-  const int nst = dk_stages(p.dtype, p.c, D);
-  const size_t smem = dk_smem_bytes(p.dtype, p.c, D);
-  auto kern = dk_kernel<T, TO, D, TPW>;
-  cudaError_t e = dk_prepare((const void*)kern, smem);
-  if (e != cudaSuccess) return e;
   const int cs = t.dk_cs;
+  const size_t recv = dk_recv_bytes(D, t.dk_hg * t.dk_max_rows, cs);
+  const size_t stage = dk_stage_bytes(p.dtype, p.c, D);
+  const int nst = dk_stages(p.dtype, p.c, D, recv);
+  const size_t smem = dk_smem_bytes(p.dtype, p.c, D, recv);
+  auto kern = dk_kernel<T, TO, D, TPW>;
+  cudaError_t e = dk_prepare((const void*)kern, kDkSmemBudget);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(t.dk_groups * cs));
   cfg.blockDim = dim3(kDkThreads);
@@ -855,7 +731,7 @@ cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend&
   T* vp = (T*)p.v + (size_t)a.layer * p.layer_stride;
   return cudaLaunchKernelEx(&cfg, kern, kp, vp, (const T*)a.q, (TO*)a.out, (const T*)ap.k, (const T*)ap.v,
                             ap.len_out, (int32_t)ap.mode, t, (int32_t)p.h, (int32_t)p.c, a.scale_log2, (int32_t)nst,
-                            (uint32_t)stage, (int32_t)cs, (int32_t)t.dk_hg, ap.xbuf, a.trace);
+                            (uint32_t)stage, (int32_t)cs, (int32_t)t.dk_hg, a.trace);
 }
 
 template <typename T, typename TO, int D>
@@ -892,16 +768,19 @@ size_t dk_stage_bytes(int32_t dtype, int32_t c, int32_t d) {
   return ((size_t)2 * c * d * e + 3 * pk * d * e + 127) / 128 * 128;
 }
 
-// (head, row) states + the helpers' last-chunk partials
-size_t dk_state_bytes(int32_t d) { return (size_t)(kStateRows + kDkHelpTails) * (d + 4) * 4; }
+size_t dk_state_bytes(int32_t d) { return (size_t)kStateRows * (d + 4) * 4; }
 
-int dk_stages(int32_t dtype, int32_t c, int32_t d) {
-  const size_t budget = kDkSmemBudget - dk_state_bytes(d);
+size_t dk_recv_bytes(int32_t d, int32_t nstate, int32_t cs) {
+  return cs <= 1 ? 0 : (size_t)((nstate + cs - 1) / cs) * (cs - 1) * (d + 4) * 4;
+}
+
+int dk_stages(int32_t dtype, int32_t c, int32_t d, size_t recv) {
+  const size_t budget = kDkSmemBudget - dk_state_bytes(d) - recv;
   return (int)std::min<size_t>(kDkMaxStages, budget / dk_stage_bytes(dtype, c, d));
 }
 
-size_t dk_smem_bytes(int32_t dtype, int32_t c, int32_t d) {
-  return (size_t)dk_stages(dtype, c, d) * dk_stage_bytes(dtype, c, d) + dk_state_bytes(d);
+size_t dk_smem_bytes(int32_t dtype, int32_t c, int32_t d, size_t recv) {
+  return (size_t)dk_stages(dtype, c, d, recv) * dk_stage_bytes(dtype, c, d) + dk_state_bytes(d) + recv;
 }
 
 int dk_consumer_warps() { return kNC; }
@@ -911,7 +790,7 @@ bool dk_supported(const PoolGeom& p) {
   const int tpw = sf_mma_tpw(p.dtype, p.c, true);
   if (tpw != 16 && tpw != 32) return false;  // c in {16, 32, 48, 64, 96, 128}
   if (p.c % 16 != 0 || p.c / tpw > kNC) return false;
-  return dk_stages(p.dtype, p.c, p.d) >= 3;
+  return dk_stages(p.dtype, p.c, p.d, dk_state_bytes(p.d)) >= 3;  // the largest recv area
 }
 
 cudaError_t launch_decode(const AttnLaunch& a, const DevTables& t, const DkAppend& ap, cudaStream_t st) {
@@ -926,8 +805,8 @@ cudaError_t launch_decode(const AttnLaunch& a, const DevTables& t, const DkAppen
 int dk_max_active_clusters(const PoolGeom& p, int out_dtype, int cs) {
   if (!dk_supported(p)) return 0;
   const void* kern = dk_kernel_for(p, out_dtype);
-  const size_t smem = dk_smem_bytes(p.dtype, p.c, p.d);
-  if (dk_prepare(kern, smem) != cudaSuccess) {
+  const size_t smem = dk_smem_bytes(p.dtype, p.c, p.d, dk_recv_bytes(p.d, kDkMaxRows, cs));
+  if (dk_prepare(kern, kDkSmemBudget) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }

@@ -90,13 +90,13 @@ struct DkAppend {
   const void* v;
   int32_t* len_out;
   int32_t mode;
-  float* xbuf;  // cluster-merge exchange: [kDkXchgCtas][64][d + 4] fp32 (workspace)
 };
 bool dk_supported(const PoolGeom& pool);
 size_t dk_stage_bytes(int32_t dtype, int32_t c, int32_t d);
 size_t dk_state_bytes(int32_t d);
-int dk_stages(int32_t dtype, int32_t c, int32_t d);
-size_t dk_smem_bytes(int32_t dtype, int32_t c, int32_t d);
+size_t dk_recv_bytes(int32_t d, int32_t nstate, int32_t cs);
+int dk_stages(int32_t dtype, int32_t c, int32_t d, size_t recv);
+size_t dk_smem_bytes(int32_t dtype, int32_t c, int32_t d, size_t recv);
 int dk_consumer_warps();
 // clusters of cs CTAs that can be co-resident (cudaOccupancyMaxActiveClusters), 0 if unsupported
 int dk_max_active_clusters(const PoolGeom& pool, int out_dtype, int cs);

@@ -28,7 +28,7 @@ def _case(seed):
                 privates=[rng.randint(0, 3 * c) for _ in range(b)], steps=rng.randint(1, 4), rng=rng)
 
 
-@pytest.mark.parametrize("opts", ["", "dk_cs=1", "dk_cs=3", "dk_max_rows=16", "dk_help=1"])
+@pytest.mark.parametrize("opts", ["", "dk_cs=1", "dk_cs=3", "dk_max_rows=16", "dk_cs=16"])
 @pytest.mark.parametrize("seed", range(40))
 def test_append_attend_property_suite(seed, opts):
     """Random trees (shared prompt, private tails 0..3c incl. empty, 1..4 fused

@@ -155,6 +155,9 @@ def main():
             end = (sel[:, 2] - t0) / 1e3
             mloop = (sel[:, TRACE_STRIDE - 2] - t0) / 1e3
             mload = (sel[:, TRACE_STRIDE - 8] - t0) / 1e3
+            alld = (sel[:, TRACE_STRIDE - 3] - t0) / 1e3
+            cwait = (sel[:, TRACE_STRIDE - 4] - t0) / 1e3
+            pushd = (sel[:, TRACE_STRIDE - 5] - t0) / 1e3
             x = sel[0]
             seq = []
             for u in range(TRACE_UNITS):
@@ -164,7 +167,8 @@ def main():
                            f"{(x[5 + 4 * u] - t0) / 1e3:.1f} {x[6 + 4 * u] // 1024}K]")
             print(f"   rank {r} CTA 0 units issue/ready/done: " + " ".join(seq))
             print(f"   rank {r}: traced units med {np.median(nun):.0f}; consumers done med {np.median(cdone):.2f} "
-                  f"max {cdone.max():.2f}; merge start med {np.median(mstart):.2f}; first loads med {np.median(mload):.2f}; "
+                  f"max {cdone.max():.2f}; all consumers {np.median(alld):.2f}; cluster wait {np.median(cwait):.2f}; "
+                  f"pushed {np.median(pushd):.2f}; merge start med {np.median(mstart):.2f}; first loads med {np.median(mload):.2f}; "
                   f"loop done med {np.median(mloop):.2f}; "
                   f"end med {np.median(end):.2f} "
                   f"max {end.max():.2f} us")
