@@ -289,6 +289,11 @@ chunkattn_status chunkattn_kernel_times(chunkattn_t h, double ms[4], int64_t lau
 chunkattn_status chunkattn_download_tables(chunkattn_t h, void* dst, size_t cap, size_t* len,
                                            void* stream);
 
+/* Copy the host-built context tables of the current epoch (the blob the
+ * lazy upload copies) to `dst`; *len = bytes.  With
+ * chunkattn_download_tables a test checks the upload byte for byte. */
+chunkattn_status chunkattn_host_tables(chunkattn_t h, void* dst, size_t cap, size_t* len);
+
 /* Message of the last error on this thread ("" if none). */
 const char* chunkattn_last_error(void);
 

@@ -80,6 +80,7 @@ _SIGS = {
     "chunkattn_set_option": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.c_int64]),
     "chunkattn_kernel_times": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double), _I64P]),
     "chunkattn_download_tables": (ctypes.c_int, [_P, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), _P]),
+    "chunkattn_host_tables": (ctypes.c_int, [_P, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
     "chunkattn_last_error": (ctypes.c_char_p, []),
 }
 

@@ -267,3 +267,12 @@ class ChunkAttention:
         C.check(self.lib.chunkattn_download_tables(self._h, buf.ctypes.data_as(ctypes.c_void_p), ln.value,
                                                    ctypes.byref(ln), self._stream()))
         return buf[:ln.value // 4]
+
+    def host_tables(self) -> np.ndarray:
+        """The host-built context tables (int32) of the current epoch."""
+        ln = ctypes.c_size_t()
+        self.lib.chunkattn_host_tables(self._h, None, 0, ctypes.byref(ln))
+        buf = np.zeros(max(1, ln.value // 4), dtype=np.int32)
+        C.check(self.lib.chunkattn_host_tables(self._h, buf.ctypes.data_as(ctypes.c_void_p), ln.value,
+                                               ctypes.byref(ln)))
+        return buf[:ln.value // 4]

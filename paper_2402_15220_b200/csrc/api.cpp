@@ -929,6 +929,17 @@ chunkattn_status chunkattn_kernel_times(chunkattn_t h, double ms[4], int64_t lau
   return CA_OK;
 }
 
+chunkattn_status chunkattn_host_tables(chunkattn_t h, void* dst, size_t cap, size_t* len) {
+  CA_GUARD_BEGIN
+  if (!h || !len) return fail(CA_EINVAL, "bad argument");
+  const size_t bytes = h->ctx.blob.size() * 4;
+  *len = bytes;
+  if (!dst || cap < bytes) return fail(CA_ERANGE, "buffer too small");
+  std::memcpy(dst, h->ctx.blob.data(), bytes);
+  return CA_OK;
+  CA_GUARD_END
+}
+
 chunkattn_status chunkattn_download_tables(chunkattn_t h, void* dst, size_t cap, size_t* len, void* stream) {
   CA_GUARD_BEGIN
   if (!h || !len) return fail(CA_EINVAL, "bad argument");

@@ -158,3 +158,15 @@ def test_lazy_context_counters():
     ca.remove_sequence(ids[0])                      # "completed sequence leaving"
     ca.attend(ids[1:])
     assert ca.counters()["builds"] == b0 + 2
+
+
+def test_configs_whose_stages_do_not_fit_are_rejected():
+    """ADVICE: two K/V tile stages of the persistent seq-first kernel must fit
+    the 227 KB shared-memory limit -- f32 with chunk 128 x d 128 or 16-bit
+    with chunk 256 x d 128 are rejected at creation (CA_EINVAL), not at the
+    first attend."""
+    import torch
+    for dt, c in ((torch.float32, 128), (torch.float16, 256)):
+        with pytest.raises(C.ChunkAttnError):
+            ChunkAttention(4, 128, c, 64, 8, 1024, dtype=dt, device=None)
+    ChunkAttention(4, 128, 64, 64, 8, 1024, dtype=torch.float32, device=None)  # fits

@@ -126,9 +126,12 @@ def _invariants(tm, seqs):
             assert ln == tm.c                          # shared chunks are full (T1)
     used, free, created, hwm, waste = tm.memory_stats()
     assert created == used + free and used == len(recs) and hwm >= used
-    for sid, toks in seqs.items():                     # waste bound
-        last = tm.path_ids(sid)[-1]
-        assert tm.c - recs[last][2] <= tm.c - 1
+    # waste ("at most c - 1 unused slots per sequence"): only a
+    # sequence's last chunk can be partial and partial chunks are never shared
+    # (T1), so the unused slots are exactly sum over sequences of (-len) mod c,
+    # computed here from the token counts alone
+    assert waste == sum((-len(toks)) % tm.c for toks in seqs.values())
+    assert waste <= (tm.c - 1) * len(seqs)
     ids = [cid for cid in recs] + tm.free
     assert len(set(ids)) == len(ids)                   # no chunk both used and free
 
