@@ -2,34 +2,39 @@
 """Decode-attention benchmark of the B200 ChunkAttention path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--mode chunk|b0|b1] [--workload cfg2]
+                    [--mode chunk|b0|b1] [--workload auto|cfg2|cfg5]
 
-Workload (BASELINE.json configs[1], the metric's configuration): Llama-2-7B
-attention shape, 32 heads x 128 dim, fp16, chunk 64, batch 32, a shared system
-prompt of 2048 tokens (n_p = n_s = 2048, fully shared), then
-iterative decoding: a STEP is one decode iteration = append one token's K/V
-per sequence (a4, host tree a1-a3) + two-phase attention (a5 chunk-first, a6
-seq-first) for all 32 sequences.  Timed steps are completion tokens 1..K of a
-fresh cache (the warm-up runs on a cache that is then drained and refilled),
-so K = 512 reproduces the token-rate point (n_s = 2048, n_c = 512) of
-fig:cuda_attn_tps.  Token rate = b * K / t.
+Workload at N = 1 (BASELINE.json configs[1], the metric's configuration):
+Llama-2-7B attention shape, 32 heads x 128 dim, fp16, chunk 64, batch 32, a
+shared system prompt of 2048 tokens (n_p = n_s = 2048, fully shared,
+PAPER.md:348-351), then iterative decoding: a STEP is one decode iteration =
+append one token's K/V per sequence (a4, host tree a1-a3) + two-phase
+attention (a5 chunk-first, a6 seq-first) for all 32 sequences -- one call of
+chunkattn_append_attend, one kernel launch (the K5 cluster decode kernel).
+Timed steps are completion tokens 1..K of a fresh cache; token rate = b * K / t
+(PAPER.md:348).
+
+Workload at N > 1 (torchrun; BASELINE.json configs[4]): b = 256, shared
+prompt 4096, 64-token questions (p = 65 at the first step), the 32 heads split
+over the N ranks ("the head dimension is always partitioned"),
+every rank replaying the same host op stream; one NCCL all_gather_into_tensor
+of the per-rank outputs per step.  Total work is fixed (strong
+scaling); value = b * K / max-over-ranks time including the gather.
 
 Timing: CUDA events on the launch stream around each step; the L2 (126 MB on
 B200) is flushed between timed steps (outside the events) by writing a 2x-L2
-buffer and then reading it back, so L2 holds clean foreign lines: our inputs
-are cold and the step does not pay the write-back of the flush's dirty lines.  Multi-GPU (torchrun): every rank decodes its own batch of 32
-sequences (independent problems, weak scaling, no data-path collective);
-value = all ranks' tokens / max-over-ranks time.
+buffer and then reading it back, so L2 holds clean foreign lines.
 
-The JSON line adds: roofline (dominant kernel, algorithmic bytes / its CUDA
-event time, against MEASURED_PEAKS.json), cpu_baseline (the fp64 oracle on the
-host, bounded sample), e2e (same metric through the C ABI with HOST buffers,
-chunkattn_decode_step_host: H2D of q/k/v and D2H of the output inside the
-call and the timed region),
-gpu_launches, clocks, and phase_roofline: the two phases timed apart on the
-two-kernel schedule (pass D) -- the sequence-first kernel's algorithmic GB/s
-against the HBM roofline (north_star's sequence-first target) and the tcgen05
-chunk-first kernel's.
+The JSON line adds: roofline (the K5 kernel's algorithmic bytes / its
+per-launch CUDA-event time, against MEASURED_PEAKS.json), seq_first_phase (the
+north_star's >= 70 % HBM target: configs[2]'s n_s = 0, b = 32, n_p = 4096
+point, K5 and the persistent seq-first kernel), sweep (configs[2] at b = 32:
+n_s = 0 / 1024 / 2048 / 4096 with the non-shared paged layout B0 beside it),
+p512 (the cfg2 step at 512 private tokens), e2e (wall clock of back-to-back
+decode steps through chunkattn_decode_step_host from pinned HOST buffers, one
+stream sync per step, plus the host microseconds of the call: tree + context
++ launch), cpu_baseline (the fp64 oracle on the host, all cores and 1 core),
+gpu_launches, clocks.
 """
 from __future__ import annotations
 
@@ -225,11 +230,14 @@ def time_steps(wl: DecodeWorkload, K: int, flush_buf, stream) -> list[float]:
     return [a.elapsed_time(b) for a, b in evs]
 
 
-def time_e2e(wl: DecodeWorkload, K: int, flush_buf, stream):
+def time_e2e_wall(wl: DecodeWorkload, K: int, stream):
     """Same steps through the C ABI with HOST buffers
-    (chunkattn_decode_step_host): every step's q, k_new, v_new come from one
-    packed pinned host buffer (one H2D inside the call) and its output goes to
-    pinned host memory (one D2H inside the call), inside the timed region."""
+    (chunkattn_decode_step_host), back to back as a serving loop runs them:
+    every step's q, k_new, v_new come from one packed pinned host buffer (one
+    H2D inside the call) and its output goes to pinned host memory (one D2H
+    inside the call); wall clock (perf_counter) around call + stream sync, no
+    L2 flush.  Also the host time of the call alone (tree a1, context a2, lazy
+    upload a3, launches)."""
     sp = stream.cuda_stream
     nq, nk = wl.q[0].numel(), wl.kn[0].numel()
     host = torch.empty((K, nq + 2 * nk), dtype=wl.q.dtype).pin_memory()
@@ -240,39 +248,121 @@ def time_e2e(wl: DecodeWorkload, K: int, flush_buf, stream):
     es = host.element_size()
     staging = torch.empty(((nq + 2 * nk) * es + 15) // 16 * 16 + wl.out.numel() * wl.out.element_size(),
                           dtype=torch.uint8, device=wl.q.device)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    with torch.cuda.stream(stream):
-        for s in range(K):
-            flush_l2(flush_buf)
-            evs[s][0].record(stream)
-            wl.ca.decode_step_host(wl.ids, wl.tokens[s], host[s], hout[s], staging, stream_ptr=sp)
-            evs[s][1].record(stream)
+    wall, hostcall = [], []
     stream.synchronize()
-    return [a.elapsed_time(b) for a, b in evs], (nq + 2 * nk) * es, wl.out.numel() * wl.out.element_size()
+    for s in range(K):
+        t0 = time.perf_counter()
+        wl.ca.decode_step_host(wl.ids, wl.tokens[s], host[s], hout[s], staging, stream_ptr=sp)
+        t1 = time.perf_counter()
+        stream.synchronize()
+        t2 = time.perf_counter()
+        wall.append(t2 - t0)
+        hostcall.append(t1 - t0)
+    return wall, hostcall, (nq + 2 * nk) * es, wl.out.numel() * wl.out.element_size()
 
 
 def cpu_baseline(seed, n_shared, question, h, d, budget_s, max_steps):
     """fp64 oracle on the host: row 0's decode step at completion tokens 1..n
-    until the budget is spent (materialisation untimed)."""
+    until the budget is spent (materialisation untimed), with the BLAS pool at
+    all host cores and at one core (threadpoolctl)."""
+    from threadpoolctl import threadpool_limits
+
     from oracle.reference import OracleSequence, timed_attend
     prompt = synth.token_ids(seed, synth.TAG_SYS, 0, n_shared).tolist()
     q0 = synth.token_ids(seed, synth.TAG_PRIV, 0, question).tolist()
-    seq = OracleSequence(seed, prompt + q0, h, d, n_shared + question + max_steps + 1)
-    wall = cpu = 0.0
-    n = 0
-    t_start = time.perf_counter()
-    while n < max_steps and time.perf_counter() - t_start < budget_s:
-        tok = int(synth.hash_py(seed, synth.TAG_DECODE, 0, n) % 31999 + 1)
-        seq.extend([tok])
-        q = synth.q_values(seed, torch.tensor([0]), n + 1, 1, h, d, alpha=8.0)[0, 0].numpy()
-        _, w, c = timed_attend(seq, q)
-        wall += w
-        cpu += c
-        n += 1
-    return {"value": n / wall, "unit": "tokens/s", "cores": max(1, round(cpu / wall)), "kind": "oracle",
+    ncores = os.cpu_count() or 1
+    res = {}
+    for label, cores, budget in (("all", ncores, budget_s / 2), ("one", 1, budget_s / 2)):
+        seq = OracleSequence(seed, prompt + q0, h, d, n_shared + question + max_steps + 1)
+        wall = cpu = 0.0
+        n = 0
+        t_start = time.perf_counter()
+        with threadpool_limits(limits=cores):
+            while n < max_steps and time.perf_counter() - t_start < budget:
+                tok = int(synth.hash_py(seed, synth.TAG_DECODE, 0, n) % 31999 + 1)
+                seq.extend([tok])
+                q = synth.q_values(seed, torch.tensor([0]), n + 1, 1, h, d, alpha=8.0)[0, 0].numpy()
+                _, w, c = timed_attend(seq, q)
+                wall += w
+                cpu += c
+                n += 1
+        res[label] = (n / wall, max(1, round(cpu / wall)), n, wall)
+    try:
+        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:
+        model = "unknown"
+    v, used, n, wall = res["all"]
+    return {"value": v, "unit": "tokens/s", "cores": used, "kind": "oracle",
+            "host_cores": ncores, "cpu_model": model, "blas_limit_all_cores": ncores,
+            "value_1core": res["one"][0], "cores_1core": 1,
             "sample": f"fp64 numpy oracle (C1), row 0 of the cfg2 batch at completion tokens 1..{n} "
                       f"(context {n_shared + question + 1}..{n_shared + question + n}); attention math only, "
-                      f"KV materialisation untimed; {wall:.1f} s of CPU work"}
+                      f"KV materialisation untimed; {wall:.1f} s (BLAS pool at all {ncores} cores) + "
+                      f"{res['one'][3]:.1f} s (1 core) of CPU work; 'cores' = threads the timed run kept busy"}
+
+
+def kernel_point(dev, flush_buf, stream, K=5, W=3, **kw):
+    """Per-kernel CUDA-event time (us per launch) and event-bracketed step time
+    of K decode steps of a DecodeWorkload (fresh cache, completion tokens 1..K)
+    and the algorithmic bytes of those steps."""
+    opts = kw.pop("opts", {})
+    wl = DecodeWorkload(dev, steps=max(K, W), **kw)
+    for k, v in opts.items():
+        wl.ca.set_option(k, v)
+    if opts.get("dk") == 0:
+        wl.one_launch = False
+    wl.fill()
+    time_steps(wl, W, flush_buf, stream)
+    wl.fill()
+    wl.ca.set_option("kernel_events", 1)
+    wl.ca.kernel_times()
+    ms = time_steps(wl, K, flush_buf, stream)
+    kt = wl.ca.kernel_times()
+    wl.ca.set_option("kernel_events", 0)
+    shapes = [wl.shape_at(s) for s in range(K)]
+    attn_ms = kt["seq_first"][0] + kt["chunk_first"][0]
+    n_attn = max(1, kt["seq_first"][1])
+    res = {"step_us": 1e3 * sum(ms) / K, "attend_kernel_us": 1e3 * attn_ms / n_attn,
+           "alg_bytes_per_step": sum(x.unique_bytes() for x in shapes) / K,
+           "seq_first_bytes_per_step": sum(x.seq_first_bytes() for x in shapes) / K,
+           "sched": wl.ca.schedule_info()}
+    del wl
+    torch.cuda.empty_cache()
+    return res
+
+
+def extra_points(dev, flush_buf, stream, hbm_peak):
+    """The north_star's own checks on the same box: the seq-first-phase HBM
+    fraction (configs[2], n_s = 0, b = 32, n_p = 4096), the configs[2] mini sweep
+    with B0, the cfg2 step at 512 private tokens."""
+    out = {}
+    sf = {}
+    for label, opts in (("k5", {}), ("persistent_seq_first", {"dk": 0})):
+        r = kernel_point(dev, flush_buf, stream, b=32, n_shared=0, question=4095, opts=opts)
+        gbs = r["alg_bytes_per_step"] / (r["attend_kernel_us"] * 1e-6) / 1e9
+        sf[label] = {"kernel_us": r["attend_kernel_us"], "alg_bytes": r["alg_bytes_per_step"], "achieved": gbs,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak, "step_us": r["step_us"]}
+    sf["workload"] = ("configs[2] n_s = 0, b = 32, n_p = 4096 (4095-token private question + the decode token): "
+                      "every byte private, the attention kernel is the sequence-first phase; per-launch CUDA events, "
+                      "completion tokens 1..5, L2 flushed")
+    out["seq_first_phase"] = sf
+    sweep = []
+    for n_s in (0, 1024, 2048, 4096):
+        row = {"n_s": n_s, "n_p": 4096, "b": 32}
+        for mode in ("chunk", "b0"):
+            r = kernel_point(dev, flush_buf, stream, b=32, n_shared=n_s, question=4096 - n_s, mode=mode)
+            row[mode] = {"step_us": r["step_us"], "kernel_us": r["attend_kernel_us"],
+                         "alg_bytes": r["alg_bytes_per_step"]}
+        row["speedup_vs_b0"] = row["b0"]["step_us"] / row["chunk"]["step_us"]
+        row["ideal_bytes_ratio"] = row["b0"]["alg_bytes"] / row["chunk"]["alg_bytes"]
+        row["chunk_frac_hbm"] = row["chunk"]["alg_bytes"] / (row["chunk"]["kernel_us"] * 1e-6) / 1e9 / hbm_peak
+        sweep.append(row)
+    out["sweep"] = sweep
+    r = kernel_point(dev, flush_buf, stream, b=32, n_shared=2048, question=511)
+    out["p512"] = {"workload": "cfg2 with a 511-token question: p = 512..516 private tokens", "step_us": r["step_us"],
+                   "kernel_us": r["attend_kernel_us"], "tokens_per_s": 32 / (r["step_us"] * 1e-6),
+                   "frac_hbm": r["alg_bytes_per_step"] / (r["attend_kernel_us"] * 1e-6) / 1e9 / hbm_peak}
+    return out
 
 
 def run_reference(args):
@@ -309,52 +399,42 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+def run_cfg2(args):
+    """N = 1: the metric's configuration (BASELINE.json configs[1])."""
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
     K, W = args.steps, args.warmup
     hbm_peak, peak_src, _ = load_peaks()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(0)
     props = torch.cuda.get_device_properties(dev)
     l2 = getattr(props, "L2_cache_size", 126 * 2 ** 20) or 126 * 2 ** 20
     flush_buf = torch.empty(2 * l2 // 4 + 1024, dtype=torch.float32, device=dev)
     stream = torch.cuda.Stream(dev)
-    wl = DecodeWorkload(dev, seed=rank, steps=max(K, W), mode=args.mode, question=args.question,
+    wl = DecodeWorkload(dev, seed=0, steps=max(K, W), mode=args.mode, question=args.question,
                         n_shared=args.n_shared, b=args.batch)
     for o in args.opt:
         key, val = o.split("=")
         wl.ca.set_option(key, int(val))
+        if key == "dk" and int(val) == 0:
+            wl.one_launch = False
     # warm-up on the same cache, then drain and refill: timed steps are tokens 1..K
     wl.fill()
     time_steps(wl, W, flush_buf, stream)
-    # spin the clocks up (~0.3 s of memsets) so the timed region runs at boost
-    t0 = time.time()
+    t0 = time.time()  # spin the clocks up (~0.3 s of memsets) so the timed region runs at boost
     while time.time() - t0 < 0.3:
         flush_l2(flush_buf)
     torch.cuda.synchronize(dev)
-    # ---- pass A: the headline number (PDL on, no per-kernel events)
+    # ---- pass A: the headline number
     wl.fill()
     c0 = wl.ca.counters()
-    if world > 1:
-        torch.distributed.barrier()
     torch.cuda.synchronize(dev)
     ms = time_steps(wl, K, flush_buf, stream)
     torch.cuda.synchronize(dev)
     c1 = wl.ca.counters()
     total_ms = sum(ms)
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-        torch.distributed.barrier()
     launches = c1["launches"] - c0["launches"]
     uploads = c1["uploads"] - c0["uploads"]
+    sched = wl.ca.schedule_info()
     # ---- pass B: per-kernel CUDA events (roofline of the dominant kernel)
     wl.fill()
     wl.ca.set_option("kernel_events", 1)
@@ -363,104 +443,198 @@ def run_ours(args):
     kt = wl.ca.kernel_times()
     wl.ca.set_option("kernel_events", 0)
     shapes = [wl.shape_at(s) for s in range(K)]
-    kbytes = {"append": sum(x.append_bytes() for x in shapes),
-              "chunk_first": sum(x.chunk_first_bytes() for x in shapes),
-              "seq_first": sum(x.seq_first_bytes() for x in shapes)}
-    if kt["chunk_first"][1] == 0:  # fused: the seq-first kernel runs the chunk-first units too
-        kbytes["seq_first"] += kbytes["chunk_first"]
-        kbytes["chunk_first"] = 0
+    fused = wl.one_launch and sched["dk"] == 1
+    if fused:  # K5: append + both phases + merge in the one kernel
+        kbytes = {"append": 0, "chunk_first": 0, "seq_first": sum(x.fused_step_bytes() for x in shapes)}
+        kname = "dk_kernel (K5 cluster decode: append + chunk-first + seq-first + cluster merge)"
+    else:
+        kbytes = {"append": sum(x.append_bytes() for x in shapes),
+                  "chunk_first": sum(x.chunk_first_bytes() for x in shapes),
+                  "seq_first": sum(x.seq_first_bytes() for x in shapes)}
+        if kt["chunk_first"][1] == 0:  # fused persistent kernel runs the chunk-first units too
+            kbytes["seq_first"] = sum(x.unique_bytes() for x in shapes)
+            kbytes["chunk_first"] = 0
+        kname = "sf_persistent_kernel"
     dom = max(("append", "chunk_first", "seq_first"), key=lambda k: kt[k][0])
     dom_ms, dom_n = kt[dom]
     achieved = kbytes[dom] / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else None
-    traffic = None
+    traffic, traffic_note = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get(f"{args.mode}:{dom}")
-    traffic_note = None
-    if isinstance(traffic, dict):  # one ncu --set full launch: its DRAM bytes vs its algorithmic bytes
-        traffic_note = {"alg_bytes_same_launch": traffic.get("alg_bytes"), "decode_step": traffic.get("step"),
-                        "capture": traffic.get("capture")}
-        traffic = traffic.get("bytes")
+            tr = json.load(f).get(f"{args.mode}:{'k5' if fused else dom}")
+        if isinstance(tr, dict):  # one ncu --set full launch of a timed step: its DRAM bytes vs algorithmic
+            traffic = tr.get("bytes")
+            traffic_note = {"alg_bytes_same_launch": tr.get("alg_bytes"), "decode_step": tr.get("step"),
+                            "capture": tr.get("capture")}
     kernels = {k: {"ms_total": kt[k][0], "launches": kt[k][1],
                    "us_avg": 1e3 * kt[k][0] / kt[k][1] if kt[k][1] else None,
-                   "alg_bytes_per_launch": kbytes[k] / kt[k][1] if kt[k][1] and k in kbytes else None,
-                   "gbs": kbytes[k] / (kt[k][0] * 1e-3) / 1e9 if kt[k][0] and k in kbytes else None}
+                   "alg_bytes_per_launch": kbytes[k] / kt[k][1] if kt[k][1] else None,
+                   "gbs": kbytes[k] / (kt[k][0] * 1e-3) / 1e9 if kt[k][0] else None}
                for k in ("append", "chunk_first", "seq_first")}
     step_bytes = sum(x.unique_bytes() for x in shapes)
-    # ---- pass D: the sequence-first phase on its own (two-kernel schedule,
-    # per-kernel events): north_star's ">= 70% of HBM roofline in the
-    # sequence-first phase"; its bytes = private K/V + q + o (+ the partial
-    # rows it merges, an overhead not counted)
-    wl.ca.set_option("dk", 0)
-    wl.ca.set_option("fused", 0)
-    wl.one_launch = False
+    # ---- pass C: end to end through the C ABI with host buffers (wall clock)
     wl.fill()
-    time_steps(wl, W, flush_buf, stream)  # warm the two-kernel schedule (module load, tensor maps, attributes)
+    time_e2e_wall(wl, min(W, K), stream)  # warm the host path
     wl.fill()
-    wl.ca.set_option("kernel_events", 1)
-    wl.ca.kernel_times()
-    time_steps(wl, K, flush_buf, stream)
-    ktd = wl.ca.kernel_times()
-    wl.ca.set_option("kernel_events", 0)
-    wl.ca.set_option("fused", 1)
-    wl.ca.set_option("dk", 1)
-    wl.one_launch = True
-    sf_ms, sf_n = ktd["seq_first"]
-    cf_ms, cf_n = ktd["chunk_first"]
-    sf_bytes = sum(x.seq_first_bytes() for x in shapes)
-    cf_bytes = sum(x.chunk_first_bytes() for x in shapes)
-    sf_gbs = sf_bytes / (sf_ms * 1e-3) / 1e9 if sf_ms > 0 else None
-    phase_split = {
-        "seq_first": {"achieved": sf_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": sf_gbs / hbm_peak if sf_gbs else None,
-                      "avg_launch_us": 1e3 * sf_ms / sf_n if sf_n else None, "alg_bytes_per_launch": sf_bytes / K},
-        "chunk_first": {"achieved": cf_bytes / (cf_ms * 1e-3) / 1e9 if cf_ms > 0 else None, "peak": hbm_peak,
-                        "unit": "GB/s", "avg_launch_us": 1e3 * cf_ms / cf_n if cf_n else None,
-                        "alg_bytes_per_launch": cf_bytes / K, "kernel": "cf_umma_kernel (tcgen05)"},
-        "schedule": "two-kernel (fused=0), per-kernel CUDA events on the launch stream, same steps 1..K"}
-    # ---- pass C: end to end through the C ABI with host buffers
-    wl.fill()
-    e2e_ms, h2d, d2h = time_e2e(wl, K, flush_buf, stream)
+    wall, hostcall, h2d, d2h = time_e2e_wall(wl, K, stream)
+    del wl
+    torch.cuda.empty_cache()
+    # ---- the north_star's own checks (seq-first HBM fraction, sweep vs B0, p = 512)
+    extras = {} if args.no_extras else extra_points(dev, flush_buf, stream, hbm_peak)
     clocks = sampler.stop()
-    e2e_total = sum(e2e_ms)
-    if world > 1:
-        t = torch.tensor([e2e_total], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_total = float(t.item())
-    value = world * wl.b * K / (total_ms * 1e-3)
+    value = args.batch * K / (total_ms * 1e-3)
     line = {
-        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1, "steps": K, "warmup": W,
         "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f16", "data": "synthetic",
-        "config": {"workload": f"cfg2_llama2_7b_b{wl.b}_s{wl.n_shared}" + ("" if args.mode == "chunk" else f"_{args.mode}"),
-                   "b_per_gpu": wl.b, "h": wl.h, "d": wl.d, "c": wl.c, "n_shared": wl.n_shared,
-                   "question": wl.question, "completion_tokens_timed": f"1..{K}", "mode": args.mode,
+        "config": {"workload": f"cfg2_llama2_7b_b{args.batch}_s{args.n_shared}" + ("" if args.mode == "chunk" else f"_{args.mode}"),
+                   "b": args.batch, "h": 32, "d": 128, "c": 64, "n_shared": args.n_shared,
+                   "question": args.question, "completion_tokens_timed": f"1..{K}", "mode": args.mode,
+                   "step": "chunkattn_append_attend (one K5 launch)" if fused else "append_kv + attend",
+                   "schedule": sched,
                    "l2": "flushed between timed steps (write a 2x-L2 buffer, then read it back so L2 holds clean "
                          "foreign lines; outside the events)",
-                   "parallelism": f"independent batch per GPU x{world}"},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                   "parallelism": "1 GPU"},
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
-                     "traffic_note": traffic_note,
-                     "peak_source": peak_src, "avg_launch_us": 1e3 * dom_ms / dom_n if dom_n else None},
+                     "traffic_note": traffic_note, "peak_source": peak_src,
+                     "avg_launch_us": 1e3 * dom_ms / dom_n if dom_n else None,
+                     "alg_bytes_per_launch": kbytes[dom] / dom_n if dom_n else None,
+                     "bytes_model": "every distinct K/V element once (the new row from the caller's k/v) + q + o "
+                                    "+ the new rows' pool writes (roofline.StepShape.fused_step_bytes)"},
         "kernels": kernels,
-        "phase_roofline": phase_split,
         "step_unique_bytes_avg": step_bytes / K,
         "step_gbs_vs_unique_bytes": step_bytes / (total_ms * 1e-3) / 1e9,
         "passB_ms_per_step": sum(ms_b) / K,
         "uploads_in_timed_region": uploads,
-        "e2e": {"value": world * wl.b * K / (e2e_total * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / K,
-                "transfer": "chunkattn_decode_step_host: packed pinned host [q|k_new|v_new] -> one H2D, append, "
-                            "attend, one D2H to pinned host, all inside the timed region"},
+        "e2e": {"value": args.batch * K / sum(wall), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * sum(wall) / K,
+                "host_us_per_step": 1e6 * statistics.median(hostcall),
+                "host_us_per_step_mean": 1e6 * sum(hostcall) / K,
+                "method": "wall clock (perf_counter) of back-to-back chunkattn_decode_step_host calls, each followed "
+                          "by a stream sync: packed pinned host [q|k_new|v_new] -> one H2D, the K5 step, one D2H "
+                          "to pinned host; no L2 flush. host_us = the call alone (tree a1 + context a2 + lazy "
+                          "upload a3 + launches, Python/ctypes included)"},
         "gpu_launches": launches,
         "clocks": clocks,
     }
-    if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(0, wl.n_shared, wl.question, wl.h, wl.d, args.cpu_budget, 4096)
+    line.update(extras)
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(0, args.n_shared, args.question, 32, 128, args.cpu_budget, 4096)
+    print(json.dumps(line), flush=True)
+
+
+def run_sharded(args):
+    """BASELINE.json configs[4] over the N ranks of one node: b = 256, shared
+    prompt 4096, 64-token questions; rank r holds heads [r h/N, (r+1) h/N) and
+    replays the full host op stream; each step = append_attend on the local
+    heads + one all_gather_into_tensor of the outputs (+ the head permutation)."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = args.dist_backend
+    if world > 1:
+        dist.init_process_group(backend)
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", local % ndev)
+    torch.cuda.set_device(dev)
+    K, W = args.steps, args.warmup
+    H, b = 32, args.batch_cfg5
+    if H % world:
+        raise SystemExit(f"{H} heads do not split over {world} ranks")
+    hl = H // world
+    hbm_peak, peak_src, _ = load_peaks()
+    sampler = ClockSampler(local % ndev) if rank == 0 else None
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush_buf = torch.empty(2 * l2 // 4 + 1024, dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(dev)
+    # every rank: the same host op stream (same seed), its heads' K/V only
+    wl = DecodeWorkload(dev, seed=0, steps=max(K, W), b=b, h=hl, n_shared=4096, question=64)
+    gbuf = torch.empty((world, b, hl, 128), dtype=torch.float16, device=dev)
+
+    def gather():
+        if world == 1:
+            return wl.out
+        if backend == "nccl":
+            dist.all_gather_into_tensor(gbuf, wl.out)
+        else:  # gloo (CPU-side test of the path): staged through the host
+            parts = [torch.empty((b, hl, 128), dtype=torch.float16) for _ in range(world)]
+            dist.all_gather(parts, wl.out.cpu())
+            gbuf.copy_(torch.stack(parts))
+        return gbuf.permute(1, 0, 2, 3).reshape(b, H, 128)
+
+    def steps_timed(n, with_gather):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        with torch.cuda.stream(stream):
+            for s in range(n):
+                flush_l2(flush_buf)
+                evs[s][0].record(stream)
+                wl.step(s, stream.cuda_stream)
+                if with_gather:
+                    gather()
+                evs[s][1].record(stream)
+        stream.synchronize()
+        return [a.elapsed_time(z) for a, z in evs]
+
+    wl.fill()
+    steps_timed(W, True)
+    wl.fill()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ms_g = steps_timed(K, True)
+    wl.fill()
+    ms_k = steps_timed(K, False)
+    tot = torch.tensor([sum(ms_g), sum(ms_k)], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    total_g, total_k = float(tot[0]), float(tot[1])
+    shapes = [wl.shape_at(s) for s in range(K)]
+    bytes_rank = sum(x.fused_step_bytes() for x in shapes) / K
+    sched = wl.ca.schedule_info()
+    clocks = sampler.stop() if sampler else None
     if rank == 0:
+        line = {
+            "metric": METRIC, "value": b * K / (total_g * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": total_g / K, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+            "config": {"workload": "cfg5_b256_s4096_q64_head_sharded", "b": b, "h": H, "heads_per_rank": hl,
+                       "d": 128, "c": 64, "n_shared": 4096, "question": 64, "completion_tokens_timed": f"1..{K}",
+                       "parallelism": f"heads split over {world} ranks (tp{world}); one {backend} "
+                                      f"all_gather_into_tensor of the outputs per step",
+                       "schedule_rank0": sched,
+                       "l2": "flushed between timed steps (outside the events)"},
+            "kernel_only_ms_per_step": total_k / K,
+            "gather_ms_per_step": (total_g - total_k) / K,
+            "roofline": {"bound": "hbm", "kernel": "dk_kernel (K5), per rank", "achieved":
+                         bytes_rank / (total_k / K * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": bytes_rank / (total_k / K * 1e-3) / 1e9 / hbm_peak, "traffic": None,
+                         "peak_source": peak_src, "alg_bytes_per_launch_per_rank": bytes_rank,
+                         "note": "event time of the whole step (launch included) per rank, max over ranks"},
+            "e2e": {"value": b * K / (total_g * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0, "note": "device-resident inputs on the sharded path"},
+            "gpu_launches": K,
+            "clocks": clocks,
+        }
         print(json.dumps(line), flush=True)
     if world > 1:
-        torch.distributed.destroy_process_group()
+        dist.destroy_process_group()
+
+
+def run_ours(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    workload = args.workload
+    if workload == "auto":
+        workload = "cfg5" if world > 1 else "cfg2"
+    if workload == "cfg5":
+        run_sharded(args)
+    else:
+        if world > 1:
+            raise SystemExit("cfg2 is a one-GPU workload; use --workload cfg5 (the sharded configs[4])")
+        run_cfg2(args)
 
 
 def main():
@@ -473,9 +647,15 @@ def main():
     ap.add_argument("--n-shared", dest="n_shared", type=int, default=2048)
     ap.add_argument("--question", type=int, default=0)
     ap.add_argument("--batch", type=int, default=32)
-    ap.add_argument("--cpu-budget", dest="cpu_budget", type=float, default=10.0)
+    ap.add_argument("--cpu-budget", dest="cpu_budget", type=float, default=16.0)
     ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
     ap.add_argument("--opt", action="append", default=[], help="library option key=value (A/B experiments)")
+    ap.add_argument("--workload", default="auto", choices=["auto", "cfg2", "cfg5"],
+                    help="auto: cfg2 on one GPU (the metric's config), the head-sharded cfg5 under torchrun")
+    ap.add_argument("--batch-cfg5", dest="batch_cfg5", type=int, default=256)
+    ap.add_argument("--dist-backend", dest="dist_backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--no-extras", dest="no_extras", action="store_true",
+                    help="skip the seq-first / sweep / p512 points")
     args = ap.parse_args()
     if os.environ.get("CA_BENCH_WATCHDOG"):  # debugging: dump the Python stacks if a pass stalls
         import faulthandler

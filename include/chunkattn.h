@@ -167,10 +167,10 @@ chunkattn_status chunkattn_attend(chunkattn_t h, int32_t layer, int64_t n, const
  *   tokens   host int32[n] (layer 0), the new token of seq_ids[k]
  *   k, v     device [n][h][d] dtype: THIS layer's new K/V rows, seq_ids order
  *   q        device [n][h][d] dtype;  out  device [n][h][d] out_dtype
- * The K/V scatter happens inside the attention kernel (the cluster decode
- * kernel K5): 16-bit dtype, d in {64, 128}, c in {16, 32, 48,
- * 64, 96, 128}.  Other shapes run append_kv + attend (num_layers == 1 only,
- * CA_EDTYPE otherwise).  Errors before the launch leave the state unchanged.
+ * On the K5 schedule (16-bit dtype, d in {64, 128}, c in {16, 32, 48, 64,
+ * 96, 128}) the K/V scatter happens inside the attention
+ * kernel; otherwise this call launches K1 for this layer and the persistent
+ * attention kernels.  Errors before the launch leave the state unchanged.
  * Asynchronous on `stream`. */
 chunkattn_status chunkattn_append_attend(chunkattn_t h, int32_t layer, int64_t n, const int64_t* seq_ids,
                                          const int32_t* tokens, const void* k, const void* v, const void* q,
@@ -234,9 +234,11 @@ chunkattn_status chunkattn_schedule_info(chunkattn_t h, int64_t out[8]);
 /* Tuning / test knobs (scheduling only; any setting gives the same result
  * within rounding, and a fixed setting is bitwise reproducible).  Unknown keys
  * fail with CA_EINVAL.
- *   "dk"               1 (default) = the cluster decode kernel K5 (one launch:
- *                      append + both phases + the cluster merge) when the shape
- *                      allows; 0 = the persistent-kernel paths below
+ *   "dk"               1 (default, auto) = the cluster decode kernel K5 (one
+ *                      launch: append + both phases + the cluster merge) when
+ *                      the shape allows and no shared run spans more rows than
+ *                      one K5 row block; 2 = K5 whenever the shape allows; 0 =
+ *                      the persistent-kernel paths below
  *   "dk_cs"            0 = auto (largest cluster with all (row block, head)
  *                      groups co-resident), else force the cluster size 1..16
  *   "dk_max_rows"      rows per K5 row block, 16..64 (default 64)

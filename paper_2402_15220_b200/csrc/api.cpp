@@ -132,7 +132,7 @@ struct chunkattn {
   bool use_pdl = true;
   int num_sms = 148;
   int64_t cf_cpt_forced = 0;
-  bool dk_opt = true;         // K5 cluster decode kernel when the shape allows (option "dk")
+  int dk_opt = 1;             // K5 cluster decode: 0 off, 1 auto (the schedule decides), 2 whenever supported
   int len_parity = 0;         // K5: which of the two device length buffers is current
   int64_t sf_ctas_req = 296;  // requested persistent grid (option sf_ctas / sf_ctas_per_sm)
   int resident_cache = -1;    // occupancy x SMs of the persistent kernel (per residency setting)
@@ -334,7 +334,8 @@ struct chunkattn {
     // persistent grid: at most one wave (the cross-CTA merges spin on other
     // CTAs' contributions, which must be resident)
     sopt.sf_ctas = std::max<int64_t>(1, std::min<int64_t>(sf_ctas_req, resident_sf_ctas()));
-    sopt.dk = dk_opt && dk_supported(geom());
+    sopt.dk = dk_opt != 0 && dk_supported(geom());
+    sopt.dk_force = dk_opt == 2;
     Context nc;
     std::string err;
     if (!build_context(tree, sopt, &nc, &err)) return fail(CA_ENOMEM, err);
@@ -702,14 +703,6 @@ chunkattn_status chunkattn_append_attend(chunkattn_t h, int32_t layer, int64_t n
   if (n == 0) return CA_OK;
   if (!k || !v || !q || !out) return fail(CA_EINVAL, "null k/v/q/out");
   if (layer == 0 && !tokens) return fail(CA_EINVAL, "null tokens");
-  const bool dk = h->dk_opt && dk_supported(h->geom());
-  if (!dk) {  // no K5 for this shape: the two-call path (one layer only)
-    if (h->cfg.num_layers != 1)
-      return fail(CA_EDTYPE, "append_attend with num_layers > 1 needs the cluster decode kernel (16-bit, d 64/128)");
-    chunkattn_status s = chunkattn_append_kv(h, n, seq_ids, tokens, k, v, stream);
-    if (s != CA_OK) return s;
-    return chunkattn_attend(h, layer, n, seq_ids, q, out, stream);
-  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (h->set_device() != CA_OK) return CA_ECUDA;
   if (layer == 0) {  // the tree grows once per step
@@ -730,12 +723,42 @@ chunkattn_status chunkattn_append_attend(chunkattn_t h, int32_t layer, int64_t n
   if (s != CA_OK) return s;
   const AttnLaunch a = h->attn_launch(layer, q, out);
   const DevTables t = h->dev_tables();
-  const DkAppend ap{k, v, h->other_len(), layer == 0 ? 3 : 1};
-  cudaError_t e = h->timed_launch(chunkattn::K_SF, st, [&] { return launch_decode(a, t, ap, st); });
-  if (e != cudaSuccess) return h->cuda_fail(e, "decode");
-  ++h->n_launches;
+  cudaError_t e = cudaSuccess;
+  if (h->ctx.dk) {  // one K5 launch: the scatter of this layer's K/V rows inside the attention kernel
+    const DkAppend ap{k, v, h->other_len(), layer == 0 ? 3 : 1};
+    e = h->timed_launch(chunkattn::K_SF, st, [&] { return launch_decode(a, t, ap, st); });
+    if (e != cudaSuccess) return h->cuda_fail(e, "decode");
+    ++h->n_launches;
+  } else {
+    // the schedule took the persistent kernels (shape without K5, or runs
+    // wider than a K5 row block): K1 for this layer, then the attend launches
+    h->append_items.resize(n);
+    for (int64_t i = 0; i < n; ++i) {
+      const Sequence* sq = h->tree.find(seq_ids[i]);
+      const int32_t chunk = sq->path.back();
+      const int64_t pre = layer == 0 ? sq->len : sq->len - 1;  // the tree advanced at layer 0
+      h->append_items[i] = AppendItem{h->ctx.row_of.at(seq_ids[i]), chunk,
+                                      (int32_t)(pre - h->tree.node(chunk).start_pos), (int32_t)(pre + 1)};
+    }
+    PoolGeom g = h->pool;  // this layer's slice, [n][h][d] sources
+    g.k = static_cast<char*>(g.k) + (size_t)layer * g.layer_stride * dtype_bytes(g.dtype);
+    g.v = static_cast<char*>(g.v) + (size_t)layer * g.layer_stride * dtype_bytes(g.dtype);
+    g.num_layers = 1;
+    e = h->timed_launch(chunkattn::K_APPEND, st,
+                        [&] { return launch_append_kv(g, t, h->append_items.data(), (int32_t)n, k, v, st); });
+    if (e != cudaSuccess) return h->cuda_fail(e, "append_kv");
+    h->n_launches += (n + kMaxAppendItems - 1) / kMaxAppendItems;
+    if (t.n_cf_tiles > 0 && !t.fused) {
+      e = h->timed_launch(chunkattn::K_CF, st, [&] { return launch_chunk_first(a, t, st); });
+      if (e != cudaSuccess) return h->cuda_fail(e, "chunk_first");
+      ++h->n_launches;
+    }
+    e = h->timed_launch(chunkattn::K_SF, st, [&] { return launch_seq_first(a, t, st); });
+    if (e != cudaSuccess) return h->cuda_fail(e, "seq_first");
+    ++h->n_launches;
+  }
   if (layer == 0) {
-    h->len_parity ^= 1;  // the kernel wrote the advanced lengths to the other buffer
+    if (h->ctx.dk) h->len_parity ^= 1;  // K5 wrote the advanced lengths to the other buffer
     h->tree.append_tokens(seq_ids, tokens, n);
   }
   return CA_OK;
@@ -765,7 +788,7 @@ chunkattn_status chunkattn_decode_step_host(chunkattn_t h, int32_t layer, int64_
   cudaError_t e = cudaMemcpyAsync(dev, in_host, in_bytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return h->cuda_fail(e, "decode_step_host H2D");
   chunkattn_status s;
-  if (h->cfg.num_layers == 1 && h->dk_opt && dk_supported(h->geom())) {  // one launch: append + attend
+  if (h->cfg.num_layers == 1) {  // append + attend in one call (one launch on the K5 schedule)
     s = chunkattn_append_attend(h, layer, n, seq_ids, tokens, dev + q_bytes, dev + q_bytes + kv_bytes, dev,
                                 dev + out_off, stream);
     if (s != CA_OK) return s;
@@ -871,7 +894,7 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
   } else if (k == "sf_item_cost") {
     h->sopt.sf_item_cost = value < 0 ? 0.0 : (double)value / 10.0;  // tenths of a unit
   } else if (k == "dk") {
-    h->dk_opt = value != 0;
+    h->dk_opt = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2));
   } else if (k == "dk_cs") {
     h->sopt.dk_cs_forced = (int32_t)std::max<int64_t>(0, std::min<int64_t>(value, kDkMaxCluster));
   } else if (k == "dk_max_rows") {

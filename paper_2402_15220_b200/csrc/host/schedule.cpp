@@ -98,7 +98,12 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
   // equal cost; the rows' last chunks are dealt in packs to the least-loaded
   // ranks.  Units carry the head of the set in the flags word (bits 8+).
   std::vector<int32_t> dk_block, dk_cta, dk_unit;
-  X.dk = opt.dk && b > 0;
+  // K5 takes the step unless a shared run spans more rows than one block
+  // holds: there the persistent kernels (tcgen05 chunk-first over up to 128
+  // rows per tile) read each shared chunk once instead of once per block
+  int32_t max_run_rows = 0;
+  for (const Run& r : runs) max_run_rows = std::max(max_run_rows, r.j - r.i + 1);
+  X.dk = opt.dk && b > 0 && (opt.dk_force || max_run_rows <= std::min(opt.dk_max_rows, kDkMaxRows));
   if (X.dk) {
     const int32_t H = opt.num_heads;
     int32_t hg = 1, cs = 1, nblk = 1;

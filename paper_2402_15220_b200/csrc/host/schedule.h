@@ -82,6 +82,7 @@ struct ScheduleOptions {
   int64_t seg_capacity = 0;        // seq-first segment partial rows available
   // K5 cluster decode
   bool dk = false;
+  bool dk_force = false;  // K5 even when a shared run spans several row blocks
   int32_t dk_max_rows = kDkMaxRows;
   int32_t dk_cs_forced = 0;                        // > 0: cluster size to use
   int32_t dk_max_clusters[kDkMaxCluster + 1] = {};  // co-resident clusters of each size (0: unsupported)

@@ -59,6 +59,12 @@ class StepShape:
         return ((self.shared_chunks * self.c + self.private_tokens) * self.token_kv_bytes
                 + self.b * self.h * self.d * (self.elem + self.out_elem))
 
+    def fused_step_bytes(self) -> int:
+        """The one-launch step (append + attend, K5): every distinct K/V element
+        read once (the new token's row read from the caller's k / v) + q + o,
+        plus the new rows written into the pool."""
+        return self.unique_bytes() + self.b * self.token_kv_bytes
+
     def chunk_first_flops(self) -> int:
         return 4 * self.h * self.d * self.shared_rows * self.c
 

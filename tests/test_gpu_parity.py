@@ -438,7 +438,7 @@ def test_tcgen05_chunk_first_wide_runs(d, c, dt, odt):
     hs.step = 1
     hs.append(ids, decode_tokens(hs, ids))
     hs.check(ids, TOL[(dt, odt)])
-    for opts in ("dk=0,cf_umma=0", ""):  # the mma.sync chunk-first, then K5 (three row blocks), same tree
+    for opts in ("dk=0,cf_umma=0", "dk=2"):  # the mma.sync chunk-first, then K5 forced (three row blocks), same tree
         hs2 = Harness(2, d, c, dt, odt, seed=11, alpha=8.0, max_chunks=1024, opts=opts)
         for i in range(130):
             pre = sys_p + (grp if i < 70 else [])
@@ -461,12 +461,12 @@ def test_config2_full_size_last_timed_step(opts):
     hs.check(ids, 2e-3, rows=list(range(0, 32, 3)))
 
 
-@pytest.mark.parametrize("opts", ["", "dk=0"])
+@pytest.mark.parametrize("opts", ["", "dk=2"])
 def test_config5_full_size_sampled_rows(opts):
     """BASELINE configs[4] on one GPU: b = 256, shared prompt 4096, 64-token
-    private question + the decode token (K5: four 64-row blocks; dk=0: the
-    two-kernel schedule, tcgen05 chunk-first): sampled rows against the fp64
-    oracle."""
+    private question + the decode token (auto: the 256-row run takes the
+    two-kernel schedule with the tcgen05 chunk-first; dk=2: K5 forced, four
+    64-row blocks): sampled rows against the fp64 oracle."""
     hs = Harness(32, 128, 64, "f16", "f16", seed=2, alpha=8.0, max_chunks=64 + 256 * 2 + 16, opts=opts)
     ids = build_shared(hs, 4096, [64] * 256)
     hs.step = 1
