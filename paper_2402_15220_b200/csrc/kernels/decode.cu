@@ -70,7 +70,10 @@ struct DkMeta {
   int prow[kNC], pnt[kNC], poff[kNC], phh[kNC], pchunk[kNC];
 };
 
-CA_DEV void dk_sync_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(kNC * 32) : "memory"); }
+CA_DEV void dk_sync_consumers() {  // bar.sync is .aligned: arrive converged
+  __syncwarp();
+  asm volatile("bar.sync 1, %0;" ::"n"(kNC * 32) : "memory");
+}
 template <int N>
 CA_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
 template <int N>

@@ -121,7 +121,11 @@ struct StageMeta {
   int mg0, mg1, seg, nsegs;
 };
 
-CA_DEV void named_sync_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory"); }
+// barrier.sync (not the .aligned bar.sync): lanes of a warp may arrive on
+// different paths (compute-sanitizer synccheck flagged bar.sync here).
+CA_DEV void named_sync_consumers() {
+  asm volatile("barrier.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+}
 
 CA_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -451,7 +455,9 @@ CA_DEV void sf_finalize(SfShared<D, NG>& S, const StageMeta& md, const float* ps
 // waits and every CTA counts its own contributions before it waits; the grid
 // is one wave (2 CTAs per SM).
 constexpr int kMergeWarps = kProducerWarps + kConsumerWarps;
-CA_DEV void named_sync_all() { asm volatile("bar.sync 2, %0;" ::"n"(kMergeWarps * 32) : "memory"); }
+CA_DEV void named_sync_all() {  // non-.aligned barrier: lanes may arrive from different paths
+  asm volatile("barrier.sync 2, %0;" ::"n"(kMergeWarps * 32) : "memory");
+}
 
 template <typename TO, int D, int NG>
 CA_DEV void merge_pending(SfShared<D, NG>& S, const float* __restrict__ pO, const float* __restrict__ segO,

@@ -1,0 +1,28 @@
+"""Small decode workloads for compute-sanitizer (memcheck / racecheck /
+synccheck): the tiny config (configs[0], fp16) and one cfg2 step, on the K5
+one-launch path and on the persistent kernels (dk=0: fused and two-kernel),
+each checked against the fp64 oracle so a silent corruption also fails.
+
+    compute-sanitizer --tool memcheck python tools/sanitize_run.py [--cfg2]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from tests.gpu_workload import Harness, build_shared, decode_tokens  # noqa: E402
+
+variants = ["", "dk=0", "dk=0,fused=0"]
+for opts in variants:
+    hs = Harness(8, 64, 16, "f16", "f16", seed=1, alpha=8.0, opts=opts)
+    ids = build_shared(hs, 64, [0, 1, 16, 32])
+    hs.check(ids, 2e-3)
+    for st in range(1, 3):
+        hs.step = st
+        hs.append_attend(ids, decode_tokens(hs, ids), 2e-3)
+    print("tiny ok", opts or "K5", flush=True)
+if "--cfg2" in sys.argv:
+    for opts in variants:
+        hs = Harness(32, 128, 64, "f16", "f16", seed=3, alpha=8.0, max_chunks=512, opts=opts)
+        ids = build_shared(hs, 2048, [0] * 32)
+        hs.step = 1
+        hs.append_attend(ids, decode_tokens(hs, ids), 2e-3, rows=[0, 31])
+        print("cfg2 ok", opts or "K5", flush=True)
