@@ -85,6 +85,13 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def snapshot(self):
+        """Clock statistics of the samples so far (the sampler keeps running)."""
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        self.f.flush()
+        return self._summary()
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
@@ -92,6 +99,11 @@ class ClockSampler:
         self.proc.terminate()
         self.proc.wait()
         self.f.close()
+        res = self._summary()
+        os.unlink(self.path)
+        return res
+
+    def _summary(self):
         sm, mx, reasons = [], None, set()
         names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
         with open(self.path) as f:
@@ -109,7 +121,6 @@ class ClockSampler:
                 for nm, v in zip(names, parts[3:7]):
                     if v.lower() == "active":
                         reasons.add(nm)
-        os.unlink(self.path)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
 

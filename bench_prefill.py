@@ -31,6 +31,8 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
+_CLOCKS = None
+
 import synth  # noqa: E402
 from bench import flush_l2  # noqa: E402
 
@@ -89,6 +91,9 @@ def run(mode, b, n_s, q_len, h=32, d=128, c=64, iters=20, seed=0):
 
 
 def main():
+    global _CLOCKS
+    from bench import ClockSampler
+    _CLOCKS = ClockSampler(0)
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--n-shared", dest="n_shared", type=int, default=2048)
@@ -97,6 +102,7 @@ def main():
     rows = [run(m, args.batch, args.n_shared, args.q_len) for m in ("lookup", "no_lookup")]
     rows[0]["speedup_vs_no_lookup"] = rows[1]["us_median"] / rows[0]["us_median"]
     for r in rows:
+        r["clocks"] = _CLOCKS.snapshot()
         print(json.dumps(r), flush=True)
 
 

@@ -29,6 +29,8 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
+_CLOCKS = None
+
 
 def run_mode(trace, prefix_match, b_max, n_p, n_c, h=32, d=128, c=64):
     from paper_2402_15220_b200 import ChunkAttention
@@ -45,6 +47,9 @@ def run_mode(trace, prefix_match, b_max, n_p, n_c, h=32, d=128, c=64):
 
 
 def main():
+    global _CLOCKS
+    from bench import ClockSampler
+    _CLOCKS = ClockSampler(0)
     ap = argparse.ArgumentParser()
     ap.add_argument("--requests", type=int, default=64)
     ap.add_argument("--rps", type=float, default=2000.0, help="Poisson arrival rate (requests / s of attention time)")
@@ -76,6 +81,7 @@ def main():
                 line["kv_bytes_ratio_vs_monolithic"] = m.peak_kv_bytes / max(1, mono.peak_kv_bytes)
                 line["latency_ratio_vs_monolithic"] = m.normalized_latency_ms_per_tok / max(
                     1e-12, mono.normalized_latency_ms_per_tok)
+            line["clocks"] = _CLOCKS.snapshot()
             print(json.dumps(line), flush=True)
 
 

@@ -28,6 +28,8 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
+_CLOCKS = None
+
 from bench import DecodeWorkload, flush_l2, load_peaks  # noqa: E402
 
 
@@ -69,6 +71,9 @@ def run_point(dev, b, n_p, n_s, mode, iters, flush, stream, c=64, opts=()):
 
 
 def main():
+    global _CLOCKS
+    from bench import ClockSampler
+    _CLOCKS = ClockSampler(0)
     ap = argparse.ArgumentParser()
     ap.add_argument("--points", default="all", choices=["tab", "cfg3", "cfg5", "all"])
     ap.add_argument("--iters", type=int, default=30)
@@ -102,6 +107,7 @@ def main():
         for mode, r in res.items():
             r["speedup_vs_b0"] = res["b0"]["us_median"] / r["us_median"]
             r["frac_hbm"] = r["gbs_alg"] / peak
+            r["clocks"] = _CLOCKS.snapshot()
             print(json.dumps(r), flush=True)
             rows.append(r)
     lines = ["| b | n_p | n_s | ChunkAttn µs | B1 (shared, no TPP) µs | B0 (non-shared paged) µs | speedup vs B0 | "

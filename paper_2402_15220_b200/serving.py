@@ -6,7 +6,7 @@ KV-cache bytes; PAPER.md:511 the 1/(1 - r) capacity argument).
 There are no model weights here: an iteration runs exactly the attention work
 of the method -- prefill attention with prefix lookup for the requests that
 join (chunkattn_add_sequence + chunkattn_prefill_attend) and one decode step
-for the running batch (chunkattn_append_kv + chunkattn_attend) -- on seeded
+for the running batch (chunkattn_append_attend: one launch) -- on seeded
 synthetic K/V/Q (synth/).  The clock advances by each iteration's device time
 (CUDA events around the iteration's launches), so latencies are attention-only;
 on a host-only handle (no GPU) it advances by a fixed cost per iteration.  The
@@ -78,7 +78,10 @@ class ServingLoop:
         p = torch.as_tensor(pos, dtype=torch.int64, device=dev)
         return synth.kv_values(self.seed, which, t, p, self.ca.L, self.ca.h, self.ca.d, device=dev).to(self.ca.dtype)
 
-    def run(self, trace: list[Request], mode: str) -> RunMetrics:
+    def run(self, trace: list[Request], mode: str, observer=None) -> RunMetrics:
+        """observer (tests): called after every iteration with a dict of that
+        iteration's prefill (ids, first positions, q, out) and decode (ids,
+        tokens appended, q, out) and the token lists of the running sequences."""
         ca, gpu = self.ca, self.gpu
         pending = sorted(trace, key=lambda r: r.arrival_s)
         running: dict[int, dict] = {}   # seq id -> {req, tokens, generated}
@@ -138,10 +141,16 @@ class ServingLoop:
                 if gpu:
                     qs.append(p_[5][got:])
             sid_counter += len(plan)
+            pf_out = pf_q = None
             if gpu and ids and sum(q.shape[0] for q in qs) > 0:
-                ca.prefill_attend(ids, firsts, torch.cat(qs).contiguous())
-            ca.append_kv(dec_sids, toks, kd, vd)
-            ca.attend(dec_sids, qd)
+                pf_q = torch.cat(qs).contiguous()
+                pf_out = ca.prefill_attend(ids, firsts, pf_q)
+            if gpu:  # one decode step: append + attend in one call (one K5 launch)
+                dec_out = ca.append_attend(dec_sids, toks, kd[:, 0].contiguous(), vd[:, 0].contiguous(), qd)
+            else:
+                ca.append_kv(dec_sids, toks, kd, vd)
+                ca.attend(dec_sids, qd)
+                dec_out = None
             if gpu:
                 ev1.record(stream)
                 ev1.synchronize()
@@ -156,6 +165,10 @@ class ServingLoop:
             for s, t in zip(dec_sids, toks):
                 running[s]["tokens"].append(t)
                 running[s]["generated"] += 1
+            if observer is not None:
+                observer({"iteration": iters, "prefill_ids": ids, "prefill_first": firsts, "prefill_q": pf_q,
+                          "prefill_out": pf_out, "decode_ids": list(dec_sids), "decode_q": qd, "decode_out": dec_out,
+                          "tokens": {s: list(running[s]["tokens"]) for s in dec_sids}})
             for s in dec_sids:
                 if running[s]["generated"] >= running[s]["req"].n_c:
                     r = running.pop(s)["req"]
