@@ -26,7 +26,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 HOST_SRC = ["api.cpp", "host/tree.cpp", "host/schedule.cpp"]
 CUDA_SRC = ["kernels/append.cu", "kernels/seq_first.cu", "kernels/chunk_first.cu", "kernels/chunk_first_umma.cu", "kernels/prefill.cu", "kernels/decode.cu"]
-HEADERS = ["kernels/common.cuh", "kernels/kernels.h", "kernels/mma_attn.cuh", "host/tree.h", "host/schedule.h"]
+HEADERS = ["kernels/common.cuh", "kernels/kernels.h", "kernels/mma_attn.cuh", "kernels/umma.cuh", "host/tree.h", "host/schedule.h"]
 
 
 def _newest_dep():

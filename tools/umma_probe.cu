@@ -25,7 +25,12 @@
     }                                                                           \
   } while (0)
 
-constexpr int C = 64, D = 128, M = 128;
+#ifndef PROBE_M
+#define PROBE_M 128
+#endif
+// M = 64 (-DPROBE_M=64): the accumulator's TMEM lane of every row is found by
+// matching each lane's S row against the CPU rows (printed as a lane map)
+constexpr int C = 64, D = 128, M = PROBE_M;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -133,7 +138,7 @@ __global__ void probe(const __half* q, const __half* kt, const __half* vt, const
   }
   mbar_wait(&bar, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int row = warp * 32 + (tid & 31);
+  const int row = warp * 32 + (tid & 31);  // TMEM lane (all 128)
   const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
   float v[32];
   for (int c0 = 0; c0 < C; c0 += 32) {
@@ -172,8 +177,8 @@ int main() {
   CK(cudaMalloc(&dk, 2 * C * D));
   CK(cudaMalloc(&dv, 2 * C * D));
   CK(cudaMalloc(&dp, 2 * M * C));
-  CK(cudaMalloc(&ds, 4 * M * C));
-  CK(cudaMalloc(&dout, 4 * M * D));
+  CK(cudaMalloc(&ds, 4 * 128 * C));
+  CK(cudaMalloc(&dout, 4 * 128 * D));
   CK(cudaMemcpy(dq, q.data(), 2 * M * D, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dk, kp.data(), 2 * C * D, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dv, vp.data(), 2 * C * D, cudaMemcpyHostToDevice));
@@ -182,21 +187,39 @@ int main() {
   CK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   probe<<<1, 128, smem>>>(dq, dk, dv, dp, ds, dout);
   CK(cudaDeviceSynchronize());
-  std::vector<float> s(M * C), o(M * D);
-  CK(cudaMemcpy(s.data(), ds, 4 * M * C, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(o.data(), dout, 4 * M * D, cudaMemcpyDeviceToHost));
+  std::vector<float> s(128 * C), o(128 * D);
+  CK(cudaMemcpy(s.data(), ds, 4 * 128 * C, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(o.data(), dout, 4 * 128 * D, cudaMemcpyDeviceToHost));
+  std::vector<int> lane_of(M, -1);
+  if (M != 128) {  // find each row's lane
+    for (int r = 0; r < M; ++r)
+      for (int L = 0; L < 128 && lane_of[r] < 0; ++L) {
+        double e = 0;
+        for (int t = 0; t < C; ++t) {
+          double a = 0;
+          for (int k = 0; k < D; ++k) a += (double)qf[r * D + k] * kf[t * D + k];
+          e = fmax(e, fabs(a - s[L * C + t]));
+        }
+        if (e < 1e-2) lane_of[r] = L;
+      }
+    printf("M=%d row -> TMEM lane:", M);
+    for (int r = 0; r < M; ++r) printf(" %d:%d", r, lane_of[r]);
+    printf("\n");
+  } else {
+    for (int r = 0; r < M; ++r) lane_of[r] = r;
+  }
   double es = 0, eo = 0;
   for (int r = 0; r < M; ++r)
     for (int t = 0; t < C; ++t) {
       double a = 0;
       for (int e = 0; e < D; ++e) a += (double)qf[r * D + e] * kf[t * D + e];
-      es = fmax(es, fabs(a - s[r * C + t]));
+      es = fmax(es, lane_of[r] < 0 ? 1e9 : fabs(a - s[lane_of[r] * C + t]));
     }
   for (int r = 0; r < M; ++r)
     for (int e = 0; e < D; ++e) {
       double a = 0;
       for (int t = 0; t < C; ++t) a += (double)pf[r * C + t] * vf[t * D + e];
-      eo = fmax(eo, fabs(a - o[r * D + e]));
+      eo = fmax(eo, lane_of[r] < 0 ? 1e9 : fabs(a - o[lane_of[r] * D + e]));
     }
   printf("S = Q K^T  max abs err %.3e  (S[0][0] %f S[5][7] %f)\n", es, s[0], s[5 * C + 7]);
   printf("O = P V    max abs err %.3e  (O[0][0] %f O[9][100] %f)\n", eo, o[0], o[9 * D + 100]);
