@@ -228,8 +228,9 @@ chunkattn_status chunkattn_counters(chunkattn_t h, int64_t out[6]);
 /* Schedule of the current context (built by the last append / attend):
  * out[8] = {K5 cluster decode in use (0/1), K5 cluster size, K5 groups
  * (row blocks x head sets), K5 row blocks, K5 work units, K5 heads per
- * group, persistent fused schedule (0/1), persistent grid CTAs}. */
-chunkattn_status chunkattn_schedule_info(chunkattn_t h, int64_t out[8]);
+ * group, persistent fused schedule (0/1), persistent grid CTAs, K5 runs its
+ * chunk-first units on tcgen05 (0/1)}. */
+chunkattn_status chunkattn_schedule_info(chunkattn_t h, int64_t out[9]);
 
 /* Tuning / test knobs (scheduling only; any setting gives the same result
  * within rounding, and a fixed setting is bitwise reproducible).  Unknown keys
@@ -245,6 +246,14 @@ chunkattn_status chunkattn_schedule_info(chunkattn_t h, int64_t out[8]);
  *   "dk_hg"            0 = auto, else heads per K5 cluster group
  *   "dk_shared_fixed", "dk_shared_row", "dk_pack_fixed"  K5 work-split unit
  *                      costs (hundredths / thousandths; defaults 100, 10, 15)
+ *   "dk_slots"         K5 tcgen05 variant: cap on its K + V ring slots (>= 4;
+ *                      0 = default = as many as fit in shared memory)
+ *   "dk_umma"          K5's chunk-first units on the tcgen05 tensor cores
+ *                      (16-bit, d in {64, 128}, c = 64; S and O in TMEM, K/V
+ *                      by 2-D TMA): 1 (default) when the step's chunk-first
+ *                      units are at least "dk_umma_ratio" (hundredths, default
+ *                      50) x its full private chunks, 2 always, 0 never (the
+ *                      mma.sync consumers run them)
  *   "fused"            1 (default) = both phases in one persistent launch
  *                      (chunk-first units first in each CTA, last-contributor
  *                      merges); 0 = chunk-first kernel + seq-first kernel

@@ -246,9 +246,10 @@ class ChunkAttention:
         return dict(zip(["builds", "uploads", "upload_bytes", "launches", "epoch", "slots"], list(a)))
 
     def schedule_info(self) -> dict:
-        a = (ctypes.c_int64 * 8)()
+        a = (ctypes.c_int64 * 9)()
         C.check(self.lib.chunkattn_schedule_info(self._h, a))
-        return dict(zip(["dk", "dk_cs", "dk_groups", "dk_blocks", "dk_units", "dk_hg", "fused", "sf_ctas"], list(a)))
+        return dict(zip(["dk", "dk_cs", "dk_groups", "dk_blocks", "dk_units", "dk_hg", "fused", "sf_ctas", "dk_um"],
+                        list(a)))
 
     def set_option(self, key: str, value: int) -> None:
         C.check(self.lib.chunkattn_set_option(self._h, key.encode(), int(value)))

@@ -128,6 +128,7 @@ struct chunkattn {
   int trace_kernel = 0;    // 1: trace seq-first, 2: trace chunk-first
   int sf_ctas_per_sm = 2;  // persistent seq-first residency (smem budget per CTA)
   int sf_prefetch = 0;     // seq-first L2 prefetch distance (units); measured slower on B200
+  int dk_slots = 0;        // K5 tcgen05 variant: cap on K + V ring slots (0 = as many as fit)
   int diag_nocompute = 0;  // DIAGNOSTIC ONLY (wrong outputs): seq-first consumers skip the math
   bool use_pdl = true;
   int num_sms = 148;
@@ -288,6 +289,7 @@ struct chunkattn {
     a.trace_cf = trace_kernel == 2;
     a.sf_ctas_per_sm = sf_ctas_per_sm;
     a.sf_prefetch = sf_prefetch | (diag_nocompute ? 256 : 0);
+    a.dk_slots = dk_slots;
     a.use_pdl = use_pdl && !kernel_events;
     return a;
   }
@@ -336,9 +338,12 @@ struct chunkattn {
     sopt.sf_ctas = std::max<int64_t>(1, std::min<int64_t>(sf_ctas_req, resident_sf_ctas()));
     sopt.dk = dk_opt != 0 && dk_supported(geom());
     sopt.dk_force = dk_opt == 2;
+    sopt.dk_umma_ok = sopt.dk && dk_umma_supported(geom());
     Context nc;
     std::string err;
     if (!build_context(tree, sopt, &nc, &err)) return fail(CA_ENOMEM, err);
+    // the tcgen05 variant only where its shared-memory layout fits this schedule
+    if (nc.dk && nc.dk_um) nc.dk_um = dk_um_fits(geom(), nc.dk_hg * nc.dk_max_rows, nc.dk_cs);
     ctx = std::move(nc);
     ++n_builds;
     if (!host_only) {
@@ -364,6 +369,7 @@ struct chunkattn {
     t.dk_max_rows = ctx.dk_max_rows;
     t.dk_blocks = ctx.dk_blocks;
     t.dk_hg = ctx.dk_hg;
+    t.dk_um = ctx.dk_um ? 1 : 0;
     t.sf_first = base + L.sf_first;
     t.last_chunk = base + L.last_chunk;
     t.last_start = base + L.last_start;
@@ -854,7 +860,7 @@ chunkattn_status chunkattn_counters(chunkattn_t h, int64_t out[6]) {
   return CA_OK;
 }
 
-chunkattn_status chunkattn_schedule_info(chunkattn_t h, int64_t out[8]) {
+chunkattn_status chunkattn_schedule_info(chunkattn_t h, int64_t out[9]) {
   if (!h || !out) return fail(CA_EINVAL, "bad argument");
   out[0] = h->ctx.dk ? 1 : 0;
   out[1] = h->ctx.dk_cs;
@@ -864,6 +870,7 @@ chunkattn_status chunkattn_schedule_info(chunkattn_t h, int64_t out[8]) {
   out[5] = h->ctx.dk_hg;
   out[6] = h->ctx.fused ? 1 : 0;
   out[7] = h->ctx.n_sf_ctas;
+  out[8] = h->ctx.dk && h->ctx.dk_um ? 1 : 0;
   return CA_OK;
 }
 
@@ -905,6 +912,10 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->sopt.dk_shared_row = std::max<int64_t>(0, value) / 1000.0;
   } else if (k == "dk_hg") {
     h->sopt.dk_hg_forced = (int32_t)std::max<int64_t>(0, value);
+  } else if (k == "dk_umma") {
+    h->sopt.dk_umma = (int32_t)std::max<int64_t>(0, std::min<int64_t>(value, 2));
+  } else if (k == "dk_umma_ratio") {  // hundredths
+    h->sopt.dk_umma_ratio = std::max<int64_t>(0, value) / 100.0;
   } else if (k == "dk_pack_fixed") {  // hundredths
     h->sopt.dk_pack_fixed = std::min<int64_t>(100, std::max<int64_t>(0, value)) / 100.0;
   } else if (k == "cf_umma") {
@@ -913,6 +924,9 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     h->cf_small = value != 0;
   } else if (k == "diag_nocompute") {
     h->diag_nocompute = value != 0;
+  } else if (k == "dk_slots") {
+    h->dk_slots = (int)std::max<int64_t>(0, std::min<int64_t>(value, 127));  // +64: 2-D TMA at d = 64 too (A/B)
+    return CA_OK;
   } else if (k == "sf_prefetch") {
     h->sf_prefetch = value < 0 ? 0 : (int)std::min<int64_t>(value, 31);
     return CA_OK;

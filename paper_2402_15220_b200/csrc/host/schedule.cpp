@@ -238,6 +238,13 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
       }
     }
     X.dk_units = (int64_t)dk_unit.size() / kDkUnitInts;
+    int64_t n_cf = 0, n_pv = 0;  // chunk-first units, full private chunks
+    for (int64_t u = 0; u < X.dk_units; ++u) {
+      const int32_t f = dk_unit[(size_t)kDkUnitInts * u + 3];
+      if (!(f & DK_PRIV)) ++n_cf;
+      else if (!(f & DK_PACK)) ++n_pv;
+    }
+    X.dk_um = opt.dk_umma_ok && n_cf > 0 && (opt.dk_umma == 2 || (opt.dk_umma == 1 && n_cf >= opt.dk_umma_ratio * n_pv));
   }
   // old schedules (two-kernel / fused persistent): not built when the K5
   // cluster decode runs the step

@@ -90,6 +90,12 @@ struct ScheduleOptions {
   double dk_shared_row = 0.01;
   double dk_pack_fixed = 1.3;    // a pack of last chunks = fixed + sum of valid / c / 2
   int32_t dk_hg_forced = 0;      // > 0: heads per cluster group (divides num_heads)
+  // K5 chunk-first units on tcgen05 (decode.cu UM variant): 0 off, 1 when the
+  // chunk-first units are at least dk_umma_ratio x the full private chunks,
+  // 2 always; dk_umma_ok = the shape has the variant (16-bit, c = 64)
+  int32_t dk_umma = 1;
+  bool dk_umma_ok = false;
+  double dk_umma_ratio = 0.5;
 };
 
 // Offsets (int32 units) of the arrays inside the blob.
@@ -121,6 +127,7 @@ struct Context {
   bool dk = false;
   int32_t dk_cs = 0, dk_blocks = 0, dk_groups = 0, dk_max_rows = 0, dk_hg = 1;
   int64_t dk_units = 0;
+  bool dk_um = false;  // chunk-first units on tcgen05 requested (the launch checks the shared-memory layout)
 };
 
 // Build the context of the current tree.  Returns false (and sets *err) when

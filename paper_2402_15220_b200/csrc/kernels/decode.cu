@@ -35,6 +35,8 @@
 // the stage (the MMA reads that token's ldmatrix rows from there); the
 // consumer warp that attends it writes those rows into the pool slot.
 // m is kept in log2 units (scale * log2 e folded into the logits).
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <map>
 #include <mutex>
@@ -43,6 +45,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "mma_attn.cuh"
+#include "umma.cuh"
 
 namespace pakv {
 
@@ -50,29 +53,58 @@ using namespace dev;
 
 namespace {
 
-// 12 warps: warpgroup 0 = the producer warp + 3 idle warps, warpgroups 1-2 =
-// NC = 8 consumer warps.  Registers are
-// re-balanced per warpgroup with setmaxnreg (72 for warpgroup 0, 216 for the
-// consumers: 128 x 72 + 256 x 216 <= 64 K).
-constexpr int kNC = 8;                           // consumer warps
-constexpr int kConsumer0 = 4;                    // first consumer warp
+// 12 warps in both variants.
+//   mma.sync variant (UM = false): warpgroup 0 = the producer warp + 3 idle
+//     warps; warpgroups 1-2 = NC = 8 mma.sync consumer warps (every unit).
+//   tcgen05 variant (UM = true, c = 64): warp 0 = the seq-first producer
+//     (private units and packs, 1-D bulk copies), warp 1 = the chunk-first
+//     TMA producer (2-D boxes of the K / V tiles, SWIZZLE_128B images), warp 2
+//     = the MMA issuer (one thread: S = Q K^T, O += P V, M = 64, S double
+//     buffered and O in TMEM), warp 3 idle; warpgroup 1 = the softmax warps
+//     (thread = query row = TMEM lane: the M = 64 layout puts row 16 q + i in
+//     lane 32 q + i, so lanes 0-15 of each warp hold rows); warpgroup 2 = NC =
+//     4 mma.sync consumer warps for the private units.  The two phases of the
+//     paper run concurrently on one SM: tensor cores for the shared chunks,
+//     the CUDA-core GEMV ring for the private ones.
+// Registers are re-balanced per warpgroup with setmaxnreg.
 constexpr int kDkThreads = 12 * 32;
-constexpr int kRegsLow = 72, kRegsHigh = 216;
+constexpr int kRegsLow = 72, kRegsHigh = 216;            // mma.sync variant
+constexpr int kRegsSoftmax = 200, kRegsConsumerUm = 232;  // tcgen05 variant: 72 + 200 + 232 = 3 x 168
 constexpr int kDkMaxStages = 8;
 constexpr int kDkSlice = 32;                     // chunk-first token slice per warp and call (>= 32: latency)
 constexpr size_t kDkSmemBudget = 232448 - 2048;  // 227 KB opt-in, minus static shared memory
 constexpr int kStateRows = kDkMaxRows;           // (head, row) states per CTA: hg * block rows <= 64
+constexpr int kMergeWarp0 = 4, kMergeThreads = 256;  // warps 4..11 run the final folds and the cluster merge
+// tcgen05 variant
+constexpr int kUmC = 64;                 // chunk size of the variant
+constexpr int kUmM = 64;                 // UMMA M (rows of a K5 block <= 64)
+constexpr int kUmMaxCf = 5;              // K (and V) ring depth cap
+constexpr int kCfProducerWarp = 1, kIssuerWarp = 2, kVProducerWarp = 3, kSoftmaxWarp0 = 4;
+constexpr float kRescaleLog2 = 8.f;      // lazy O rescale threshold (P <= 2^8), as chunk_first_umma.cu
+
+template <bool UM>
+struct DkRoles {
+  static constexpr int NC = UM ? 4 : 8;  // mma.sync consumer warps
+  static constexpr int C0 = UM ? 8 : 4;  // first consumer warp
+};
 
 // Stage metadata: a unit (flags, valid tokens, rows, head of the set) or a
 // PACK of n rows' last chunks (row, valid tokens, first slot row, head), or END.
 struct DkMeta {
   int flags, n, nt, row0, nrows, hh;
-  int prow[kNC], pnt[kNC], poff[kNC], phh[kNC], pchunk[kNC];
+  int prow[8], pnt[8], poff[8], phh[8], pchunk[8];
 };
 
+template <int NC>
 CA_DEV void dk_sync_consumers() {  // bar.sync is .aligned: arrive converged
   __syncwarp();
-  asm volatile("bar.sync 1, %0;" ::"n"(kNC * 32) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(NC * 32) : "memory");
+}
+// warps 4..11 (an mbarrier of 8 warp arrivals, phase `ph`)
+CA_DEV void dk_sync_merge(uint64_t* bar, uint32_t ph) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive_cta(bar);
+  mbar_wait(bar, ph);
 }
 template <int N>
 CA_DEV void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
@@ -84,13 +116,6 @@ CA_DEV void mbar_arrive1(uint64_t* bar) {
 CA_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-CA_DEV void bulk_s2g(void* dst, const void* src, uint32_t bytes) {  // shared -> global, bulk group
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
-               : "memory");
-}
-CA_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-CA_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-CA_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 CA_DEV void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 CA_DEV void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 // 16 bytes into another CTA's shared memory, completing bytes on its mbarrier
@@ -103,19 +128,6 @@ CA_DEV uint32_t mapa(uint32_t addr, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
-}
-CA_DEV float4 ld_cluster_f4(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(addr)
-               : "memory");
-  return v;
-}
-CA_DEV float2 ld_cluster_f2(uint32_t addr) {
-  float2 v;
-  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
-  return v;
 }
 
 // (head, row) state layout in shared memory: [hg][rows][D + 4] fp32 =
@@ -133,19 +145,44 @@ CA_DEV void fold_weights(float ms, float mj, float& M, float& ws, float& wj) {
   wj = mj == -INFINITY ? 0.f : fast_exp2(mj - M);
 }
 
-template <typename T, typename TO, int D, int TPW>
+// Shared-memory layout (bytes from the dynamic base): SF ring [nst][stage] |
+// states [scap][SR] | (UM) chunk-first states [scap][SR] | recv area | (UM,
+// 1024-aligned at run time) K ring [nk][K image] | V ring [nv][V image] | Q
+// image | P images [2].
+struct DkLayout {
+  int32_t nst, nk, nv, scap;
+  uint32_t stage_bytes, cf_off;
+  int32_t bulk1d;  // d = 64: K/V tiles by one 1-D bulk copy (the pool tile is already the SWIZZLE_128B image)
+};
+
+template <typename T, typename TO, int D, int TPW, bool UM>
 __global__ void __launch_bounds__(kDkThreads, 1)
-    dk_kernel(T* kpool, T* vpool, const T* __restrict__ q, TO* __restrict__ out, const T* __restrict__ knew,
+    dk_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v, T* kpool,
+              T* vpool, const T* __restrict__ q, TO* __restrict__ out, const T* __restrict__ knew,
               const T* __restrict__ vnew, int32_t* __restrict__ len_out, int32_t mode, DevTables t, int32_t h,
-              int32_t c, float scale_log2, int32_t nst, uint32_t stage_bytes, int32_t cs, int32_t hg,
+              int32_t c, float scale_log2, DkLayout ly, int64_t layer_rows, int32_t cs, int32_t hg,
               uint64_t* __restrict__ trace) {
   using WA = WarpAttn<T, D, TPW>;
+  constexpr int NC = DkRoles<UM>::NC, kConsumer0 = DkRoles<UM>::C0;
   constexpr int SR = RowState<D>::kStride;
   constexpr uint32_t kRowBytes = D * sizeof(T);
+  // tcgen05 variant geometry (c = 64)
+  constexpr int HALVES = D / 64;                             // 128-byte d-halves of a token row
+  constexpr uint32_t kCfTile = HALVES * kUmC * 128;          // one K (or V) SWIZZLE_128B image
+  constexpr uint32_t kQImg = HALVES * kUmM * 128;            // Q image, M = 64 rows
+  constexpr uint32_t kPImg = kUmM * 128;                     // P image (c = 64 tokens = one 128-byte atom)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[kDkMaxStages], empty_bar[kDkMaxStages];
   __shared__ DkMeta meta[kDkMaxStages];
   __shared__ uint64_t recv_bar;  // the other ranks' copies of this rank's merge states have arrived
+  __shared__ uint64_t merge_bar;  // warps 4..11 done with their units (phase 0) / the state folds (phase 1)
+  // tcgen05 variant: chunk-first ring, MMA / softmax hand-offs
+  __shared__ uint64_t k_full[UM ? kUmMaxCf : 1], k_empty[UM ? kUmMaxCf : 1];
+  __shared__ uint64_t v_full[UM ? kUmMaxCf : 1], v_empty[UM ? kUmMaxCf : 1];
+  __shared__ int4 cf_meta[UM ? kUmMaxCf : 1];  // K slot's unit {flags, row0, rows, head of the set}
+  __shared__ int4 s_meta[2];                   // the unit of S buffer b (issuer -> softmax)
+  __shared__ uint64_t s_full[2], s_free[2], s_meta_full[2], p_full[2], pv_done[2], q_full, o_ready, o_free;
+  __shared__ uint32_t tmem_base;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rank = (int)(blockIdx.x % (unsigned)cs), grp = (int)(blockIdx.x / (unsigned)cs);
@@ -157,9 +194,16 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   const int32_t* crp = t.dk_cta + (size_t)kDkCtaInts * (blk * cs + rank);
   const int4 crec = *reinterpret_cast<const int4*>(crp);
   const int u0 = crec.x, u1 = crec.y, npre = crec.z;
+  const int nst = ly.nst, nk = ly.nk, nv = ly.nv;
+  const uint32_t stage_bytes = ly.stage_bytes;
   const uint32_t tile_bytes = (uint32_t)c * kRowBytes;
   float* st = reinterpret_cast<float*>(smem_raw + (size_t)nst * stage_bytes);  // (head, row) states
-  float* recv = st + (size_t)kStateRows * SR;  // [owned state][other rank][SR]: pushed by the other ranks
+  float* cst = st + (size_t)ly.scap * SR;                 // UM: chunk-first states (same indexing)
+  float* recv = (UM ? cst : st) + (size_t)ly.scap * SR;  // [owned state][other rank][SR]: pushed by the other ranks
+  unsigned char* cfr = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + ly.cf_off + 1023) & ~uintptr_t(1023));  // UM: chunk-first ring
+  unsigned char* sQ = cfr + (size_t)(nk + nv) * kCfTile;
+  unsigned char* sP = sQ + kQImg;
   auto state_row = [&](int hh, int row) { return st + (size_t)(hh * brows + row - brow0) * SR; };
   // mode bit 0: scatter the step's new K/V row into each row's last chunk
   // (K1 folded in); bit 1: the lengths advance by one in this launch (the
@@ -172,23 +216,53 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full_bar[s], 1);  // producer: expected bytes per copy, then one arrive with the metadata
-      mbar_init(&empty_bar[s], kNC);
+      mbar_init(&empty_bar[s], NC);
     }
     mbar_init(&recv_bar, 1);
+    mbar_init(&merge_bar, kMergeThreads / 32);
+    if constexpr (UM) {
+      for (int s = 0; s < nk; ++s) {
+        mbar_init(&k_full[s], 1);   // K producer: arrive + expected bytes
+        mbar_init(&k_empty[s], 1);  // commit after the slot's S
+      }
+      for (int s = 0; s < nv; ++s) {
+        mbar_init(&v_full[s], 1);   // V producer: arrive + expected bytes
+        mbar_init(&v_empty[s], 1);  // commit after the slot's P V
+      }
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&s_meta_full[b], 1);
+        mbar_init(&s_full[b], 1);
+        mbar_init(&s_free[b], 4);
+        mbar_init(&p_full[b], 4);
+        mbar_init(&pv_done[b], 1);
+      }
+      mbar_init(&q_full, 4);
+      mbar_init(&o_ready, 1);
+      mbar_init(&o_free, 4);
+    }
     fence_barrier_init();
   }
+  if constexpr (UM) {
+    if (warp == kIssuerWarp) {  // S double buffer (2 x 64 columns) + O (D columns) <= 256
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+  }
   __syncthreads();
+  if constexpr (UM) tc_fence_after();
   // cluster barrier phase: every CTA's recv_bar is initialised before any
   // rank pushes into it (waited for just before the pushes, at the end)
   if (cs > 1) cluster_arrive();
 
-  if (warp < kConsumer0) {
+  if (warp < 4) {
    regs_dec<kRegsLow>();
    if (warp == 0) {
     // ------------------------------------------------------------ producer
-    // Stages: a chunk-first unit, a cooperative seq-first unit, or a PACK of
-    // up to NC rows' last chunks (16-token slots, one row per consumer warp),
-    // packed greedily in unit order; then an END stage.
+    // Stages: a chunk-first unit (mma.sync variant only), a cooperative
+    // seq-first unit, or a PACK of up to NC rows' last chunks (16-token slots,
+    // one row per consumer warp), packed greedily in unit order; then an END
+    // stage.
     int jj = 0, rs = 0;  // stages published; ring slot / phase of the next one
     uint32_t rph = 0;
     int pk_n = 0, pk_q = 0, pk_s = 0;  // open pack: rows, 16-token slots used, its stage
@@ -201,7 +275,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     auto publish = [&](int s, uint32_t bytes) {  // metadata written: complete the stage (lane 0)
       if (lane == 0) {
         mbar_arrive1(&full_bar[s]);
-        if (tr && jj < kTraceUnits) {
+        if (!UM && tr && jj < kTraceUnits) {
           tr[3 + 4 * jj] = globaltimer_ns();
           tr[6 + 4 * jj] = bytes;
         }
@@ -279,12 +353,13 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     };
     pdl_wait();  // the pool, q and the lengths may come from the previous kernel (PDL)
     // the leading chunk-first units straight from the CTA record (one
-    // dependent load less before the first copy)
+    // dependent load less before the first copy); the tcgen05 variant's
+    // chunk-first units belong to the TMA producer (warp 1)
     int upre = u0;
     for (int k = 0; k < npre; ++k) {
       const int4 dd = *reinterpret_cast<const int4*>(crp + 4 + 4 * k);
       if (dd.w & DK_PRIV) break;
-      issue_unit(dd.x, dd.y, dd.z, dd.w & 0xff, dd.w >> 8, 0, c);
+      if constexpr (!UM) issue_unit(dd.x, dd.y, dd.z, dd.w & 0xff, dd.w >> 8, 0, c);
       ++upre;
     }
     for (int base = upre; base < u1; base += 32) {
@@ -307,7 +382,8 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         const int i_row0 = __shfl_sync(0xffffffffu, d.y, i);
         const int i_nrows = __shfl_sync(0xffffffffu, d.z, i);
         const int i_word = __shfl_sync(0xffffffffu, d.w, i);
-        const int i_flags = i_word & 0xff, i_hh = i_word >> 8, head = head0 + i_hh;
+        const int i_flags = i_word & 0xff, i_hh = i_word >> 8;
+        if (UM && !(i_flags & DK_PRIV)) continue;  // warp 1's
         int i_caller = 0, i_nt = c;
         if (i_flags & DK_PRIV) {  // warp-uniform
           i_caller = __shfl_sync(0xffffffffu, caller, i);
@@ -316,7 +392,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         const uint32_t kv_bytes = (uint32_t)i_nt * kRowBytes;
         if (i_flags & DK_PACK) {
           const int slots = (i_nt + 15) >> 4;
-          if (pk_n > 0 && (pk_q + slots > pk_cap || pk_n == kNC)) close_pack(d, caller, nt, lenv);
+          if (pk_n > 0 && (pk_q + slots > pk_cap || pk_n == NC)) close_pack(d, caller, nt, lenv);
           if (pk_n == 0) pk_s = acquire();
           if (lane == i) {
             my_pack = pk_id;
@@ -336,16 +412,367 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     const int s = acquire();
     if (lane == 0) meta[s].flags = DK_END;
     publish(s, 0);
+   } else if (UM && (warp == kCfProducerWarp || warp == kVProducerWarp)) {
+    // ----------------------------------- chunk-first TMA producers (K, V)
+    // The CTA's chunk-first units (they precede its private ones): warp 1
+    // loads K tiles into the K ring (released after S), warp 3 V tiles into
+    // the V ring (released after P V), each a 2-D box of 64 elements x 64
+    // rows per d-half -- the pool rows are XOR pre-swizzled within each
+    // 128-byte half, so the boxes land as canonical SWIZZLE_128B atoms.  The
+    // K producer ends with an END stage.
+    const bool isk = warp == kCfProducerWarp;
+    const int nslot = isk ? nk : nv;
+    uint64_t* fullb = isk ? k_full : v_full;
+    uint64_t* emptyb = isk ? k_empty : v_empty;
+    unsigned char* ring = isk ? cfr : cfr + (size_t)nk * kCfTile;
+    const CUtensorMap* map = isk ? &tmap_k : &tmap_v;
+    if (lane == 0) prefetch_tmap(map);
+    pdl_wait();
+    int k = 0;
+    bool done = false;
+    for (int base = u0; base < u1 && !done; base += 32) {
+      const int u = base + lane;
+      int4 d = make_int4(-1, 0, 0, DK_PRIV);
+      if (u < u1) d = *reinterpret_cast<const int4*>(u - u0 < npre ? crp + 4 + 4 * (u - u0) : t.dk_unit + 4 * (size_t)u);
+      const int cnt = min(32, u1 - base);
+      for (int i = 0; i < cnt; ++i, ++k) {
+        const int i_chunk = __shfl_sync(0xffffffffu, d.x, i);
+        const int i_row0 = __shfl_sync(0xffffffffu, d.y, i);
+        const int i_nrows = __shfl_sync(0xffffffffu, d.z, i);
+        const int i_word = __shfl_sync(0xffffffffu, d.w, i);
+        if (i_word & DK_PRIV) {
+          done = true;
+          break;
+        }
+        const int s = k % nslot;
+        if (k >= nslot) mbar_wait(&emptyb[s], (uint32_t)(((k / nslot) - 1) & 1));
+        if (lane == 0) {
+          if (isk) {
+            cf_meta[s] = make_int4(i_word & 0xff, i_row0, i_nrows, i_word >> 8);
+            if (tr && k < 16) {  // tcgen05 variant: the timeline traces the chunk-first units
+              tr[3 + 4 * k] = globaltimer_ns();
+              tr[6 + 4 * k] = 2 * kCfTile;
+            }
+          }
+          mbar_arrive_expect_tx(&fullb[s], kCfTile);
+          const int y = (int)(layer_rows + ((int64_t)i_chunk * h + head0 + (i_word >> 8)) * kUmC);
+          unsigned char* stg = ring + (size_t)s * kCfTile;
+          if (HALVES == 1 && ly.bulk1d)
+            bulk_g2s(stg, (isk ? kpool : vpool) + ((size_t)i_chunk * h + head0 + (i_word >> 8)) * kUmC * D, kCfTile,
+                     &fullb[s]);
+          else
+#pragma unroll
+            for (int hf = 0; hf < HALVES; ++hf) tma_load_2d(stg + hf * kUmC * 128, map, hf * 64, y, &fullb[s]);
+        }
+        __syncwarp();
+      }
+    }
+    if (isk) {
+      const int s = k % nk;
+      if (k >= nk) mbar_wait(&k_empty[s], (uint32_t)(((k / nk) - 1) & 1));
+      if (lane == 0) {
+        cf_meta[s] = make_int4(DK_END, 0, 0, 0);
+        mbar_arrive_cta(&k_full[s]);
+      }
+      __syncwarp();
+    }
+   } else if (UM && warp == kIssuerWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    // chunk k: S_{k&1} = Q K_k^T (M = 64, N = 64, K = d; its K slot released
+    // when S completes), then O += P_{k-1} V_{k-1} of the previous chunk of
+    // the same job (a job boundary flushes the pending P V first: its O is
+    // read before the next job's Q lands).  The chunk's metadata goes to the
+    // softmax warps through s_meta[k&1] (s_meta_full).
+    const uint32_t tmem = tmem_base;
+    constexpr uint32_t idS = umma_idesc<T, kUmM>(kUmC, false), idO = umma_idesc<T, kUmM>(D, true);
+    const uint32_t qa = smem_u32(sQ), pa = smem_u32(sP), ka0 = smem_u32(cfr), va0 = ka0 + nk * kCfTile;
+    int jobs_q = 0, jobs_done = 0, pend = -1, pend_flags = 0;
+    auto issue_pv = [&](int j, int fj) {
+      const int b = j & 1, sv = j % nv;
+      mbar_wait(&p_full[b], (uint32_t)((j >> 1) & 1));
+      mbar_wait(&v_full[sv], (uint32_t)((j / nv) & 1));
+      if ((fj & DK_FIRST) && jobs_done > 0) mbar_wait(&o_free, (uint32_t)((jobs_done - 1) & 1));
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t va = va0 + sv * kCfTile, pb = pa + b * kPImg;
+#pragma unroll
+        for (int ks = 0; ks < kUmC / 16; ++ks)
+          umma_f16(tmem + 2 * kUmC, umma_sdesc(pb + ks * 32, 16, 1024), umma_sdesc(va + ks * 16 * 128, kUmC * 128, 1024),
+                   idO, (!(fj & DK_FIRST) || ks > 0) ? 1u : 0u);
+        umma_commit(&pv_done[b]);
+        umma_commit(&v_empty[sv]);
+        if (fj & DK_LAST) umma_commit(&o_ready);
+      }
+      __syncwarp();
+      if (fj & DK_LAST) ++jobs_done;
+    };
+    int k = 0;
+    for (;; ++k) {
+      const int s = k % nk, b = k & 1;
+      mbar_wait(&k_full[s], (uint32_t)((k / nk) & 1));
+      if (tr && lane == 0 && k < 16) tr[70 + k] = globaltimer_ns();  // K tile k in shared memory (issuer view)
+      const int4 mk = cf_meta[s];
+      if (k >= 2) mbar_wait(&s_free[b], (uint32_t)(((k >> 1) - 1) & 1));  // S_b and s_meta[b] consumed
+      if (lane == 0) {
+        s_meta[b] = mk;
+        mbar_arrive_cta(&s_meta_full[b]);
+      }
+      if (mk.x & DK_END) break;
+      if (mk.x & DK_FIRST) {
+        if (pend >= 0) issue_pv(pend, pend_flags);
+        pend = -1;
+        mbar_wait(&q_full, (uint32_t)(jobs_q & 1));
+        ++jobs_q;
+      }
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t ka = ka0 + s * kCfTile;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {  // S = Q K^T over d
+          const uint32_t o = (ks % 4) * 32;
+          umma_f16(tmem + b * kUmC, umma_sdesc(qa + (ks / 4) * kUmM * 128 + o, 16, 1024),
+                   umma_sdesc(ka + (ks / 4) * kUmC * 128 + o, 16, 1024), idS, ks > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[b]);
+        umma_commit(&k_empty[s]);
+        if (tr && k == 0) tr[kTraceStride - 10] = globaltimer_ns();  // first S issued
+      }
+      __syncwarp();
+      if (pend >= 0) issue_pv(pend, pend_flags);
+      pend = k;
+      pend_flags = mk.x;
+    }
+    if (pend >= 0) issue_pv(pend, pend_flags);
+    // TMEM is released once the softmax warps have read the last job's O
+    if (jobs_done > 0) mbar_wait(&o_free, (uint32_t)((jobs_done - 1) & 1));
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
    }
    if (cs > 1) cluster_wait();  // the cluster barrier phase begun at entry
   } else {
+    // merge-phase constants, loaded now (the row's caller index is a cold load)
+    const int nstate = hg * brows;
+    const int mw = warp - kMergeWarp0;
+    const int mw0 = rank + cs * mw;
+    const int mcaller = mw0 < nstate ? t.row_caller[brow0 + mw0 % brows] : 0;
+    if (UM && warp < kSoftmaxWarp0 + 4) {
+      regs_inc<kRegsSoftmax>();
+      // ------------------------------------------------ softmax (tcgen05)
+      // Warp qd reads TMEM lane quadrant qd = M rows 16 qd .. 16 qd + 15 of
+      // the M = 64 tile (M row 16 q + i sits in lane 32 q + i) in the
+      // .16x256b shape: thread t holds M rows m0 = 16 qd + t / 4 and m0 + 8,
+      // columns 8 j + 2 (t % 4) + {0, 1} -- a quad shares a row (max / sum by
+      // two shuffles).  Jobs of <= 32 rows are placed 8 per quadrant (job row
+      // j at M row 16 (j / 8) + j % 8: all four warps -- all four SM
+      // sub-partitions' exp units -- work, on the m0 rows only); larger jobs
+      // fill M rows 0..63 in order.  Per chunk: S from TMEM, online softmax
+      // with the lazy O rescale, P (16-bit, SWIZZLE_128B) to shared memory;
+      // per job: O from TMEM folded into the (head, row) chunk-first states
+      // (Eqn 2).
+      const int qd = warp - kSoftmaxWarp0;  // TMEM lane quadrant
+      const int jr = qd * 16 + (lane & 15);  // Q image (M) row written by this thread
+      const int m0 = qd * 16 + (lane >> 2), c0 = 2 * (lane & 3);
+      const uint32_t tmem = tmem_base;
+      const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
+      const uint32_t tO = tmem + 2 * kUmC;
+      const int sct = tid - kSoftmaxWarp0 * 32;
+      // job row of M row m (-1: unused row)
+      auto job_row = [&](int m, int nrows) {
+        const int j = nrows > 32 ? m : ((m & 15) < 8 ? (m >> 4) * 8 + (m & 7) : -1);
+        return j < nrows ? j : -1;
+      };
+      // Q image of a job's rows (unused M rows zero); the previous job's S
+      // MMAs (the only readers) completed before its last S_full
+      constexpr int G = D / 8 / 2;  // 16-byte groups per lane half
+      uint4 qv[G];
+      auto load_q = [&](int row0, int nrows, int hh) {
+        const int j = job_row(jr, nrows);
+        const T* qrow = j >= 0 ? q + ((size_t)t.row_caller[row0 + j] * h + head0 + hh) * D : nullptr;
+#pragma unroll
+        for (int e = 0; e < G; ++e)
+          qv[e] = qrow ? *reinterpret_cast<const uint4*>(qrow + ((lane >> 4) * G + e) * 8) : make_uint4(0u, 0u, 0u, 0u);
+      };
+      auto store_q = [&]() {
+#pragma unroll
+        for (int e = 0; e < G; ++e) {
+          const int gg = (lane >> 4) * G + e;
+          *reinterpret_cast<uint4*>(sQ + (gg / 8) * kUmM * 128 + sw128(jr, gg % 8)) = qv[e];
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cta(&q_full);
+      };
+      pdl_wait();  // q comes from the previous kernel
+      // the CTA's first job from its record: its Q loads are in flight while
+      // the chunk-first states are initialised and the first K/V tiles load
+      bool qpre = false;
+      if (npre > 0) {
+        const int4 d0 = *reinterpret_cast<const int4*>(crp + 4);
+        if (!(d0.w & DK_PRIV)) {
+          load_q(d0.y, d0.z, d0.w >> 8);
+          qpre = true;
+        }
+      }
+#pragma unroll 1
+      for (int i = sct; i < hg * brows * SR; i += 128) cst[i] = (i % SR) == D ? -INFINITY : 0.f;
+      asm volatile("bar.sync 3, 128;" ::: "memory");  // chunk-first states initialised
+      if (qpre) {
+        store_q();
+        if (tr && sct == 0) tr[kTraceStride - 6] = globaltimer_ns();  // first Q image written
+      }
+      float m_ref[2] = {-INFINITY, -INFINITY}, n[2] = {0.f, 0.f};  // M rows m0, m0 + 8 (n: this thread's columns)
+      int crow0 = 0, cnrows = 0, chh = 0, jobs = 0, nh = 2;
+      for (int k = 0;; ++k) {
+        const int b = k & 1;
+        mbar_wait(&s_meta_full[b], (uint32_t)((k >> 1) & 1));
+        const int4 mt = s_meta[b];
+        if (mt.x & DK_END) break;
+        if (mt.x & DK_FIRST) {
+          crow0 = mt.y;
+          cnrows = mt.z;
+          chh = mt.w;
+          nh = cnrows > 32 ? 2 : 1;  // M row halves holding job rows (warp-uniform)
+          if (!qpre) {
+            load_q(crow0, cnrows, chh);
+            store_q();
+          }
+          qpre = false;
+          m_ref[0] = m_ref[1] = -INFINITY;
+          n[0] = n[1] = 0.f;
+        }
+        mbar_wait(&s_full[b], (uint32_t)((k >> 1) & 1));
+        tc_fence_after();
+        if (tr && sct == 0 && k < 16) tr[4 + 4 * k] = globaltimer_ns();
+        uint32_t u[32];  // rep j: S[m0][8j + c0 + 0/1] = u[4j], u[4j + 1]; S[m0 + 8][...] = u[4j + 2], u[4j + 3]
+        tmem_ld16x256_x8(tmem + b * kUmC + lane_base, u);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cta(&s_free[b]);
+        float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          if (hf >= nh) break;
+          float a0 = __uint_as_float(u[2 * hf]), a1 = __uint_as_float(u[2 * hf + 1]);
+#pragma unroll
+          for (int j = 1; j < 8; ++j) {
+            a0 = fmaxf(a0, __uint_as_float(u[4 * j + 2 * hf]));
+            a1 = fmaxf(a1, __uint_as_float(u[4 * j + 2 * hf + 1]));
+          }
+          float m = fmaxf(a0, a1);
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+          mx[hf] = m * scale_log2;  // scale > 0: the max commutes with it
+        }
+        // lazy rescale: a new reference max only when a row's max grew by more than 2^8
+        const bool need0 = mx[0] > m_ref[0] + kRescaleLog2, need1 = mx[1] > m_ref[1] + kRescaleLog2;
+        if (__any_sync(0xffffffffu, need0 || need1)) {
+          float f[2];
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            const bool nd = hf ? need1 : need0;
+            const float m_new = nd ? mx[hf] : m_ref[hf];
+            f[hf] = (nd && m_ref[hf] != -INFINITY) ? fast_exp2(m_ref[hf] - m_new) : 1.f;
+            n[hf] *= f[hf];
+            m_ref[hf] = m_new;
+          }
+          if (!(mt.x & DK_FIRST)) {  // O holds this job's chunks so far: wait for the last P V, scale in TMEM
+            mbar_wait(&pv_done[(k - 1) & 1], (uint32_t)(((k - 1) >> 1) & 1));
+            tc_fence_after();
+#pragma unroll 1
+            for (int cb = 0; cb < D; cb += 64) {
+              uint32_t o[32];
+              tmem_ld16x256_x8(tO + lane_base + cb, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f[(i >> 1) & 1]);
+              tmem_st16x256_x8(tO + lane_base + cb, o);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+          }
+        }
+        // P = exp2(s - m_ref) rounded to T (n from the rounded P, reading A11)
+        if (k >= 2) mbar_wait(&pv_done[b], (uint32_t)(((k >> 1) - 1) & 1));  // P V_{k-2} read this buffer
+        unsigned char* pb = sP + b * kPImg;
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          if (hf >= nh) break;
+          float ns0 = 0.f, ns1 = 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t w = Mma<T>::pack(fast_exp2(fmaf(__uint_as_float(u[4 * j + 2 * hf]), scale_log2, -m_ref[hf])),
+                                            fast_exp2(fmaf(__uint_as_float(u[4 * j + 2 * hf + 1]), scale_log2, -m_ref[hf])));
+            const float2 f2 = Mma<T>::unpack(w);
+            if (j & 1) ns1 += f2.x + f2.y; else ns0 += f2.x + f2.y;
+            *reinterpret_cast<uint32_t*>(pb + sw128(m0 + 8 * hf, j) + c0 * 2) = w;
+          }
+          n[hf] += ns0 + ns1;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cta(&p_full[b]);
+        if (tr && sct == 0 && k < 16) tr[5 + 4 * k] = globaltimer_ns();
+        if (mt.x & DK_LAST) {
+          // job end: O from TMEM folded into the (head, row) chunk-first states
+          float nr[2];
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            nr[hf] = n[hf] + __shfl_xor_sync(0xffffffffu, n[hf], 1);
+            nr[hf] += __shfl_xor_sync(0xffffffffu, nr[hf], 2);
+          }
+          mbar_wait(&o_ready, (uint32_t)(jobs & 1));
+          tc_fence_after();
+          float* srow[2];
+          float ws[2], wj[2], Mn[2];
+          bool ok[2];
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            const int j = hf < nh ? job_row(m0 + 8 * hf, cnrows) : -1;
+            ok[hf] = j >= 0;
+            srow[hf] = cst + (size_t)(chh * brows + (ok[hf] ? crow0 + j : brow0) - brow0) * SR;
+            ws[hf] = wj[hf] = Mn[hf] = 0.f;
+            if (ok[hf]) fold_weights(srow[hf][D], m_ref[hf], Mn[hf], ws[hf], wj[hf]);
+          }
+#pragma unroll 1
+          for (int cb = 0; cb < D; cb += 64) {
+            uint32_t o[32];
+            tmem_ld16x256_x8(tO + lane_base + cb, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              if (!ok[hf]) continue;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                float2* p = reinterpret_cast<float2*>(srow[hf] + cb + 8 * j + c0);
+                const float2 x = *p;
+                *p = make_float2(fmaf(wj[hf], __uint_as_float(o[4 * j + 2 * hf]), x.x * ws[hf]),
+                                 fmaf(wj[hf], __uint_as_float(o[4 * j + 2 * hf + 1]), x.y * ws[hf]));
+              }
+            }
+          }
+          __syncwarp();  // the quad read m, n before they change
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf)
+            if (ok[hf] && (lane & 3) == 0) {
+              srow[hf][D + 1] = fmaf(wj[hf], nr[hf], srow[hf][D + 1] * ws[hf]);
+              srow[hf][D] = Mn[hf];
+            }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cta(&o_free);
+          ++jobs;
+          if (tr && sct == 0) tr[kTraceStride - 7] = globaltimer_ns();  // job epilogue done
+        }
+      }
+    } else {
     // ----------------------------------------------------------- consumers
-    regs_inc<kRegsHigh>();
+    if constexpr (UM) regs_inc<kRegsConsumerUm>(); else regs_inc<kRegsHigh>();
     const int ct = tid - kConsumer0 * 32, cw = warp - kConsumer0;
 #pragma unroll 1
-    for (int i = ct; i < hg * brows * SR; i += kNC * 32) st[i] = (i % SR) == D ? -INFINITY : 0.f;
+    for (int i = ct; i < hg * brows * SR; i += NC * 32) st[i] = (i % SR) == D ? -INFINITY : 0.f;
     pdl_wait();  // q comes from the previous kernel
-    dk_sync_consumers();  // states initialised
+    dk_sync_consumers<NC>();  // states initialised
     WA wa;
     uint32_t qa[WA::KS][4];
     auto q_row0 = [&](const unsigned char* qrow) {  // the query in row 0 of the MMA tile (lanes 0..3)
@@ -366,7 +793,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       chh = hh;
       int g = 1;
       while (g * 16 < nrows) g *= 2;
-      cfL = kNC / g;
+      cfL = NC / g;
       cfg = cw / cfL;
       cfl = cw % cfL;
       cact = cfg * 16 < crows;
@@ -416,11 +843,13 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     // the CTA's first job, if chunk-first: its Q fragments (global loads)
     // overlap the first K/V copies
     bool pre = false;
-    if (npre > 0) {
-      const int4 d0 = *reinterpret_cast<const int4*>(crp + 4);
-      if (!(d0.w & DK_PRIV)) {
-        begin_cf(d0.y, d0.z, d0.w >> 8);
-        pre = true;
+    if constexpr (!UM) {
+      if (npre > 0) {
+        const int4 d0 = *reinterpret_cast<const int4*>(crp + 4);
+        if (!(d0.w & DK_PRIV)) {
+          begin_cf(d0.y, d0.z, d0.w >> 8);
+          pre = true;
+        }
       }
     }
     int jj = 0, rs = 0;
@@ -428,7 +857,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     for (;; ++jj) {
       const int s = rs;
       mbar_wait(&full_bar[s], rph);
-      if (tr && ct == 0 && jj < kTraceUnits) tr[4 + 4 * jj] = globaltimer_ns();
+      if (!UM && tr && ct == 0 && jj < kTraceUnits) tr[4 + 4 * jj] = globaltimer_ns();
       const int flags = meta[s].flags;
       if (flags & DK_END) break;
       const unsigned char* stg = smem_raw + (size_t)s * stage_bytes;
@@ -462,8 +891,10 @@ __global__ void __launch_bounds__(kDkThreads, 1)
           }
         }
       } else if (flags & DK_PRIV) {
-        // ---- cooperative seq-first unit (Alg 2): one row; two teams of four
-        // warps take alternate chunks of the job, warp (team, w) = token slice w
+        // ---- cooperative seq-first unit (Alg 2): one row; NC / 4 teams of
+        // four warps take alternate chunks of the job, warp (team, w) = token
+        // slice w
+        constexpr int kTeams = NC / 4;
         const int nt = meta[s].nt;
         if (flags & DK_FIRST) {
           wa.reset();
@@ -471,14 +902,14 @@ __global__ void __launch_bounds__(kDkThreads, 1)
           kp = 0;
         }
         const int team = cw >> 2, tw = cw & 3;
-        if ((kp & 1) == team && tw * TPW < nt) wa.template chunk<true>(qa, k_u32, v_u32, tw * TPW, nt, scale_log2, lane);
+        if ((kp % kTeams) == team && tw * TPW < nt) wa.template chunk<true>(qa, k_u32, v_u32, tw * TPW, nt, scale_log2, lane);
         ++kp;
         if (flags & DK_LAST) {
           // fold the warps' row-0 states into the row's state, warp order
           // (scratch: this stage's K tile -- every warp is done reading it)
           wa.finish();
           float* pw = reinterpret_cast<float*>(const_cast<unsigned char*>(stg));
-          dk_sync_consumers();
+          dk_sync_consumers<NC>();
           if (lane < 4) {
             if (lane == 0) {
               pw[cw * SR + D] = wa.m_lo;
@@ -488,39 +919,39 @@ __global__ void __launch_bounds__(kDkThreads, 1)
             for (int i = 0; i < WA::DT; ++i)
               *reinterpret_cast<float2*>(&pw[cw * SR + i * 8 + lane * 2]) = make_float2(wa.o[i][0], wa.o[i][1]);
           }
-          dk_sync_consumers();
+          dk_sync_consumers<NC>();
           float* srow = state_row(meta[s].hh, meta[s].row0);
           const float ms = srow[D], ns = srow[D + 1];
           float M = ms;
 #pragma unroll
-          for (int w = 0; w < kNC; ++w) M = fmaxf(M, pw[w * SR + D]);
+          for (int w = 0; w < NC; ++w) M = fmaxf(M, pw[w * SR + D]);
           if (M != -INFINITY) {
-            float wgt[kNC];
+            float wgt[NC];
             const float wsf = ms == -INFINITY ? 0.f : fast_exp2(ms - M);
 #pragma unroll
-            for (int w = 0; w < kNC; ++w) {
+            for (int w = 0; w < NC; ++w) {
               const float mw = pw[w * SR + D];
               wgt[w] = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
             }
-            for (int x = ct; x < D; x += kNC * 32) {
+            for (int x = ct; x < D; x += NC * 32) {
               float a = srow[x] * wsf;
 #pragma unroll
-              for (int w = 0; w < kNC; ++w) a = fmaf(wgt[w], pw[w * SR + x], a);
+              for (int w = 0; w < NC; ++w) a = fmaf(wgt[w], pw[w * SR + x], a);
               srow[x] = a;
             }
-            dk_sync_consumers();  // every thread read ms before it changes
+            dk_sync_consumers<NC>();  // every thread read ms before it changes
             if (ct == 0) {
               float nn = ns * wsf;
 #pragma unroll
-              for (int w = 0; w < kNC; ++w) nn = fmaf(wgt[w], pw[w * SR + D + 1], nn);
+              for (int w = 0; w < NC; ++w) nn = fmaf(wgt[w], pw[w * SR + D + 1], nn);
               srow[D] = M;
               srow[D + 1] = nn;
             }
           }
           fence_proxy_async();  // generic writes to the stage before its next bulk copy
-          dk_sync_consumers();  // scratch / row state reuse
+          dk_sync_consumers<NC>();  // scratch / row state reuse
         }
-      } else {
+      } else if constexpr (!UM) {
         // ---- chunk-first unit (Alg 1): rows [row0, row0 + nrows) of a shared run
         if (flags & DK_FIRST) {
           if (!pre) begin_cf(meta[s].row0, meta[s].nrows, meta[s].hh);
@@ -537,7 +968,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
           // fold lane l's 16-row partial into the rows' states, lanes in order
           wa.finish();
           for (int l = 0; l < cfL; ++l) {
-            dk_sync_consumers();
+            dk_sync_consumers<NC>();
             if (cfl == l && cact) {
               const int rl = lane >> 2, cq = (lane & 3) * 2;
 #pragma unroll
@@ -566,38 +997,56 @@ __global__ void __launch_bounds__(kDkThreads, 1)
               }
             }
           }
-          dk_sync_consumers();
+          dk_sync_consumers<NC>();
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive1(&empty_bar[s]);
-      if (tr && ct == 0 && jj < kTraceUnits) tr[5 + 4 * jj] = globaltimer_ns();
+      if (!UM && tr && ct == 0 && jj < kTraceUnits) tr[5 + 4 * jj] = globaltimer_ns();
       if (++rs == nst) {
         rs = 0;
         rph ^= 1u;
       }
     }
+    }
     // ------------------------------------------- cluster merge (Eqn 2), O / n
-    // State i is merged by rank i % cs (consumer warp (i / cs) % NC): every
+    // Warps 4..11.  (tcgen05 variant: first every chunk-first state is folded
+    // into its seq-first state, state i by warp i % 8, chunk-first first.)
+    // State i is merged by rank i % cs (merge warp (i / cs) % 8): every
     // other rank pushes its copy of state i into the owner's recv area with
     // st.async (bytes completing on the owner's recv_bar), the owner merges
     // the cs copies in rank order.  No barrier after the pushes; a cluster of
     // one merges nothing.
-    if (tr && tid == kConsumer0 * 32) tr[1] = globaltimer_ns();  // consumers done with their units
     constexpr int CPL = D / 32;  // columns per lane (4 for d = 128, 2 for d = 64)
     constexpr int Q4 = SR / 4;   // float4 per state
-    const int nstate = hg * brows;
-    const int mw = warp - kConsumer0;
-    const int mw0 = rank + cs * mw;
-    const int mcaller = mw0 < nstate ? t.row_caller[brow0 + mw0 % brows] : 0;
-    dk_sync_consumers();  // every warp's last fold is in the states
+    const int mth = tid - kMergeWarp0 * 32;
+    if (tr && tid == kConsumer0 * 32) tr[1] = globaltimer_ns();  // consumers done with their units
+    dk_sync_merge(&merge_bar, 0);
+    if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 9] = globaltimer_ns();  // merge warps synced  // every warp's last fold is in the states
+    if constexpr (UM) {
+#pragma unroll 1
+      for (int i = mw; i < nstate; i += kMergeThreads / 32) {
+        float* a = st + (size_t)i * SR;
+        const float* b = cst + (size_t)i * SR;
+        float M, wa_, wb;
+        fold_weights(b[D], a[D], M, wb, wa_);
+#pragma unroll
+        for (int e = 0; e < CPL; ++e) a[lane * CPL + e] = fmaf(wa_, a[lane * CPL + e], wb * b[lane * CPL + e]);
+        __syncwarp();
+        if (lane == 0) {
+          a[D + 1] = fmaf(wa_, a[D + 1], wb * b[D + 1]);
+          a[D] = M;
+        }
+      }
+      dk_sync_merge(&merge_bar, 1);
+    }
     if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 3] = globaltimer_ns();  // all consumer warps done
     if (cs > 1) {
       cluster_wait();  // the other ranks' recv_bar are initialised
       if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 4] = globaltimer_ns();
       const uint32_t rbase = smem_u32(recv);
 #pragma unroll 1
-      for (int v = ct; v < nstate * Q4; v += kNC * 32) {
+      for (int v = mth; v < nstate * Q4; v += kMergeThreads) {
         const int i = v / Q4, q4 = v - i * Q4, owner = i % cs;
         if (owner == rank) continue;
         const int slot = (i / cs) * (cs - 1) + (rank < owner ? rank : rank - 1);
@@ -606,7 +1055,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
                     mapa(smem_u32(&recv_bar), (uint32_t)owner));
       }
       if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 5] = globaltimer_ns();  // pushes issued
-      if (ct == 0) {
+      if (mth == 0) {
         const int owned = (nstate - rank + cs - 1) / cs;
         mbar_arrive_expect_tx(&recv_bar, (uint32_t)(owned * (cs - 1) * SR * 4));
       }
@@ -619,7 +1068,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       return j == rank ? st + (size_t)i * SR : recv + (size_t)((i / cs) * (cs - 1) + (j < rank ? j : j - 1)) * SR;
     };
 #pragma unroll 1
-    for (int i = mw0; i < nstate; i += cs * kNC) {
+    for (int i = mw0; i < nstate; i += cs * (kMergeThreads / 32)) {
       float M = -INFINITY, nsum = 0.f, acc[CPL];
 #pragma unroll 1
       for (int j = 0; j < cs; ++j) M = fmaxf(M, copy_of(i, j)[D]);
@@ -653,12 +1102,15 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     }
     if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 2] = globaltimer_ns();  // merge loop done (rank's states written)
   }
+  // warps 0-3 stay resident until the merge warps are done: an exited warp
+  // counts as arrived at the named barriers the merge warps use (bar 2)
+  __syncthreads();
   if (tr && tid == 0) tr[2] = globaltimer_ns();
 }
 
 template <typename T, typename TO, int D, int TPW>
 const void* dk_kernel_ptr() {
-  return (const void*)dk_kernel<T, TO, D, TPW>;
+  return (const void*)dk_kernel<T, TO, D, TPW, false>;
 }
 
 template <typename T, typename TO, int D>
@@ -700,15 +1152,52 @@ cudaError_t dk_prepare(const void* kern, size_t smem) {
   return e;
 }
 
+size_t state_bytes(int32_t d, int32_t n) { return (size_t)n * (d + 4) * 4; }
+
+// Shared-memory layout of a launch (kernel comment "DkLayout") and its size;
+// nk = 0 when the tcgen05 variant does not fit.
+DkLayout dk_layout(int32_t dtype, int32_t c, int32_t d, int32_t nstate, int32_t cs, bool um, size_t* smem,
+                   int max_slots = 0) {
+  DkLayout L{};
+  L.stage_bytes = (uint32_t)dk_stage_bytes(dtype, c, d);
+  if (!um) {
+    const size_t recv = dk_recv_bytes(d, nstate, cs);
+    L.scap = kStateRows;
+    L.nst = dk_stages(dtype, c, d, recv);
+    *smem = dk_smem_bytes(dtype, c, d, recv);
+    return L;
+  }
+  L.scap = nstate;
+  const size_t tile = (size_t)(d / 64) * kUmC * 128, q_img = (size_t)(d / 64) * kUmM * 128, p_img = (size_t)kUmM * 128;
+  const size_t recv = dk_recv_bytes(d, nstate, cs);
+  const size_t fixed = 2 * state_bytes(d, nstate) + recv + 1024 + q_img + 2 * p_img + L.stage_bytes;
+  *smem = 0;
+  if (fixed + 4 * tile > kDkSmemBudget) return L;
+  int slots = (int)std::min<size_t>(2 * kUmMaxCf, (kDkSmemBudget - fixed) / tile);
+  if (max_slots >= 4) slots = std::min(slots, max_slots);
+  L.nst = 1;
+  L.nv = std::min(3, slots / 2);                  // V slots wait for P V: K slots come free sooner
+  L.nk = std::min(kUmMaxCf, slots - L.nv);
+  L.cf_off = (uint32_t)(L.nst * L.stage_bytes + 2 * state_bytes(d, nstate) + recv);
+  *smem = L.cf_off + 1024 + (L.nk + L.nv) * tile + q_img + 2 * p_img;
+  return L;
+}
+
 template <typename T, typename TO, int D, int TPW>
 cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend& ap, cudaStream_t st) {
   const PoolGeom& p = a.pool;
   const int cs = t.dk_cs;
-  const size_t recv = dk_recv_bytes(D, t.dk_hg * t.dk_max_rows, cs);
-  const size_t stage = dk_stage_bytes(p.dtype, p.c, D);
-  const int nst = dk_stages(p.dtype, p.c, D, recv);
-  const size_t smem = dk_smem_bytes(p.dtype, p.c, D, recv);
-  auto kern = dk_kernel<T, TO, D, TPW>;
+  bool um = t.dk_um != 0 && dk_umma_supported(p);
+  size_t smem = 0;
+  DkLayout ly = dk_layout(p.dtype, p.c, D, t.dk_hg * t.dk_max_rows, cs, um, &smem, a.dk_slots & 63);
+  if (um && ly.nk < 2) {
+    um = false;
+    ly = dk_layout(p.dtype, p.c, D, t.dk_hg * t.dk_max_rows, cs, false, &smem);
+  }
+  ly.bulk1d = (a.dk_slots & 64) ? 0 : 1;
+  CUtensorMap mk{}, mv{};
+  if (um && !pool_maps(p, D, kUmC, &mk, &mv)) return cudaErrorNotSupported;
+  auto kern = um ? dk_kernel<T, TO, D, TPW, true> : dk_kernel<T, TO, D, TPW, false>;
   cudaError_t e = dk_prepare((const void*)kern, kDkSmemBudget);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -732,9 +1221,10 @@ cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend&
   cfg.numAttrs = na;
   T* kp = (T*)p.k + (size_t)a.layer * p.layer_stride;
   T* vp = (T*)p.v + (size_t)a.layer * p.layer_stride;
-  return cudaLaunchKernelEx(&cfg, kern, kp, vp, (const T*)a.q, (TO*)a.out, (const T*)ap.k, (const T*)ap.v,
-                            ap.len_out, (int32_t)ap.mode, t, (int32_t)p.h, (int32_t)p.c, a.scale_log2, (int32_t)nst,
-                            (uint32_t)stage, (int32_t)cs, (int32_t)t.dk_hg, a.trace);
+  const int64_t layer_rows = (int64_t)a.layer * p.max_chunks * p.h * p.c;
+  return cudaLaunchKernelEx(&cfg, kern, mk, mv, kp, vp, (const T*)a.q, (TO*)a.out, (const T*)ap.k, (const T*)ap.v,
+                            ap.len_out, (int32_t)ap.mode, t, (int32_t)p.h, (int32_t)p.c, a.scale_log2, ly, layer_rows,
+                            (int32_t)cs, (int32_t)t.dk_hg, a.trace);
 }
 
 template <typename T, typename TO, int D>
@@ -766,7 +1256,7 @@ cudaError_t dk_dispatch(const AttnLaunch& a, const DevTables& t, const DkAppend&
 
 size_t dk_stage_bytes(int32_t dtype, int32_t c, int32_t d) {
   const size_t e = (size_t)dtype_bytes(dtype);
-  const size_t pk = (size_t)std::min(kNC, std::max(1, c / 16));  // rows of one PACK
+  const size_t pk = (size_t)std::min(8, std::max(1, c / 16));  // rows of one PACK
   // K tile | V tile | pk q rows | pk new (K, V) row pairs (PACK)
   return ((size_t)2 * c * d * e + 3 * pk * d * e + 127) / 128 * 128;
 }
@@ -786,14 +1276,25 @@ size_t dk_smem_bytes(int32_t dtype, int32_t c, int32_t d, size_t recv) {
   return (size_t)dk_stages(dtype, c, d, recv) * dk_stage_bytes(dtype, c, d) + dk_state_bytes(d) + recv;
 }
 
-int dk_consumer_warps() { return kNC; }
+int dk_consumer_warps() { return DkRoles<false>::NC; }
 
 bool dk_supported(const PoolGeom& p) {
   if (p.dtype == DT_F32 || (p.d != 64 && p.d != 128)) return false;
   const int tpw = sf_mma_tpw(p.dtype, p.c, true);
   if (tpw != 16 && tpw != 32) return false;  // c in {16, 32, 48, 64, 96, 128}
-  if (p.c % 16 != 0 || p.c / tpw > kNC) return false;
+  if (p.c % 16 != 0 || p.c / tpw > DkRoles<false>::NC) return false;
   return dk_stages(p.dtype, p.c, p.d, dk_state_bytes(p.d)) >= 3;  // the largest recv area
+}
+
+bool dk_umma_supported(const PoolGeom& p) {
+  return dk_supported(p) && (p.dtype == DT_F16 || p.dtype == DT_BF16) && p.c == kUmC && (p.d == 64 || p.d == 128) &&
+         sf_mma_tpw(p.dtype, p.c, true) * 4 >= p.c;  // one team of four consumer warps covers a chunk
+}
+
+bool dk_um_fits(const PoolGeom& p, int nstate, int cs) {
+  if (!dk_umma_supported(p)) return false;
+  size_t smem = 0;
+  return dk_layout(p.dtype, p.c, p.d, nstate, cs, true, &smem).nk >= 2;
 }
 
 cudaError_t launch_decode(const AttnLaunch& a, const DevTables& t, const DkAppend& ap, cudaStream_t st) {

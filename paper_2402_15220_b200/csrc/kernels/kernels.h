@@ -37,6 +37,7 @@ struct DevTables {
   const int32_t* dk_cta;      // [blocks * cs][4] {u0, u1}: units of CTA rank r of the block's clusters
   const int32_t* dk_unit;     // [units][4] {chunk, row0, rows, DK_* flags}
   int32_t dk_cs, dk_groups, dk_max_rows, dk_blocks, dk_hg;
+  int32_t dk_um;              // chunk-first units on tcgen05 (UM variant) when its layout fits
 };
 
 
@@ -78,6 +79,7 @@ struct AttnLaunch {
   bool cf_tensor_cores;  // use the mma chunk-first kernel
   bool cf_small;         // 4-warp chunk-first CTA (co-resident with seq-first) when tiles allow
   bool cf_umma;          // tcgen05 chunk-first kernel when supported (two-kernel path)
+  int dk_slots;          // K5 tcgen05 variant: cap on K + V ring slots (0 = as many as fit)
   bool sf_tensor_cores;  // use the mma consumers in the seq-first kernel (16-bit types)
   bool use_pdl;
 };
@@ -101,6 +103,10 @@ size_t dk_recv_bytes(int32_t d, int32_t nstate, int32_t cs);
 int dk_stages(int32_t dtype, int32_t c, int32_t d, size_t recv);
 size_t dk_smem_bytes(int32_t dtype, int32_t c, int32_t d, size_t recv);
 int dk_consumer_warps();
+// the UM variant (tcgen05 chunk-first units) exists for this pool shape
+bool dk_umma_supported(const PoolGeom& pool);
+// ... and its shared-memory layout fits nstate (head, row) states in clusters of cs
+bool dk_um_fits(const PoolGeom& pool, int nstate, int cs);
 // clusters of cs CTAs that can be co-resident (cudaOccupancyMaxActiveClusters), 0 if unsupported
 int dk_max_active_clusters(const PoolGeom& pool, int out_dtype, int cs);
 cudaError_t launch_decode(const AttnLaunch& a, const DevTables& t, const DkAppend& ap, cudaStream_t st);

@@ -28,12 +28,14 @@ def _case(seed):
                 privates=[rng.randint(0, 3 * c) for _ in range(b)], steps=rng.randint(1, 4), rng=rng)
 
 
-@pytest.mark.parametrize("opts", ["", "dk_cs=1", "dk_cs=3", "dk_max_rows=16", "dk_cs=16"])
+@pytest.mark.parametrize("opts", ["", "dk_cs=1", "dk_cs=3", "dk_max_rows=16", "dk_cs=16", "dk_umma=0",
+                                  "dk_umma=2", "dk_umma=2,dk_cs=3", "dk_umma=2,dk_max_rows=16"])
 @pytest.mark.parametrize("seed", range(40))
 def test_append_attend_property_suite(seed, opts):
     """Random trees (shared prompt, private tails 0..3c incl. empty, 1..4 fused
     decode steps, permuted seq_ids order every step), cluster sizes auto / 1 /
-    3 and 16-row blocks: every (row, head) against the oracle."""
+    3 and 16-row blocks, chunk-first units on mma.sync (dk_umma=0) and on
+    tcgen05 (dk_umma=2, c = 64 cases): every (row, head) against the oracle."""
     p = _case(seed)
     hs = Harness(p["h"], p["d"], p["c"], p["dt"], p["odt"], seed=seed, alpha=p["alpha"], mode=p["mode"], opts=opts)
     ids = build_shared(hs, p["n_shared"], p["privates"], seed_tag=seed)
@@ -104,13 +106,15 @@ def test_append_attend_deterministic_and_layers():
         assert float(np.abs(o0.double().cpu().numpy() - ref).max()) <= 2e-3
 
 
+@pytest.mark.parametrize("umma", [0, 2])
 @pytest.mark.parametrize("p", [1, 65])
-def test_config2_append_attend_full_size(p):
+def test_config2_append_attend_full_size(p, umma):
     """BASELINE configs[1] (b = 32, n_s = 2048, 32 x 128 fp16) through the
-    fused step at completion tokens 1..3 after a p-1 token question: every row,
-    every head against the oracle."""
-    hs = Harness(32, 128, 64, "f16", "f16", seed=3, alpha=8.0, max_chunks=512)
+    fused step at completion tokens 1..3 after a p-1 token question, chunk-first
+    units on mma.sync and on tcgen05: every row, every head against the oracle."""
+    hs = Harness(32, 128, 64, "f16", "f16", seed=3, alpha=8.0, max_chunks=512, opts=f"dk_umma={umma}")
     ids = build_shared(hs, 2048, [p - 1] * 32)
     for st in range(1, 4):
         hs.step = st
         hs.append_attend(ids, decode_tokens(hs, ids), 2e-3, rows=list(range(32)) if st == 3 else [0, 17, 31])
+    assert hs.ca.schedule_info()["dk_um"] == (1 if umma else 0)

@@ -166,6 +166,10 @@ def main():
                 seq.append(f"[{(x[3 + 4 * u] - t0) / 1e3:.1f}/{(x[4 + 4 * u] - t0) / 1e3:.1f}/"
                            f"{(x[5 + 4 * u] - t0) / 1e3:.1f} {x[6 + 4 * u] // 1024}K]")
             print(f"   rank {r} CTA 0 units issue/ready/done: " + " ".join(seq))
+            ex = {"firstQ": TRACE_STRIDE - 6, "cf_epi": TRACE_STRIDE - 7, "firstS": TRACE_STRIDE - 10,
+                  "mergesync": TRACE_STRIDE - 9}
+            print("   rank %d (tcgen05 marks, median): " % r + " ".join(
+                f"{k} {np.median((sel[:, w] - t0) / 1e3):.2f}" for k, w in ex.items() if (sel[:, w] > 0).any()))
             print(f"   rank {r}: traced units med {np.median(nun):.0f}; consumers done med {np.median(cdone):.2f} "
                   f"max {cdone.max():.2f}; all consumers {np.median(alld):.2f}; cluster wait {np.median(cwait):.2f}; "
                   f"pushed {np.median(pushd):.2f}; merge start med {np.median(mstart):.2f}; first loads med {np.median(mload):.2f}; "
