@@ -230,6 +230,16 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
           dk_unit.insert(dk_unit.end(), {sf_chunk[sf_ptr[tl.second + 1] - 1], tl.second, 1,
                                          DK_PRIV | DK_TAIL | DK_PACK | DK_FIRST | DK_LAST | (tl.first << 8)});
         const int64_t g1 = (int64_t)dk_unit.size() / kDkUnitInts;
+        {  // the CTA's last chunk-first unit (and whether its chunk-first units are one job)
+          int64_t last_cf = -1, jobs = 0;
+          for (int64_t u = g0; u < g1; ++u) {
+            const int32_t f = dk_unit[(size_t)kDkUnitInts * u + 3];
+            if (f & DK_PRIV) continue;
+            last_cf = u;
+            if (f & DK_FIRST) ++jobs;
+          }
+          if (last_cf >= 0) dk_unit[(size_t)kDkUnitInts * last_cf + 3] |= DK_FINAL | (jobs == 1 ? DK_SOLO : 0);
+        }
         const int32_t npre = (int32_t)std::min<int64_t>(kDkCtaPre, g1 - g0);
         dk_cta.insert(dk_cta.end(), {(int32_t)g0, (int32_t)g1, npre, 0});
         for (int32_t k = 0; k < kDkCtaPre; ++k)

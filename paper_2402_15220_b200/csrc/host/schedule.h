@@ -53,8 +53,12 @@ constexpr int kSfMerger = 1 << 30;
 // {chunk id, first row, rows, DK_* flags}; CTA record (kDkCtaInts): {u0, u1}
 // = units of CTA rank r of the block's clusters; block record: {row0, rows}.
 // DK_PACK: a row's last chunk packed with other rows' into one stage (one
-// row per consumer warp); DK_END: the producer's end marker (device only).
-enum DkFlags : int32_t { DK_FIRST = 1, DK_LAST = 2, DK_TAIL = 4, DK_PRIV = 8, DK_PACK = 16, DK_END = 32 };
+// row per consumer warp); DK_END: the producer's end marker (device only);
+// DK_FINAL: the CTA's last chunk-first unit; DK_SOLO (with DK_FINAL): the
+// CTA's chunk-first units form one job.
+enum DkFlags : int32_t {
+  DK_FIRST = 1, DK_LAST = 2, DK_TAIL = 4, DK_PRIV = 8, DK_PACK = 16, DK_END = 32, DK_FINAL = 64, DK_SOLO = 128
+};
 constexpr int kDkUnitInts = 4;
 constexpr int kDkCtaInts = 16;    // {u0, u1, npre, 0, descriptors of the first npre <= kDkCtaPre units}
 constexpr int kDkCtaPre = 3;

@@ -116,12 +116,16 @@ CA_DEV void mbar_arrive1(uint64_t* bar) {
 CA_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-CA_DEV void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+// relaxed: the only writes the other ranks rely on are the mbarrier inits,
+// published by fence.mbarrier_init.release.cluster (a .release arrive is a
+// GPU-scope MEMBAR in SASS, which waits out every thread's entry loads)
+CA_DEV void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
 CA_DEV void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
-// 16 bytes into another CTA's shared memory, completing bytes on its mbarrier
-CA_DEV void st_async_f4(uint32_t addr, float4 v, uint32_t bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
-               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(bar)
+// bulk copy of `bytes` from this CTA's shared memory to another CTA's (both
+// cluster addresses), completing bytes on that CTA's mbarrier
+CA_DEV void bulk_s2cluster(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "r"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
 CA_DEV uint32_t mapa(uint32_t addr, uint32_t rank) {
@@ -153,6 +157,7 @@ struct DkLayout {
   int32_t nst, nk, nv, scap;
   uint32_t stage_bytes, cf_off;
   int32_t bulk1d;  // d = 64: K/V tiles by one 1-D bulk copy (the pool tile is already the SWIZZLE_128B image)
+  int32_t diag_empty;  // DIAGNOSTIC ONLY (no output): every CTA returns at entry -- the launch's own cost
 };
 
 template <typename T, typename TO, int D, int TPW, bool UM>
@@ -183,6 +188,8 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   __shared__ int4 s_meta[2];                   // the unit of S buffer b (issuer -> softmax)
   __shared__ uint64_t s_full[2], s_free[2], s_meta_full[2], p_full[2], pv_done[2], q_full, o_ready, o_free;
   __shared__ uint32_t tmem_base;
+  __shared__ uint64_t sf_done;  // UM: the private-unit consumers are done with the states
+  __shared__ int cf_direct;     // UM: the CTA's one chunk-first job was folded straight into the states
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rank = (int)(blockIdx.x % (unsigned)cs), grp = (int)(blockIdx.x / (unsigned)cs);
@@ -212,6 +219,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   // debug timeline (option "trace"): kernel_timeline.py layout (kernels.h)
   uint64_t* tr = trace && blockIdx.x < kTraceCtas ? trace + (size_t)blockIdx.x * kTraceStride : nullptr;
   if (tr && tid == 0) tr[0] = globaltimer_ns();
+  if (ly.diag_empty) return;
 
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) {
@@ -239,6 +247,8 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       mbar_init(&q_full, 4);
       mbar_init(&o_ready, 1);
       mbar_init(&o_free, 4);
+      mbar_init(&sf_done, DkRoles<UM>::NC);
+      cf_direct = 0;
     }
     fence_barrier_init();
   }
@@ -253,7 +263,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   if constexpr (UM) tc_fence_after();
   // cluster barrier phase: every CTA's recv_bar is initialised before any
   // rank pushes into it (waited for just before the pushes, at the end)
-  if (cs > 1) cluster_arrive();
+  if (cs > 1) cluster_arrive_relaxed();
 
   if (warp < 4) {
    regs_dec<kRegsLow>();
@@ -548,7 +558,10 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
    }
-   if (cs > 1) cluster_wait();  // the cluster barrier phase begun at entry
+   if (cs > 1) {
+     cluster_wait();            // the cluster barrier phase begun at entry
+     cluster_arrive_relaxed();  // phase 2 (the merge warps arrive once their copies are in)
+   }
   } else {
     // merge-phase constants, loaded now (the row's caller index is a cold load)
     const int nstate = hg * brows;
@@ -721,6 +734,11 @@ __global__ void __launch_bounds__(kDkThreads, 1)
             nr[hf] = n[hf] + __shfl_xor_sync(0xffffffffu, n[hf], 1);
             nr[hf] += __shfl_xor_sync(0xffffffffu, nr[hf], 2);
           }
+          // the CTA's only job: straight into the (head, row) states once the
+          // private-unit consumers are done with them (the same arithmetic as
+          // folding the chunk-first state in at the end: Eqn 2 of two partials)
+          const bool direct = (mt.x & DK_SOLO) != 0;
+          if (direct) mbar_wait(&sf_done, 0);
           mbar_wait(&o_ready, (uint32_t)(jobs & 1));
           tc_fence_after();
           float* srow[2];
@@ -730,10 +748,11 @@ __global__ void __launch_bounds__(kDkThreads, 1)
           for (int hf = 0; hf < 2; ++hf) {
             const int j = hf < nh ? job_row(m0 + 8 * hf, cnrows) : -1;
             ok[hf] = j >= 0;
-            srow[hf] = cst + (size_t)(chh * brows + (ok[hf] ? crow0 + j : brow0) - brow0) * SR;
+            srow[hf] = (direct ? st : cst) + (size_t)(chh * brows + (ok[hf] ? crow0 + j : brow0) - brow0) * SR;
             ws[hf] = wj[hf] = Mn[hf] = 0.f;
             if (ok[hf]) fold_weights(srow[hf][D], m_ref[hf], Mn[hf], ws[hf], wj[hf]);
           }
+          if (direct && sct == 0) cf_direct = 1;
 #pragma unroll 1
           for (int cb = 0; cb < D; cb += 64) {
             uint32_t o[32];
@@ -1008,6 +1027,10 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         rph ^= 1u;
       }
     }
+    if constexpr (UM) {  // the states are the chunk-first epilogue's now
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&sf_done);
+    }
     }
     // ------------------------------------------- cluster merge (Eqn 2), O / n
     // Warps 4..11.  (tcgen05 variant: first every chunk-first state is folded
@@ -1021,9 +1044,10 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     constexpr int Q4 = SR / 4;   // float4 per state
     const int mth = tid - kMergeWarp0 * 32;
     if (tr && tid == kConsumer0 * 32) tr[1] = globaltimer_ns();  // consumers done with their units
+    fence_proxy_async();  // the states' generic writes before the bulk copies read them
     dk_sync_merge(&merge_bar, 0);
     if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 9] = globaltimer_ns();  // merge warps synced  // every warp's last fold is in the states
-    if constexpr (UM) {
+    if (UM && !cf_direct) {
 #pragma unroll 1
       for (int i = mw; i < nstate; i += kMergeThreads / 32) {
         float* a = st + (size_t)i * SR;
@@ -1038,21 +1062,22 @@ __global__ void __launch_bounds__(kDkThreads, 1)
           a[D] = M;
         }
       }
+      fence_proxy_async();
       dk_sync_merge(&merge_bar, 1);
     }
     if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 3] = globaltimer_ns();  // all consumer warps done
     if (cs > 1) {
       cluster_wait();  // the other ranks' recv_bar are initialised
       if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 4] = globaltimer_ns();
-      const uint32_t rbase = smem_u32(recv);
+      const uint32_t rbase = smem_u32(recv), rbar = smem_u32(&recv_bar);
+      // one bulk shared -> shared copy per state owned by another rank
 #pragma unroll 1
-      for (int v = mth; v < nstate * Q4; v += kMergeThreads) {
-        const int i = v / Q4, q4 = v - i * Q4, owner = i % cs;
+      for (int i = mth; i < nstate; i += kMergeThreads) {
+        const int grp_i = i / cs, owner = i - grp_i * cs;
         if (owner == rank) continue;
-        const int slot = (i / cs) * (cs - 1) + (rank < owner ? rank : rank - 1);
-        const float4 x = reinterpret_cast<const float4*>(st + (size_t)i * SR)[q4];
-        st_async_f4(mapa(rbase + (uint32_t)(slot * SR + q4 * 4) * 4u, (uint32_t)owner), x,
-                    mapa(smem_u32(&recv_bar), (uint32_t)owner));
+        const int slot = grp_i * (cs - 1) + (rank < owner ? rank : rank - 1);
+        bulk_s2cluster(mapa(rbase + (uint32_t)(slot * SR) * 4u, (uint32_t)owner), smem_u32(st + (size_t)i * SR),
+                       (uint32_t)(SR * 4), mapa(rbar, (uint32_t)owner));
       }
       if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 5] = globaltimer_ns();  // pushes issued
       if (mth == 0) {
@@ -1060,24 +1085,28 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         mbar_arrive_expect_tx(&recv_bar, (uint32_t)(owned * (cs - 1) * SR * 4));
       }
       mbar_wait(&recv_bar, 0);
+      // every copy of ours landed once every rank's recv completed: phase 2
+      // of the cluster barrier (waited for at the end) keeps the sources alive
+      cluster_arrive_relaxed();
     }
     if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 1] = globaltimer_ns();  // merge start (copies arrived)
     // compact code on purpose: this runs once per CTA from a cold instruction
     // cache (ncu: the merge phase was bound by no_instruction stalls)
-    auto copy_of = [&](int i, int j) -> const float* {
-      return j == rank ? st + (size_t)i * SR : recv + (size_t)((i / cs) * (cs - 1) + (j < rank ? j : j - 1)) * SR;
-    };
 #pragma unroll 1
     for (int i = mw0; i < nstate; i += cs * (kMergeThreads / 32)) {
+      const float* rcv = recv + (size_t)(i / cs) * (cs - 1) * SR;  // the other ranks' copies, rank order
+      auto copy_of = [&](int j) -> const float* {
+        return j == rank ? st + (size_t)i * SR : rcv + (size_t)(j < rank ? j : j - 1) * SR;
+      };
       float M = -INFINITY, nsum = 0.f, acc[CPL];
 #pragma unroll 1
-      for (int j = 0; j < cs; ++j) M = fmaxf(M, copy_of(i, j)[D]);
+      for (int j = 0; j < cs; ++j) M = fmaxf(M, copy_of(j)[D]);
       if (tr && tid == kConsumer0 * 32 && i == mw0) tr[kTraceStride - 8] = globaltimer_ns() + (M > 1e30f);
 #pragma unroll
       for (int e = 0; e < CPL; ++e) acc[e] = 0.f;
 #pragma unroll 1
       for (int j = 0; j < cs; ++j) {  // Eqn 2, rank order
-        const float* r = copy_of(i, j);
+        const float* r = copy_of(j);
         const float w = r[D] == -INFINITY ? 0.f : fast_exp2(r[D] - M);
         nsum = fmaf(w, r[D + 1], nsum);
 #pragma unroll
@@ -1102,9 +1131,8 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     }
     if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 2] = globaltimer_ns();  // merge loop done (rank's states written)
   }
-  // warps 0-3 stay resident until the merge warps are done: an exited warp
-  // counts as arrived at the named barriers the merge warps use (bar 2)
-  __syncthreads();
+  // no CTA leaves while another rank's bulk copy may still read its states
+  if (cs > 1) cluster_wait();
   if (tr && tid == 0) tr[2] = globaltimer_ns();
 }
 
@@ -1195,6 +1223,7 @@ cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend&
     ly = dk_layout(p.dtype, p.c, D, t.dk_hg * t.dk_max_rows, cs, false, &smem);
   }
   ly.bulk1d = (a.dk_slots & 64) ? 0 : 1;
+  ly.diag_empty = (a.dk_slots & 128) ? 1 : 0;
   CUtensorMap mk{}, mv{};
   if (um && !pool_maps(p, D, kUmC, &mk, &mv)) return cudaErrorNotSupported;
   auto kern = um ? dk_kernel<T, TO, D, TPW, true> : dk_kernel<T, TO, D, TPW, false>;
