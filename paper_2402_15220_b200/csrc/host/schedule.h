@@ -60,8 +60,8 @@ enum DkFlags : int32_t {
   DK_FIRST = 1, DK_LAST = 2, DK_TAIL = 4, DK_PRIV = 8, DK_PACK = 16, DK_END = 32, DK_FINAL = 64, DK_SOLO = 128
 };
 constexpr int kDkUnitInts = 4;
-constexpr int kDkCtaInts = 16;    // {u0, u1, npre, 0, descriptors of the first npre <= kDkCtaPre units}
-constexpr int kDkCtaPre = 3;
+constexpr int kDkCtaInts = 32;    // {u0, u1, npre, 0, descriptors of the first npre <= kDkCtaPre units}
+constexpr int kDkCtaPre = 7;
 constexpr int kDkBlockInts = 4;
 constexpr int kDkMaxRows = 64;     // (head, row) states of one CTA: head-set size x block rows
 constexpr int kDkPack = 4;         // rows' last chunks dealt per pack (16-token slots of a c = 64 stage)

@@ -68,11 +68,11 @@ namespace {
 //     the CUDA-core GEMV ring for the private ones.
 // Registers are re-balanced per warpgroup with setmaxnreg.
 constexpr int kDkThreads = 12 * 32;
-constexpr int kRegsLow = 72, kRegsHigh = 216;            // mma.sync variant
-constexpr int kRegsSoftmax = 200, kRegsConsumerUm = 232;  // tcgen05 variant: 72 + 200 + 232 = 3 x 168
+constexpr int kRegsLow = 80, kRegsHigh = 208;            // mma.sync variant: 80 + 2 x 208 <= 3 x 168
+constexpr int kRegsLowUm = 80, kRegsSoftmax = 192, kRegsConsumerUm = 232;  // tcgen05 variant: 80 + 192 + 232 = 3 x 168
 constexpr int kDkMaxStages = 8;
 constexpr int kDkSlice = 32;                     // chunk-first token slice per warp and call (>= 32: latency)
-constexpr size_t kDkSmemBudget = 232448 - 2048;  // 227 KB opt-in, minus static shared memory
+constexpr size_t kDkSmemBudget = 232448 - 3328;  // 227 KB opt-in, minus static shared memory (<= 3 KB, ptxas)
 constexpr int kStateRows = kDkMaxRows;           // (head, row) states per CTA: hg * block rows <= 64
 constexpr int kMergeWarp0 = 4, kMergeThreads = 256;  // warps 4..11 run the final folds and the cluster merge
 // tcgen05 variant
@@ -158,6 +158,7 @@ struct DkLayout {
   uint32_t stage_bytes, cf_off;
   int32_t bulk1d;  // d = 64: K/V tiles by one 1-D bulk copy (the pool tile is already the SWIZZLE_128B image)
   int32_t diag_empty;  // DIAGNOSTIC ONLY (no output): every CTA returns at entry -- the launch's own cost
+  int32_t diag_nosf;   // DIAGNOSTIC ONLY (wrong output): the private-unit producer issues nothing
 };
 
 template <typename T, typename TO, int D, int TPW, bool UM>
@@ -195,8 +196,10 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   const int rank = (int)(blockIdx.x % (unsigned)cs), grp = (int)(blockIdx.x / (unsigned)cs);
   const int hsets = h / hg;
   const int head0 = (grp % hsets) * hg, blk = grp / hsets;
-  const int4 brec = *reinterpret_cast<const int4*>(t.dk_block + 4 * blk);  // {row0, rows}
-  const int brow0 = brec.x, brows = brec.y;
+  // the block's rows (schedule.cpp: balanced blocks of ceil(b / blocks) rows,
+  // = the dk_block record) -- arithmetic, no dependent load at entry
+  const int bper = (t.b + t.dk_blocks - 1) / t.dk_blocks;
+  const int brow0 = blk * bper, brows = min(bper, t.b - brow0);
   // CTA record: units [u0, u1), then the descriptors of its first kDkCtaPre units
   const int32_t* crp = t.dk_cta + (size_t)kDkCtaInts * (blk * cs + rank);
   const int4 crec = *reinterpret_cast<const int4*>(crp);
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   if (cs > 1) cluster_arrive_relaxed();
 
   if (warp < 4) {
-   regs_dec<kRegsLow>();
+   if constexpr (UM) regs_dec<kRegsLowUm>(); else regs_dec<kRegsLow>();
    if (warp == 0) {
     // ------------------------------------------------------------ producer
     // Stages: a chunk-first unit (mma.sync variant only), a cooperative
@@ -372,7 +375,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       if constexpr (!UM) issue_unit(dd.x, dd.y, dd.z, dd.w & 0xff, dd.w >> 8, 0, c);
       ++upre;
     }
-    for (int base = upre; base < u1; base += 32) {
+    for (int base = ly.diag_nosf ? u1 : upre; base < u1; base += 32) {
       const int u = base + lane;
       int4 d = make_int4(-1, 0, 0, 0);  // {chunk, row0, rows, flags | hh << 8}
       int caller = 0, nt = c, lenv = 0;
@@ -440,11 +443,18 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     pdl_wait();
     int k = 0;
     bool done = false;
-    for (int base = u0; base < u1 && !done; base += 32) {
+    // the first npre units come from the CTA record (loaded at entry), the
+    // rest in batches of 32 descriptors, one per lane
+    for (int base = u0, first = 1; base < u1 && !done; base += first ? npre : 32, first = 0) {
+      if (first && npre == 0) continue;
       const int u = base + lane;
       int4 d = make_int4(-1, 0, 0, DK_PRIV);
-      if (u < u1) d = *reinterpret_cast<const int4*>(u - u0 < npre ? crp + 4 + 4 * (u - u0) : t.dk_unit + 4 * (size_t)u);
-      const int cnt = min(32, u1 - base);
+      if (first) {
+        if (lane < npre) d = *reinterpret_cast<const int4*>(crp + 4 + 4 * lane);
+      } else if (u < u1) {
+        d = *reinterpret_cast<const int4*>(t.dk_unit + 4 * (size_t)u);
+      }
+      const int cnt = first ? npre : min(32, u1 - base);
       for (int i = 0; i < cnt; ++i, ++k) {
         const int i_chunk = __shfl_sync(0xffffffffu, d.x, i);
         const int i_row0 = __shfl_sync(0xffffffffu, d.y, i);
@@ -463,6 +473,8 @@ __global__ void __launch_bounds__(kDkThreads, 1)
               tr[3 + 4 * k] = globaltimer_ns();
               tr[6 + 4 * k] = 2 * kCfTile;
             }
+          } else if (tr && k < 14) {
+            tr[102 + k] = globaltimer_ns();  // V tile k issued
           }
           mbar_arrive_expect_tx(&fullb[s], kCfTile);
           const int y = (int)(layer_rows + ((int64_t)i_chunk * h + head0 + (i_word >> 8)) * kUmC);
@@ -500,15 +512,17 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     auto issue_pv = [&](int j, int fj) {
       const int b = j & 1, sv = j % nv;
       mbar_wait(&p_full[b], (uint32_t)((j >> 1) & 1));
+      if (tr && lane == 0 && j < 16) tr[86 + j] = globaltimer_ns();  // P_j in (issuer view)
       mbar_wait(&v_full[sv], (uint32_t)((j / nv) & 1));
       if ((fj & DK_FIRST) && jobs_done > 0) mbar_wait(&o_free, (uint32_t)((jobs_done - 1) & 1));
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t va = va0 + sv * kCfTile, pb = pa + b * kPImg;
+        // descriptors built once, advanced by constant address steps (>> 4)
+        const uint64_t da = umma_sdesc(pa + b * kPImg, 16, 1024), db = umma_sdesc(va0 + sv * kCfTile, kUmC * 128, 1024);
 #pragma unroll
         for (int ks = 0; ks < kUmC / 16; ++ks)
-          umma_f16(tmem + 2 * kUmC, umma_sdesc(pb + ks * 32, 16, 1024), umma_sdesc(va + ks * 16 * 128, kUmC * 128, 1024),
-                   idO, (!(fj & DK_FIRST) || ks > 0) ? 1u : 0u);
+          umma_f16(tmem + 2 * kUmC, da + (uint64_t)(ks * 32 >> 4), db + (uint64_t)(ks * 16 * 128 >> 4), idO,
+                   (!(fj & DK_FIRST) || ks > 0) ? 1u : 0u);
         umma_commit(&pv_done[b]);
         umma_commit(&v_empty[sv]);
         if (fj & DK_LAST) umma_commit(&o_ready);
@@ -536,15 +550,17 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       }
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t ka = ka0 + s * kCfTile;
+        if (tr && k == 3) tr[116] = globaltimer_ns();
+        const uint64_t dq = umma_sdesc(qa, 16, 1024), dk = umma_sdesc(ka0 + s * kCfTile, 16, 1024);
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {  // S = Q K^T over d
           const uint32_t o = (ks % 4) * 32;
-          umma_f16(tmem + b * kUmC, umma_sdesc(qa + (ks / 4) * kUmM * 128 + o, 16, 1024),
-                   umma_sdesc(ka + (ks / 4) * kUmC * 128 + o, 16, 1024), idS, ks > 0 ? 1u : 0u);
+          umma_f16(tmem + b * kUmC, dq + (uint64_t)(((ks / 4) * kUmM * 128 + o) >> 4),
+                   dk + (uint64_t)(((ks / 4) * kUmC * 128 + o) >> 4), idS, ks > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[b]);
         umma_commit(&k_empty[s]);
+        if (tr && k == 3) tr[117] = globaltimer_ns();
         if (tr && k == 0) tr[kTraceStride - 10] = globaltimer_ns();  // first S issued
       }
       __syncwarp();
@@ -598,9 +614,14 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       // MMAs (the only readers) completed before its last S_full
       constexpr int G = D / 8 / 2;  // 16-byte groups per lane half
       uint4 qv[G];
+      // speculative: the CTA's first job usually spans the whole block, so the
+      // caller index of this thread's Q row is loaded at entry
+      const int jspec = job_row(jr, brows);
+      const int cspec = jspec >= 0 ? t.row_caller[brow0 + jspec] : 0;
       auto load_q = [&](int row0, int nrows, int hh) {
         const int j = job_row(jr, nrows);
-        const T* qrow = j >= 0 ? q + ((size_t)t.row_caller[row0 + j] * h + head0 + hh) * D : nullptr;
+        const int caller = j < 0 ? 0 : (row0 == brow0 && nrows == brows) ? cspec : t.row_caller[row0 + j];
+        const T* qrow = j >= 0 ? q + ((size_t)caller * h + head0 + hh) * D : nullptr;
 #pragma unroll
         for (int e = 0; e < G; ++e)
           qv[e] = qrow ? *reinterpret_cast<const uint4*>(qrow + ((lane >> 4) * G + e) * 8) : make_uint4(0u, 0u, 0u, 0u);
@@ -618,11 +639,12 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       pdl_wait();  // q comes from the previous kernel
       // the CTA's first job from its record: its Q loads are in flight while
       // the chunk-first states are initialised and the first K/V tiles load
+      load_q(brow0, brows, 0);  // speculative: the whole block, head 0 of the set (the usual first job)
       bool qpre = false;
       if (npre > 0) {
         const int4 d0 = *reinterpret_cast<const int4*>(crp + 4);
         if (!(d0.w & DK_PRIV)) {
-          load_q(d0.y, d0.z, d0.w >> 8);
+          if (d0.y != brow0 || d0.z != brows || (d0.w >> 8) != 0) load_q(d0.y, d0.z, d0.w >> 8);
           qpre = true;
         }
       }
@@ -1098,19 +1120,31 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       auto copy_of = [&](int j) -> const float* {
         return j == rank ? st + (size_t)i * SR : rcv + (size_t)(j < rank ? j : j - 1) * SR;
       };
-      float M = -INFINITY, nsum = 0.f, acc[CPL];
-#pragma unroll 1
-      for (int j = 0; j < cs; ++j) M = fmaxf(M, copy_of(j)[D]);
+      // lane j holds copy j's (m, n): the max and the Eqn 2 weights by
+      // shuffles, then every lane sums its columns over the copies
+      float mj = -INFINITY, nj = 0.f;
+      if (lane < cs) {
+        const float2 mn = *reinterpret_cast<const float2*>(copy_of(lane) + D);
+        mj = mn.x;
+        nj = mn.y;
+      }
+      float M = mj;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      const float wl = mj == -INFINITY ? 0.f : fast_exp2(mj - M);
+      float nsum = wl * nj;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
       if (tr && tid == kConsumer0 * 32 && i == mw0) tr[kTraceStride - 8] = globaltimer_ns() + (M > 1e30f);
+      float acc[CPL];
 #pragma unroll
       for (int e = 0; e < CPL; ++e) acc[e] = 0.f;
-#pragma unroll 1
+#pragma unroll 4
       for (int j = 0; j < cs; ++j) {  // Eqn 2, rank order
-        const float* r = copy_of(j);
-        const float w = r[D] == -INFINITY ? 0.f : fast_exp2(r[D] - M);
-        nsum = fmaf(w, r[D + 1], nsum);
+        const float w = __shfl_sync(0xffffffffu, wl, j);
+        const float* r = copy_of(j) + lane * CPL;
 #pragma unroll
-        for (int e = 0; e < CPL; ++e) acc[e] = fmaf(w, r[lane * CPL + e], acc[e]);
+        for (int e = 0; e < CPL; ++e) acc[e] = fmaf(w, r[e], acc[e]);
       }
       const int hh = i / brows, row = brow0 + i % brows;
       const float inv = 1.f / nsum;
@@ -1224,6 +1258,7 @@ cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend&
   }
   ly.bulk1d = (a.dk_slots & 64) ? 0 : 1;
   ly.diag_empty = (a.dk_slots & 128) ? 1 : 0;
+  ly.diag_nosf = (a.dk_slots & 256) ? 1 : 0;
   CUtensorMap mk{}, mv{};
   if (um && !pool_maps(p, D, kUmC, &mk, &mv)) return cudaErrorNotSupported;
   auto kern = um ? dk_kernel<T, TO, D, TPW, true> : dk_kernel<T, TO, D, TPW, false>;

@@ -31,11 +31,11 @@ n = int((tr[:, 0] > 0).sum())
 t0 = tr[:n, 0][tr[:n, 0] > 0].min()
 rel = lambda x: np.where(x > 0, (x - t0) / 1e3, np.nan)
 marks = dict(entry=0, cons_done=1, end=2, firstQ=122, cf_epi=121, firstS=118, mergesync=119, allcons=125, clw=124,
-             pushed=123, mstart=127, firstld=120, loopdone=126)
+             pushed=123, mstart=127, firstld=120, loopdone=126, s3_issue0=116, s3_issue1=117)
 print("median over CTAs:", {k: round(float(np.nanmedian(rel(tr[:n, w]))), 2) for k, w in marks.items()})
-print("chunk-first unit k: producer start / issued / in smem (issuer) / S ready / P done  (CTA 0, then medians)")
-for k in range(16):
+print("chunk-first unit k: K issued / V issued / K in smem (issuer) / S ready / P done / P seen by issuer  (CTA 0 | medians)")
+for k in range(14):
     if tr[0, 3 + 4 * k] == 0:
         break
-    cols = [3 + 4 * k, 86 + k, 70 + k, 4 + 4 * k, 5 + 4 * k]
+    cols = [3 + 4 * k, 102 + k, 70 + k, 4 + 4 * k, 5 + 4 * k, 86 + k]
     print(k, " ".join(f"{rel(tr[0, c]):6.2f}" for c in cols), " | ", " ".join(f"{np.nanmedian(rel(tr[:n, c])):6.2f}" for c in cols))
