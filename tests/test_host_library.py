@@ -170,3 +170,20 @@ def test_configs_whose_stages_do_not_fit_are_rejected():
         with pytest.raises(C.ChunkAttnError):
             ChunkAttention(4, 128, c, 64, 8, 1024, dtype=dt, device=None)
     ChunkAttention(4, 128, 64, 64, 8, 1024, dtype=torch.float32, device=None)  # fits
+
+
+@pytest.mark.parametrize("question,umma,expect", [(0, 1, 1), (0, 0, 0), (0, 2, 1), (511, 1, 0), (511, 2, 1)])
+def test_k5_tcgen05_variant_selection(question, umma, expect):
+    """The K5 step takes the tcgen05 chunk-first variant (schedule_info
+    "dk_um") when the step's chunk-first units are at least half its full
+    private chunks (option dk_umma = 1, default), always with dk_umma = 2,
+    never with 0 -- cfg2 shape (32 x 128 fp16, c = 64, 32 rows sharing 2048
+    tokens), with a 1-token or a 512-token private tail per row."""
+    import torch
+    ca = ChunkAttention(32, 128, 64, 4096, 64, 8192, dtype=torch.float16, device=None)
+    ca.set_option("dk_umma", umma)
+    prompt = list(range(1, 2049))
+    ids = [ca.add_sequence(prompt + [5000 + 7 * r + t for t in range(question + 1)])[0] for r in range(32)]
+    ca.attend(ids)
+    info = ca.schedule_info()
+    assert info["dk"] == 1 and info["dk_um"] == expect
