@@ -247,7 +247,11 @@ chunkattn_status chunkattn_schedule_info(chunkattn_t h, int64_t out[9]);
  *   "dk_shared_fixed", "dk_shared_row", "dk_pack_fixed"  K5 work-split unit
  *                      costs (hundredths / thousandths; defaults 100, 10, 15)
  *   "dk_slots"         K5 tcgen05 variant: cap on its K + V ring slots (>= 4;
- *                      0 = default = as many as fit in shared memory)
+ *                      0 = default = as many as fit in shared memory).
+ *                      DIAGNOSTIC bits (wrong outputs, timing studies only):
+ *                      +64 2-D TMA also at d = 64, +128 every CTA returns at
+ *                      entry (launch cost), +256 no private units, +512 no
+ *                      UMMA issued, +1024 no softmax math
  *   "dk_umma"          K5's chunk-first units on the tcgen05 tensor cores
  *                      (16-bit, d in {64, 128}, c = 64; S and O in TMEM, K/V
  *                      by 2-D TMA): 1 (default) when the step's chunk-first
