@@ -251,7 +251,8 @@ chunkattn_status chunkattn_schedule_info(chunkattn_t h, int64_t out[9]);
  *                      DIAGNOSTIC bits (wrong outputs, timing studies only):
  *                      +64 2-D TMA also at d = 64, +128 every CTA returns at
  *                      entry (launch cost), +256 no private units, +512 no
- *                      UMMA issued, +1024 no softmax math
+ *                      UMMA issued, +1024 no softmax math, +2048 no P.V
+ *                      UMMA, +4096 no S UMMA
  *   "dk_umma"          K5's chunk-first units on the tcgen05 tensor cores
  *                      (16-bit, d in {64, 128}, c = 64; S and O in TMEM, K/V
  *                      by 2-D TMA): 1 (default) when the step's chunk-first

@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         const uint64_t da = umma_sdesc(pa + b * kPImg, 16, 1024), db = umma_sdesc(va0 + sv * kCfTile, kUmC * 128, 1024);
 #pragma unroll
         for (int ks = 0; ks < kUmC / 16; ++ks)
-          if (!(ly.diag_cf & 1)) umma_f16(tmem + 2 * kUmC, da + (uint64_t)(ks * 32 >> 4), db + (uint64_t)(ks * 16 * 128 >> 4), idO,
+          if (!(ly.diag_cf & 5)) umma_f16(tmem + 2 * kUmC, da + (uint64_t)(ks * 32 >> 4), db + (uint64_t)(ks * 16 * 128 >> 4), idO,
                    (!(fj & DK_FIRST) || ks > 0) ? 1u : 0u);
         umma_commit(&pv_done[b]);
         umma_commit(&v_empty[sv]);
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         const uint64_t dq = umma_sdesc(qa, 16, 1024), dk = umma_sdesc(ka0 + s * kCfTile, 16, 1024);
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {  // S = Q K^T over d
-          if (ly.diag_cf & 1) break;
+          if (ly.diag_cf & 9) break;
           const uint32_t o = (ks % 4) * 32;
           umma_f16(tmem + b * kUmC, dq + (uint64_t)(((ks / 4) * kUmM * 128 + o) >> 4),
                    dk + (uint64_t)(((ks / 4) * kUmC * 128 + o) >> 4), idS, ks > 0 ? 1u : 0u);
@@ -1261,7 +1261,7 @@ cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend&
   ly.bulk1d = (a.dk_slots & 64) ? 0 : 1;
   ly.diag_empty = (a.dk_slots & 128) ? 1 : 0;
   ly.diag_nosf = (a.dk_slots & 256) ? 1 : 0;
-  ly.diag_cf = (a.dk_slots >> 9) & 3;
+  ly.diag_cf = ((a.dk_slots >> 9) & 3) | ((a.dk_slots >> 9) & 12);  // +2048: no P.V UMMA, +4096: no S UMMA
   CUtensorMap mk{}, mv{};
   if (um && !pool_maps(p, D, kUmC, &mk, &mv)) return cudaErrorNotSupported;
   auto kern = um ? dk_kernel<T, TO, D, TPW, true> : dk_kernel<T, TO, D, TPW, false>;
