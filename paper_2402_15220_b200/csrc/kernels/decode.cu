@@ -490,12 +490,10 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         __syncwarp();
       }
     }
-    if (isk) {
-      const int s = k % nk;
-      if (k >= nk) mbar_wait(&k_empty[s], (uint32_t)(((k / nk) - 1) & 1));
+    if (isk && k == 0) {  // no chunk-first unit: an END stage (else the last unit carries DK_FINAL)
       if (lane == 0) {
-        cf_meta[s] = make_int4(DK_END, 0, 0, 0);
-        mbar_arrive_cta(&k_full[s]);
+        cf_meta[0] = make_int4(DK_END, 0, 0, 0);
+        mbar_arrive_cta(&k_full[0]);
       }
       __syncwarp();
     }
@@ -569,6 +567,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       if (pend >= 0) issue_pv(pend, pend_flags);
       pend = k;
       pend_flags = mk.x;
+      if (mk.x & DK_FINAL) break;  // the CTA's last chunk-first unit: its P V follows at once
     }
     if (pend >= 0) issue_pv(pend, pend_flags);
     // TMEM is released once the softmax warps have read the last job's O
@@ -807,6 +806,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
           ++jobs;
           if (tr && sct == 0) tr[kTraceStride - 7] = globaltimer_ns();  // job epilogue done
         }
+        if (mt.x & DK_FINAL) break;  // the CTA's last chunk-first unit
       }
     } else {
     // ----------------------------------------------------------- consumers

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests/test_gpu_decode.py -x -q 2>&1 | tail -2 > gpurun_out/r2ad_dec.txt
+timeout 300 python tools/rawtrace.py 10 > gpurun_out/r2ad_raw.txt 2>&1
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu --no-extras > gpurun_out/r2ad_bench.json 2>/dev/null
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu --no-extras > gpurun_out/r2ad_bench2.json 2>/dev/null
