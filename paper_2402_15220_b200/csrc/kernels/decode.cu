@@ -69,7 +69,7 @@ namespace {
 // Registers are re-balanced per warpgroup with setmaxnreg.
 constexpr int kDkThreads = 12 * 32;
 constexpr int kRegsLow = 80, kRegsHigh = 208;            // mma.sync variant: 80 + 2 x 208 <= 3 x 168
-constexpr int kRegsLowUm = 80, kRegsSoftmax = 192, kRegsConsumerUm = 232;  // tcgen05 variant: 80 + 192 + 232 = 3 x 168
+constexpr int kRegsLowUm = 80, kRegsSoftmax = 208, kRegsConsumerUm = 216;  // tcgen05 variant: 80 + 208 + 216 = 3 x 168
 constexpr int kDkMaxStages = 8;
 constexpr int kDkSlice = 32;                     // chunk-first token slice per warp and call (>= 32: latency)
 constexpr size_t kDkSmemBudget = 232448 - 3328;  // 227 KB opt-in, minus static shared memory (<= 3 KB, ptxas)
@@ -151,8 +151,8 @@ CA_DEV void fold_weights(float ms, float mj, float& M, float& ws, float& wj) {
 
 // Shared-memory layout (bytes from the dynamic base): SF ring [nst][stage] |
 // states [scap][SR] | (UM) chunk-first states [scap][SR] | recv area | (UM,
-// 1024-aligned at run time) K ring [nk][K image] | V ring [nv][V image] | Q
-// image | P images [2].
+// 1024-aligned at run time) K ring [nk][K image] | V ring [nv][V image].
+// TMEM (UM, 512 columns): S [2][64] | O [D] | P [2][32] (16-bit pairs) | Q [D / 2].
 struct DkLayout {
   int32_t nst, nk, nv, scap;
   uint32_t stage_bytes, cf_off;
@@ -176,8 +176,8 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   // tcgen05 variant geometry (c = 64)
   constexpr int HALVES = D / 64;                             // 128-byte d-halves of a token row
   constexpr uint32_t kCfTile = HALVES * kUmC * 128;          // one K (or V) SWIZZLE_128B image
-  constexpr uint32_t kQImg = HALVES * kUmM * 128;            // Q image, M = 64 rows
-  constexpr uint32_t kPImg = kUmM * 128;                     // P image (c = 64 tokens = one 128-byte atom)
+  constexpr uint32_t kTmemP = 4 * kUmC;                      // P buffers in TMEM: columns 256 + 32 b (16-bit pairs)
+  constexpr uint32_t kTmemQ = kTmemP + kUmC;                // Q in TMEM: D / 2 columns after the two P buffers
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[kDkMaxStages], empty_bar[kDkMaxStages];
   __shared__ DkMeta meta[kDkMaxStages];
@@ -213,8 +213,6 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   float* recv = (UM ? cst : st) + (size_t)ly.scap * SR;  // [owned state][other rank][SR]: pushed by the other ranks
   unsigned char* cfr = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + ly.cf_off + 1023) & ~uintptr_t(1023));  // UM: chunk-first ring
-  unsigned char* sQ = cfr + (size_t)(nk + nv) * kCfTile;
-  unsigned char* sP = sQ + kQImg;
   auto state_row = [&](int hh, int row) { return st + (size_t)(hh * brows + row - brow0) * SR; };
   // mode bit 0: scatter the step's new K/V row into each row's last chunk
   // (K1 folded in); bit 1: the lengths advance by one in this launch (the
@@ -258,7 +256,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   }
   if constexpr (UM) {
     if (warp == kIssuerWarp) {  // S double buffer (2 x 64 columns) + O (D columns) <= 256
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base)));
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -506,7 +504,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     // softmax warps through s_meta[k&1] (s_meta_full).
     const uint32_t tmem = tmem_base;
     constexpr uint32_t idS = umma_idesc<T, kUmM>(kUmC, false), idO = umma_idesc<T, kUmM>(D, true);
-    const uint32_t qa = smem_u32(sQ), pa = smem_u32(sP), ka0 = smem_u32(cfr), va0 = ka0 + nk * kCfTile;
+    const uint32_t ka0 = smem_u32(cfr), va0 = ka0 + nk * kCfTile;
     int jobs_q = 0, jobs_done = 0, pend = -1, pend_flags = 0;
     auto issue_pv = [&](int j, int fj) {
       const int b = j & 1, sv = j % nv;
@@ -516,12 +514,15 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       if ((fj & DK_FIRST) && jobs_done > 0) mbar_wait(&o_free, (uint32_t)((jobs_done - 1) & 1));
       tc_fence_after();
       if (lane == 0) {
-        // descriptors built once, advanced by constant address steps (>> 4)
-        const uint64_t da = umma_sdesc(pa + b * kPImg, 16, 1024), db = umma_sdesc(va0 + sv * kCfTile, kUmC * 128, 1024);
+        // A = P from TMEM (8 columns = 16 tokens per step), B = V from shared
+        // memory (descriptor advanced by constant address steps, >> 4)
+        const uint64_t db = umma_sdesc(va0 + sv * kCfTile, kUmC * 128, 1024);
+        const uint32_t tp = tmem + kTmemP + (uint32_t)(b * (kUmC / 2));
 #pragma unroll
         for (int ks = 0; ks < kUmC / 16; ++ks)
-          if (!(ly.diag_cf & 5)) umma_f16(tmem + 2 * kUmC, da + (uint64_t)(ks * 32 >> 4), db + (uint64_t)(ks * 16 * 128 >> 4), idO,
-                   (!(fj & DK_FIRST) || ks > 0) ? 1u : 0u);
+          if (!(ly.diag_cf & 5))
+            umma_f16_ta(tmem + 2 * kUmC, tp + (uint32_t)(ks * 8), db + (uint64_t)(ks * 16 * 128 >> 4), idO,
+                        (!(fj & DK_FIRST) || ks > 0) ? 1u : 0u);
         umma_commit(&pv_done[b]);
         umma_commit(&v_empty[sv]);
         if (fj & DK_LAST) umma_commit(&o_ready);
@@ -550,13 +551,14 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       tc_fence_after();
       if (lane == 0) {
         if (tr && k == 3) tr[116] = globaltimer_ns();
-        const uint64_t dq = umma_sdesc(qa, 16, 1024), dk = umma_sdesc(ka0 + s * kCfTile, 16, 1024);
+        const uint64_t dk = umma_sdesc(ka0 + s * kCfTile, 16, 1024);
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {  // S = Q K^T over d
           if (ly.diag_cf & 9) break;
           const uint32_t o = (ks % 4) * 32;
-          umma_f16(tmem + b * kUmC, dq + (uint64_t)(((ks / 4) * kUmM * 128 + o) >> 4),
-                   dk + (uint64_t)(((ks / 4) * kUmC * 128 + o) >> 4), idS, ks > 0 ? 1u : 0u);
+          // A = Q from TMEM (8 columns = 16 elements of d per step), B = K tile
+          umma_f16_ta(tmem + b * kUmC, tmem + kTmemQ + (uint32_t)(ks * 8), dk + (uint64_t)(((ks / 4) * kUmC * 128 + o) >> 4),
+                      idS, ks > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[b]);
         umma_commit(&k_empty[s]);
@@ -573,7 +575,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     // TMEM is released once the softmax warps have read the last job's O
     if (jobs_done > 0) mbar_wait(&o_free, (uint32_t)((jobs_done - 1) & 1));
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
    }
    if (cs > 1) {
      cluster_wait();            // the cluster barrier phase begun at entry
@@ -600,7 +602,6 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       // per job: O from TMEM folded into the (head, row) chunk-first states
       // (Eqn 2).
       const int qd = warp - kSoftmaxWarp0;  // TMEM lane quadrant
-      const int jr = qd * 16 + (lane & 15);  // Q image (M) row written by this thread
       const int m0 = qd * 16 + (lane >> 2), c0 = 2 * (lane & 3);
       const uint32_t tmem = tmem_base;
       const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
@@ -611,29 +612,35 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         const int j = nrows > 32 ? m : ((m & 15) < 8 ? (m >> 4) * 8 + (m & 7) : -1);
         return j < nrows ? j : -1;
       };
-      // Q image of a job's rows (unused M rows zero); the previous job's S
-      // MMAs (the only readers) completed before its last S_full
-      constexpr int G = D / 8 / 2;  // 16-byte groups per lane half
-      uint4 qv[G];
+      // Q of a job's rows into TMEM, the A operand of S (unused M rows zero):
+      // thread t provides, for M rows m0 and m0 + 8, the packed pairs of d =
+      // 8 j + 2 (t % 4), + 1 -- the .16x128b store shape puts them at column
+      // 4 j + t % 4 of the rows' lanes, the A layout.  The previous job's S
+      // MMAs (the only readers) completed before its last S_full.
+      constexpr int QJ = D / 8;
+      uint32_t qv[2 * QJ];
       // speculative: the CTA's first job usually spans the whole block, so the
-      // caller index of this thread's Q row is loaded at entry
-      const int jspec = job_row(jr, brows);
-      const int cspec = jspec >= 0 ? t.row_caller[brow0 + jspec] : 0;
+      // caller indices of this thread's Q rows are loaded at entry
+      const int js0 = job_row(m0, brows), js1 = job_row(m0 + 8, brows);
+      const int cs0 = js0 >= 0 ? t.row_caller[brow0 + js0] : 0, cs1 = js1 >= 0 ? t.row_caller[brow0 + js1] : 0;
       auto load_q = [&](int row0, int nrows, int hh) {
-        const int j = job_row(jr, nrows);
-        const int caller = j < 0 ? 0 : (row0 == brow0 && nrows == brows) ? cspec : t.row_caller[row0 + j];
-        const T* qrow = j >= 0 ? q + ((size_t)caller * h + head0 + hh) * D : nullptr;
 #pragma unroll
-        for (int e = 0; e < G; ++e)
-          qv[e] = qrow ? *reinterpret_cast<const uint4*>(qrow + ((lane >> 4) * G + e) * 8) : make_uint4(0u, 0u, 0u, 0u);
+        for (int hf = 0; hf < 2; ++hf) {
+          const int j = job_row(m0 + 8 * hf, nrows);
+          const int caller = j < 0 ? 0 : (row0 == brow0 && nrows == brows) ? (hf ? cs1 : cs0) : t.row_caller[row0 + j];
+          const uint32_t* qrow =
+              j >= 0 ? reinterpret_cast<const uint32_t*>(q + ((size_t)caller * h + head0 + hh) * D) : nullptr;
+#pragma unroll
+          for (int jj = 0; jj < QJ; ++jj) qv[2 * jj + hf] = qrow ? qrow[4 * jj + (lane & 3)] : 0u;
+        }
       };
       auto store_q = [&]() {
-#pragma unroll
-        for (int e = 0; e < G; ++e) {
-          const int gg = (lane >> 4) * G + e;
-          *reinterpret_cast<uint4*>(sQ + (gg / 8) * kUmM * 128 + sw128(jr, gg % 8)) = qv[e];
-        }
-        fence_proxy_async();
+        if constexpr (QJ == 16)
+          tmem_st16x128_x16(tmem + kTmemQ + lane_base, qv);
+        else
+          tmem_st16x128_x8(tmem + kTmemQ + lane_base, qv);
+        tmem_wait_st();
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cta(&q_full);
       };
@@ -654,7 +661,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       asm volatile("bar.sync 3, 128;" ::: "memory");  // chunk-first states initialised
       if (qpre) {
         store_q();
-        if (tr && sct == 0) tr[kTraceStride - 6] = globaltimer_ns();  // first Q image written
+        if (tr && sct == 0) tr[kTraceStride - 6] = globaltimer_ns();  // first Q in TMEM
       }
       float m_ref[2] = {-INFINITY, -INFINITY}, n[2] = {0.f, 0.f};  // M rows m0, m0 + 8 (n: this thread's columns)
       int crow0 = 0, cnrows = 0, chh = 0, jobs = 0, nh = 2;
@@ -730,7 +737,12 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         }
         // P = exp2(s - m_ref) rounded to T (n from the rounded P, reading A11)
         if (k >= 2) mbar_wait(&pv_done[b], (uint32_t)(((k >> 1) - 1) & 1));  // P V_{k-2} read this buffer
-        unsigned char* pb = sP + b * kPImg;
+        // P -> TMEM (the A operand of P V): the .16x128b shape puts this
+        // thread's packed pair (row m0 (+8), tokens 8j + c0, +1) at column
+        // 4j + t % 4 of its row's lane -- exactly the A layout
+        uint32_t pw[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pw[i] = 0u;
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           if (hf >= nh || (ly.diag_cf & 2)) break;
@@ -741,11 +753,13 @@ __global__ void __launch_bounds__(kDkThreads, 1)
                                             fast_exp2(fmaf(__uint_as_float(u[4 * j + 2 * hf + 1]), scale_log2, -m_ref[hf])));
             const float2 f2 = Mma<T>::unpack(w);
             if (j & 1) ns1 += f2.x + f2.y; else ns0 += f2.x + f2.y;
-            *reinterpret_cast<uint32_t*>(pb + sw128(m0 + 8 * hf, j) + c0 * 2) = w;
+            pw[2 * j + hf] = w;
           }
           n[hf] += ns0 + ns1;
         }
-        fence_proxy_async();
+        tmem_st16x128_x8(tmem + kTmemP + (uint32_t)(b * (kUmC / 2)) + lane_base, pw);
+        tmem_wait_st();
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cta(&p_full[b]);
         if (tr && sct == 0 && k < 16) tr[5 + 4 * k] = globaltimer_ns();
@@ -1232,9 +1246,9 @@ DkLayout dk_layout(int32_t dtype, int32_t c, int32_t d, int32_t nstate, int32_t 
     return L;
   }
   L.scap = nstate;
-  const size_t tile = (size_t)(d / 64) * kUmC * 128, q_img = (size_t)(d / 64) * kUmM * 128, p_img = (size_t)kUmM * 128;
+  const size_t tile = (size_t)(d / 64) * kUmC * 128;  // Q and P live in TMEM
   const size_t recv = dk_recv_bytes(d, nstate, cs);
-  const size_t fixed = 2 * state_bytes(d, nstate) + recv + 1024 + q_img + 2 * p_img + L.stage_bytes;
+  const size_t fixed = 2 * state_bytes(d, nstate) + recv + 1024 + L.stage_bytes;
   *smem = 0;
   if (fixed + 4 * tile > kDkSmemBudget) return L;
   int slots = (int)std::min<size_t>(2 * kUmMaxCf, (kDkSmemBudget - fixed) / tile);
@@ -1243,7 +1257,7 @@ DkLayout dk_layout(int32_t dtype, int32_t c, int32_t d, int32_t nstate, int32_t 
   L.nv = std::min(3, slots / 2);                  // V slots wait for P V: K slots come free sooner
   L.nk = std::min(kUmMaxCf, slots - L.nv);
   L.cf_off = (uint32_t)(L.nst * L.stage_bytes + 2 * state_bytes(d, nstate) + recv);
-  *smem = L.cf_off + 1024 + (L.nk + L.nv) * tile + q_img + 2 * p_img;
+  *smem = L.cf_off + 1024 + (L.nk + L.nv) * tile;
   return L;
 }
 
