@@ -417,6 +417,50 @@ bool pool_maps(const PoolGeom& p, int D, int C, CUtensorMap* mk, CUtensorMap* mv
 }
 
 namespace {
+// 3-D view of a d = 128 pool: {64 elements, rows (stride d * 2 bytes), 2
+// d-halves (stride 128 bytes)}; a box {64, c, 2} lands as [half][row][128 B]
+// -- both SWIZZLE_128B images of a (chunk, head) tile in ONE TMA op
+bool encode_map3(const void* base, int64_t rows, int c, CUtensorMap* out) {
+  static std::mutex mu;
+  static std::map<MapKey, CUtensorMap> cache;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  const MapKey key{base, rows, 128, c};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q{};
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {64, (cuuint64_t)rows, 2};
+  const cuuint64_t strides[2] = {256, 128};
+  const cuuint32_t box[3] = {64, (cuuint32_t)c, 2};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  if (encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  cache[key] = m;
+  *out = m;
+  return true;
+}
+}  // namespace
+
+bool pool_maps3(const PoolGeom& p, int C, CUtensorMap* mk, CUtensorMap* mv) {
+  if (p.d != 128) return false;
+  const int64_t rows = (int64_t)p.num_layers * p.max_chunks * p.h * p.c;
+  return encode_map3(p.k, rows, C, mk) && encode_map3(p.v, rows, C, mv);
+}
+
+namespace {
 
 template <typename T, int D, int C>
 cudaError_t launch_t(const AttnLaunch& a, const DevTables& t, cudaStream_t st) {

@@ -157,6 +157,7 @@ struct DkLayout {
   int32_t nst, nk, nv, scap;
   uint32_t stage_bytes, cf_off;
   int32_t bulk1d;  // d = 64: K/V tiles by one 1-D bulk copy (the pool tile is already the SWIZZLE_128B image)
+  int32_t map3;        // d = 128: the maps are 3-D (one TMA op per tile)
   int32_t diag_empty;  // DIAGNOSTIC ONLY (no output): every CTA returns at entry -- the launch's own cost
   int32_t diag_nosf;   // DIAGNOSTIC ONLY (wrong output): the private-unit producer issues nothing
   int32_t diag_cf;     // DIAGNOSTIC ONLY (wrong output): bit 0 no UMMA issued, bit 1 no softmax math
@@ -221,6 +222,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   // debug timeline (option "trace"): kernel_timeline.py layout (kernels.h)
   uint64_t* tr = trace && blockIdx.x < kTraceCtas ? trace + (size_t)blockIdx.x * kTraceStride : nullptr;
   if (tr && tid == 0) tr[0] = globaltimer_ns();
+  if (tr && tid == 32) tr[115] = (uint64_t)(npre + 100 * ly.nk + 10000 * ly.nv);  // layout probe (trace only)
   if (ly.diag_empty) return;
 
   if (tid == 0) {
@@ -478,7 +480,9 @@ __global__ void __launch_bounds__(kDkThreads, 1)
           mbar_arrive_expect_tx(&fullb[s], kCfTile);
           const int y = (int)(layer_rows + ((int64_t)i_chunk * h + head0 + (i_word >> 8)) * kUmC);
           unsigned char* stg = ring + (size_t)s * kCfTile;
-          if (HALVES == 1 && ly.bulk1d)
+          if (HALVES == 2 && ly.map3)
+            tma_load_3d(stg, map, 0, y, 0, &fullb[s]);
+          else if (HALVES == 1 && ly.bulk1d)
             bulk_g2s(stg, (isk ? kpool : vpool) + ((size_t)i_chunk * h + head0 + (i_word >> 8)) * kUmC * D, kCfTile,
                      &fullb[s]);
           else
@@ -1235,7 +1239,7 @@ size_t state_bytes(int32_t d, int32_t n) { return (size_t)n * (d + 4) * 4; }
 // Shared-memory layout of a launch (kernel comment "DkLayout") and its size;
 // nk = 0 when the tcgen05 variant does not fit.
 DkLayout dk_layout(int32_t dtype, int32_t c, int32_t d, int32_t nstate, int32_t cs, bool um, size_t* smem,
-                   int max_slots = 0) {
+                   int max_slots = 0, int vslots = 0) {
   DkLayout L{};
   L.stage_bytes = (uint32_t)dk_stage_bytes(dtype, c, d);
   if (!um) {
@@ -1254,7 +1258,7 @@ DkLayout dk_layout(int32_t dtype, int32_t c, int32_t d, int32_t nstate, int32_t 
   int slots = (int)std::min<size_t>(2 * kUmMaxCf, (kDkSmemBudget - fixed) / tile);
   if (max_slots >= 4) slots = std::min(slots, max_slots);
   L.nst = 1;
-  L.nv = std::min(3, slots / 2);                  // V slots wait for P V: K slots come free sooner
+  L.nv = vslots > 0 ? std::min(vslots, slots - 2) : std::min(3, slots / 2);  // V slots wait for P V: K slots come free sooner
   L.nk = std::min(kUmMaxCf, slots - L.nv);
   L.cf_off = (uint32_t)(L.nst * L.stage_bytes + 2 * state_bytes(d, nstate) + recv);
   *smem = L.cf_off + 1024 + (L.nk + L.nv) * tile;
@@ -1267,7 +1271,7 @@ cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend&
   const int cs = t.dk_cs;
   bool um = t.dk_um != 0 && dk_umma_supported(p);
   size_t smem = 0;
-  DkLayout ly = dk_layout(p.dtype, p.c, D, t.dk_hg * t.dk_max_rows, cs, um, &smem, a.dk_slots & 63);
+  DkLayout ly = dk_layout(p.dtype, p.c, D, t.dk_hg * t.dk_max_rows, cs, um, &smem, a.dk_slots & 63, (a.dk_slots >> 15) & 7);
   if (um && ly.nk < 2) {
     um = false;
     ly = dk_layout(p.dtype, p.c, D, t.dk_hg * t.dk_max_rows, cs, false, &smem);
@@ -1277,7 +1281,13 @@ cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend&
   ly.diag_nosf = (a.dk_slots & 256) ? 1 : 0;
   ly.diag_cf = ((a.dk_slots >> 9) & 3) | ((a.dk_slots >> 9) & 12);  // +2048: no P.V UMMA, +4096: no S UMMA
   CUtensorMap mk{}, mv{};
-  if (um && !pool_maps(p, D, kUmC, &mk, &mv)) return cudaErrorNotSupported;
+  ly.map3 = 0;
+  if (um) {
+    if (D == 128 && !(a.dk_slots & 16384) && pool_maps3(p, kUmC, &mk, &mv))
+      ly.map3 = 1;
+    else if (!pool_maps(p, D, kUmC, &mk, &mv))
+      return cudaErrorNotSupported;
+  }
   auto kern = um ? dk_kernel<T, TO, D, TPW, true> : dk_kernel<T, TO, D, TPW, false>;
   cudaError_t e = dk_prepare((const void*)kern, kDkSmemBudget);
   if (e != cudaSuccess) return e;

@@ -97,6 +97,9 @@ bool dk_supported(const PoolGeom& pool);
 // 2-D TMA views of the K / V pools (boxes of 64 elements x c rows; the pool
 // rows are XOR pre-swizzled, so a box lands as SWIZZLE_128B atoms), cached
 bool pool_maps(const PoolGeom& p, int D, int C, CUtensorMap* mk, CUtensorMap* mv);
+// d = 128 only: 3-D views {64, rows, 2 halves} so one box moves a whole tile as
+// its two SWIZZLE_128B images (false if the driver rejects the map)
+bool pool_maps3(const PoolGeom& p, int C, CUtensorMap* mk, CUtensorMap* mv);
 size_t dk_stage_bytes(int32_t dtype, int32_t c, int32_t d);
 size_t dk_state_bytes(int32_t d);
 size_t dk_recv_bytes(int32_t d, int32_t nstate, int32_t cs);
