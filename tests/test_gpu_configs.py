@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 
 # ------------------------------------------------------- configs[2]: sweep ---
-@pytest.mark.parametrize("opts", ["", "dk=0"])
+@pytest.mark.parametrize("opts", ["", "dk=0", "dk_umma=2"])
 @pytest.mark.parametrize("b", [8, 32])
 @pytest.mark.parametrize("n_s", [0, 2048, 4096])
 def test_config3_sweep_point_all_rows(n_s, b, opts):
@@ -25,12 +25,14 @@ def test_config3_sweep_point_all_rows(n_s, b, opts):
     attend; the two-call path for dk=0): every row and head against C1."""
     if opts == "dk=0" and b == 8 and n_s == 2048:
         pytest.skip("covered by the neighbouring points")
+    if opts == "dk_umma=2" and n_s == 0:
+        pytest.skip("no chunk-first unit: the tcgen05 variant is not taken")
     hs = Harness(32, 128, 64, "f16", "f16", seed=31 + n_s // 1024, alpha=8.0,
                  max_chunks=b * 66 + 80, max_batch=64, max_seq_len=4200, opts=opts)
     ids = build_shared(hs, n_s, [4096 - n_s] * b)
     hs.step = 1
     toks = decode_tokens(hs, ids)
-    if opts:
+    if opts.startswith("dk=0"):
         hs.append(ids, toks)
         hs.check(ids, 2e-3)
     else:
@@ -38,8 +40,11 @@ def test_config3_sweep_point_all_rows(n_s, b, opts):
 
 
 # ----------------------------------------- configs[3]: two-level tree, real ---
-def test_config4_two_level_tree_real_shape():
-    """BASELINE configs[3] at its real shape: 32 heads x 128, chunk 64, a
+@pytest.mark.parametrize("umma", [1, 2])
+def test_config4_two_level_tree_real_shape(umma):
+    """BASELINE configs[3] at its real shape (chunk-first units on the
+    auto-selected variant, and forced onto tcgen05: CTAs with several jobs --
+    the system run and group runs): 32 heads x 128, chunk 64, a
     1024-token system prompt shared by all 64 rows, 4 groups x 16 rows sharing
     1024 tokens of examples, questions of 1..63 tokens, 512 fused decode steps
     with completion targets U[64, 512]: a finished sequence is removed (evict)
@@ -49,7 +54,7 @@ def test_config4_two_level_tree_real_shape():
     rng = random.Random(4)
     c, H, steps = 64, 32, 512
     hs = Harness(H, 128, c, "f16", "f16", seed=4, alpha=8.0, max_chunks=16 + 64 + 64 * 12 + 64,
-                 max_batch=64, max_seq_len=4096)
+                 max_batch=64, max_seq_len=4096, opts=f"dk_umma={umma}")
     tm = TreeModel(c, 16 + 64 + 64 * 12 + 64)
     sys_p = synth.token_ids(4, synth.TAG_SYS, 0, 1024).tolist()
     groups = [synth.token_ids(4, synth.TAG_GROUP, g, 1024).tolist() for g in range(4)]
