@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[kDkMaxStages], empty_bar[kDkMaxStages];
   __shared__ DkMeta meta[kDkMaxStages];
-  __shared__ uint64_t recv_bar;  // the other ranks' copies of this rank's merge states have arrived
+  __shared__ uint64_t recv_bar[kDkMaxCluster];  // rank r's copies of this rank's merge states have arrived
   __shared__ uint64_t merge_bar;  // warps 4..11 done with their units (phase 0) / the state folds (phase 1)
   // tcgen05 variant: chunk-first ring, MMA / softmax hand-offs
   __shared__ uint64_t k_full[UM ? kUmMaxCf : 1], k_empty[UM ? kUmMaxCf : 1];
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       mbar_init(&full_bar[s], 1);  // producer: expected bytes per copy, then one arrive with the metadata
       mbar_init(&empty_bar[s], NC);
     }
-    mbar_init(&recv_bar, 1);
+    for (int r = 0; r < cs; ++r) mbar_init(&recv_bar[r], 1);
     mbar_init(&merge_bar, kMergeThreads / 32);
     if constexpr (UM) {
       for (int s = 0; s < nk; ++s) {
@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     if (cs > 1) {
       cluster_wait();  // the other ranks' recv_bar are initialised
       if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 4] = globaltimer_ns();
-      const uint32_t rbase = smem_u32(recv), rbar = smem_u32(&recv_bar);
+      const uint32_t rbase = smem_u32(recv), rbar = smem_u32(&recv_bar[rank]);
       // one bulk shared -> shared copy per state owned by another rank
 #pragma unroll 1
       for (int i = mth; i < nstate; i += kMergeThreads) {
@@ -1122,50 +1122,38 @@ __global__ void __launch_bounds__(kDkThreads, 1)
                        (uint32_t)(SR * 4), mapa(rbar, (uint32_t)owner));
       }
       if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 5] = globaltimer_ns();  // pushes issued
-      if (mth == 0) {
+      if (mth < cs && mth != rank) {  // each other rank's share of copies completes its own barrier
         const int owned = (nstate - rank + cs - 1) / cs;
-        mbar_arrive_expect_tx(&recv_bar, (uint32_t)(owned * (cs - 1) * SR * 4));
+        mbar_arrive_expect_tx(&recv_bar[mth], (uint32_t)(owned * SR * 4));
       }
-      mbar_wait(&recv_bar, 0);
-      // every copy of ours landed once every rank's recv completed: phase 2
-      // of the cluster barrier (waited for at the end) keeps the sources alive
-      cluster_arrive_relaxed();
     }
-    if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 1] = globaltimer_ns();  // merge start (copies arrived)
-    // compact code on purpose: this runs once per CTA from a cold instruction
-    // cache (ncu: the merge phase was bound by no_instruction stalls)
+    if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 1] = globaltimer_ns();  // merge start (pushes issued)
+    // Eqn 2 folds in rank order, each copy as soon as its rank's pushes have
+    // landed: after the last arrival only one fold and O / n remain
 #pragma unroll 1
     for (int i = mw0; i < nstate; i += cs * (kMergeThreads / 32)) {
       const float* rcv = recv + (size_t)(i / cs) * (cs - 1) * SR;  // the other ranks' copies, rank order
-      auto copy_of = [&](int j) -> const float* {
-        return j == rank ? st + (size_t)i * SR : rcv + (size_t)(j < rank ? j : j - 1) * SR;
-      };
-      // lane j holds copy j's (m, n): the max and the Eqn 2 weights by
-      // shuffles, then every lane sums its columns over the copies
-      float mj = -INFINITY, nj = 0.f;
-      if (lane < cs) {
-        const float2 mn = *reinterpret_cast<const float2*>(copy_of(lane) + D);
-        mj = mn.x;
-        nj = mn.y;
-      }
-      float M = mj;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-      const float wl = mj == -INFINITY ? 0.f : fast_exp2(mj - M);
-      float nsum = wl * nj;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-      if (tr && tid == kConsumer0 * 32 && i == mw0) tr[kTraceStride - 8] = globaltimer_ns() + (M > 1e30f);
-      float acc[CPL];
+      float acc[CPL], M = -INFINITY, nsum = 0.f;
 #pragma unroll
       for (int e = 0; e < CPL; ++e) acc[e] = 0.f;
-#pragma unroll 4
-      for (int j = 0; j < cs; ++j) {  // Eqn 2, rank order
-        const float w = __shfl_sync(0xffffffffu, wl, j);
-        const float* r = copy_of(j) + lane * CPL;
+#pragma unroll 1
+      for (int j = 0; j < cs; ++j) {
+        const float* r;
+        if (j == rank) {
+          r = st + (size_t)i * SR;
+        } else {
+          mbar_wait(&recv_bar[j], 0);
+          r = rcv + (size_t)(j < rank ? j : j - 1) * SR;
+        }
+        const float2 mn = *reinterpret_cast<const float2*>(r + D);
+        float Mn, wa, wj;
+        fold_weights(M, mn.x, Mn, wa, wj);
+        nsum = fmaf(wj, mn.y, nsum * wa);
 #pragma unroll
-        for (int e = 0; e < CPL; ++e) acc[e] = fmaf(w, r[e], acc[e]);
+        for (int e = 0; e < CPL; ++e) acc[e] = fmaf(wj, r[lane * CPL + e], acc[e] * wa);
+        M = Mn;
       }
+      if (tr && tid == kConsumer0 * 32 && i == mw0) tr[kTraceStride - 8] = globaltimer_ns() + (M > 1e30f);
       const int hh = i / brows, row = brow0 + i % brows;
       const float inv = 1.f / nsum;
       const int caller = i == mw0 ? mcaller : t.row_caller[row];
@@ -1184,6 +1172,13 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       }
     }
     if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 2] = globaltimer_ns();  // merge loop done (rank's states written)
+    if (cs > 1) {
+      // every copy of ours landed once every rank's recv completed: phase 2
+      // of the cluster barrier (waited for at the end) keeps the sources alive
+      for (int r = 0; r < cs; ++r)
+        if (r != rank) mbar_wait(&recv_bar[r], 0);
+      cluster_arrive_relaxed();
+    }
   }
   // no CTA leaves while another rank's bulk copy may still read its states
   if (cs > 1) cluster_wait();

@@ -34,6 +34,7 @@ marks = dict(entry=0, cons_done=1, end=2, firstQ=122, cf_epi=121, firstS=118, me
              pushed=123, mstart=127, firstld=120, loopdone=126, s3_issue0=116, s3_issue1=117)
 print("CTA0 npre + 100 nk + 10000 nv:", tr[0, 115], " CTA1:", tr[1, 115])
 print("median over CTAs:", {k: round(float(np.nanmedian(rel(tr[:n, w]))), 2) for k, w in marks.items()})
+print("max over CTAs:", {k: round(float(np.nanmax(rel(tr[:n, w]))), 2) for k, w in marks.items()})
 print("chunk-first unit k: K issued / V issued / K in smem (issuer) / S ready / P done / P seen by issuer  (CTA 0 | medians)")
 for k in range(14):
     if tr[0, 3 + 4 * k] == 0:
