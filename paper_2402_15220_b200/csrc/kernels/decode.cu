@@ -79,7 +79,7 @@ constexpr int kMergeWarp0 = 4, kMergeThreads = 256;  // warps 4..11 run the fina
 constexpr int kUmC = 64;                 // chunk size of the variant
 constexpr int kUmM = 64;                 // UMMA M (rows of a K5 block <= 64)
 constexpr int kUmMaxCf = 5;              // K (and V) ring depth cap
-constexpr int kCfProducerWarp = 1, kIssuerWarp = 2, kVProducerWarp = 3, kSoftmaxWarp0 = 4;
+constexpr int kCfProducerWarp = 1, kIssuerWarp = 2, kPvIssuerWarp = 3, kSoftmaxWarp0 = 4;
 constexpr float kRescaleLog2 = 8.f;      // lazy O rescale threshold (P <= 2^8), as chunk_first_umma.cu
 
 template <bool UM>
@@ -189,7 +189,8 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   __shared__ uint64_t v_full[UM ? kUmMaxCf : 1], v_empty[UM ? kUmMaxCf : 1];
   __shared__ int4 cf_meta[UM ? kUmMaxCf : 1];  // K slot's unit {flags, row0, rows, head of the set}
   __shared__ int4 s_meta[2];                   // the unit of S buffer b (issuer -> softmax)
-  __shared__ uint64_t s_full[2], s_free[2], s_meta_full[2], p_full[2], pv_done[2], q_full, o_ready, o_free;
+  __shared__ uint64_t s_full[2], s_free[2], s_meta_full[2], p_full[2], pv_done[2], q_full, o_ready, o_free, tm_done;
+  __shared__ int pv_flags[2];                  // the unit flags of P buffer b (softmax -> P V issuer)
   __shared__ uint32_t tmem_base;
   __shared__ uint64_t sf_done;  // UM: the private-unit consumers are done with the states
   __shared__ int cf_direct;     // UM: the CTA's one chunk-first job was folded straight into the states
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       mbar_init(&q_full, 4);
       mbar_init(&o_ready, 1);
       mbar_init(&o_free, 4);
+      mbar_init(&tm_done, 1);
       mbar_init(&sf_done, DkRoles<UM>::NC);
       cf_direct = 0;
     }
@@ -426,24 +428,32 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     const int s = acquire();
     if (lane == 0) meta[s].flags = DK_END;
     publish(s, 0);
-   } else if (UM && (warp == kCfProducerWarp || warp == kVProducerWarp)) {
-    // ----------------------------------- chunk-first TMA producers (K, V)
-    // The CTA's chunk-first units (they precede its private ones): warp 1
-    // loads K tiles into the K ring (released after S), warp 3 V tiles into
-    // the V ring (released after P V), each a 2-D box of 64 elements x 64
-    // rows per d-half -- the pool rows are XOR pre-swizzled within each
-    // 128-byte half, so the boxes land as canonical SWIZZLE_128B atoms.  The
-    // K producer ends with an END stage.
-    const bool isk = warp == kCfProducerWarp;
-    const int nslot = isk ? nk : nv;
-    uint64_t* fullb = isk ? k_full : v_full;
-    uint64_t* emptyb = isk ? k_empty : v_empty;
-    unsigned char* ring = isk ? cfr : cfr + (size_t)nk * kCfTile;
-    const CUtensorMap* map = isk ? &tmap_k : &tmap_v;
-    if (lane == 0) prefetch_tmap(map);
+   } else if (UM && warp == kCfProducerWarp) {
+    // ----------------------------------- chunk-first TMA producer (K, V)
+    // The CTA's chunk-first units (they precede its private ones): per unit
+    // its K tile into the K ring (released after S) and its V tile into the V
+    // ring (released after P V) -- one 3-D TMA box per tile at d = 128 (2-D
+    // boxes of 64 elements x 64 rows per d-half otherwise): the pool rows are
+    // XOR pre-swizzled within each 128-byte half, so the boxes land as
+    // canonical SWIZZLE_128B atoms.  No chunk-first unit: an END stage.
+    if (lane == 0) {
+      prefetch_tmap(&tmap_k);
+      prefetch_tmap(&tmap_v);
+    }
     pdl_wait();
     int k = 0;
     bool done = false;
+    auto load_tile = [&](const CUtensorMap* map, T* pool, unsigned char* stg, uint64_t* bar, int chunk, int hh) {
+      mbar_arrive_expect_tx(bar, kCfTile);
+      const int y = (int)(layer_rows + ((int64_t)chunk * h + head0 + hh) * kUmC);
+      if (HALVES == 2 && ly.map3)
+        tma_load_3d(stg, map, 0, y, 0, bar);
+      else if (HALVES == 1 && ly.bulk1d)
+        bulk_g2s(stg, pool + ((size_t)chunk * h + head0 + hh) * kUmC * D, kCfTile, bar);
+      else
+#pragma unroll
+        for (int hf = 0; hf < HALVES; ++hf) tma_load_2d(stg + hf * kUmC * 128, map, hf * 64, y, bar);
+    };
     // the first npre units come from the CTA record (loaded at entry), the
     // rest in batches of 32 descriptors, one per lane
     for (int base = u0, first = 1; base < u1 && !done; base += first ? npre : 32, first = 0) {
@@ -465,34 +475,26 @@ __global__ void __launch_bounds__(kDkThreads, 1)
           done = true;
           break;
         }
-        const int s = k % nslot;
-        if (k >= nslot) mbar_wait(&emptyb[s], (uint32_t)(((k / nslot) - 1) & 1));
+        const int sk = k % nk, sv = k % nv;
+        if (k >= nk) mbar_wait(&k_empty[sk], (uint32_t)(((k / nk) - 1) & 1));
         if (lane == 0) {
-          if (isk) {
-            cf_meta[s] = make_int4(i_word & 0xff, i_row0, i_nrows, i_word >> 8);
-            if (tr && k < 16) {  // tcgen05 variant: the timeline traces the chunk-first units
-              tr[3 + 4 * k] = globaltimer_ns();
-              tr[6 + 4 * k] = 2 * kCfTile;
-            }
-          } else if (tr && k < 14) {
-            tr[102 + k] = globaltimer_ns();  // V tile k issued
+          cf_meta[sk] = make_int4(i_word & 0xff, i_row0, i_nrows, i_word >> 8);
+          if (tr && k < 16) {  // tcgen05 variant: the timeline traces the chunk-first units
+            tr[3 + 4 * k] = globaltimer_ns();
+            tr[6 + 4 * k] = 2 * kCfTile;
           }
-          mbar_arrive_expect_tx(&fullb[s], kCfTile);
-          const int y = (int)(layer_rows + ((int64_t)i_chunk * h + head0 + (i_word >> 8)) * kUmC);
-          unsigned char* stg = ring + (size_t)s * kCfTile;
-          if (HALVES == 2 && ly.map3)
-            tma_load_3d(stg, map, 0, y, 0, &fullb[s]);
-          else if (HALVES == 1 && ly.bulk1d)
-            bulk_g2s(stg, (isk ? kpool : vpool) + ((size_t)i_chunk * h + head0 + (i_word >> 8)) * kUmC * D, kCfTile,
-                     &fullb[s]);
-          else
-#pragma unroll
-            for (int hf = 0; hf < HALVES; ++hf) tma_load_2d(stg + hf * kUmC * 128, map, hf * 64, y, &fullb[s]);
+          load_tile(&tmap_k, kpool, cfr + (size_t)sk * kCfTile, &k_full[sk], i_chunk, i_word >> 8);
+        }
+        __syncwarp();
+        if (k >= nv) mbar_wait(&v_empty[sv], (uint32_t)(((k / nv) - 1) & 1));
+        if (lane == 0) {
+          if (tr && k < 14) tr[102 + k] = globaltimer_ns();  // V tile k issued
+          load_tile(&tmap_v, vpool, cfr + (size_t)(nk + sv) * kCfTile, &v_full[sv], i_chunk, i_word >> 8);
         }
         __syncwarp();
       }
     }
-    if (isk && k == 0) {  // no chunk-first unit: an END stage (else the last unit carries DK_FINAL)
+    if (k == 0) {  // no chunk-first unit: an END stage (else the last unit carries DK_FINAL)
       if (lane == 0) {
         cf_meta[0] = make_int4(DK_END, 0, 0, 0);
         mbar_arrive_cta(&k_full[0]);
@@ -500,42 +502,16 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       __syncwarp();
     }
    } else if (UM && warp == kIssuerWarp) {
-    // ------------------------------------------------------------ MMA issuer
-    // chunk k: S_{k&1} = Q K_k^T (M = 64, N = 64, K = d; its K slot released
-    // when S completes), then O += P_{k-1} V_{k-1} of the previous chunk of
-    // the same job (a job boundary flushes the pending P V first: its O is
-    // read before the next job's Q lands).  The chunk's metadata goes to the
-    // softmax warps through s_meta[k&1] (s_meta_full).
+    // --------------------------------------------------------- S issuer
+    // chunk k: S_{k&1} = Q K_k^T (M = 64, N = 64, K = d; A = Q from TMEM, its
+    // K slot released when S completes).  The chunk's metadata goes to the
+    // softmax warps through s_meta[k&1] (s_meta_full).  P V runs on its own
+    // issuer (warp 3), so S of the next chunks is never held up behind it.
     const uint32_t tmem = tmem_base;
-    constexpr uint32_t idS = umma_idesc<T, kUmM>(kUmC, false), idO = umma_idesc<T, kUmM>(D, true);
-    const uint32_t ka0 = smem_u32(cfr), va0 = ka0 + nk * kCfTile;
-    int jobs_q = 0, jobs_done = 0, pend = -1, pend_flags = 0;
-    auto issue_pv = [&](int j, int fj) {
-      const int b = j & 1, sv = j % nv;
-      mbar_wait(&p_full[b], (uint32_t)((j >> 1) & 1));
-      if (tr && lane == 0 && j < 16) tr[86 + j] = globaltimer_ns();  // P_j in (issuer view)
-      mbar_wait(&v_full[sv], (uint32_t)((j / nv) & 1));
-      if ((fj & DK_FIRST) && jobs_done > 0) mbar_wait(&o_free, (uint32_t)((jobs_done - 1) & 1));
-      tc_fence_after();
-      if (lane == 0) {
-        // A = P from TMEM (8 columns = 16 tokens per step), B = V from shared
-        // memory (descriptor advanced by constant address steps, >> 4)
-        const uint64_t db = umma_sdesc(va0 + sv * kCfTile, kUmC * 128, 1024);
-        const uint32_t tp = tmem + kTmemP + (uint32_t)(b * (kUmC / 2));
-#pragma unroll
-        for (int ks = 0; ks < kUmC / 16; ++ks)
-          if (!(ly.diag_cf & 5))
-            umma_f16_ta(tmem + 2 * kUmC, tp + (uint32_t)(ks * 8), db + (uint64_t)(ks * 16 * 128 >> 4), idO,
-                        (!(fj & DK_FIRST) || ks > 0) ? 1u : 0u);
-        umma_commit(&pv_done[b]);
-        umma_commit(&v_empty[sv]);
-        if (fj & DK_LAST) umma_commit(&o_ready);
-      }
-      __syncwarp();
-      if (fj & DK_LAST) ++jobs_done;
-    };
-    int k = 0;
-    for (;; ++k) {
+    constexpr uint32_t idS = umma_idesc<T, kUmM>(kUmC, false);
+    const uint32_t ka0 = smem_u32(cfr);
+    int jobs_q = 0;
+    for (int k = 0;; ++k) {
       const int s = k % nk, b = k & 1;
       mbar_wait(&k_full[s], (uint32_t)((k / nk) & 1));
       if (tr && lane == 0 && k < 16) tr[70 + k] = globaltimer_ns();  // K tile k in shared memory (issuer view)
@@ -547,8 +523,6 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       }
       if (mk.x & DK_END) break;
       if (mk.x & DK_FIRST) {
-        if (pend >= 0) issue_pv(pend, pend_flags);
-        pend = -1;
         mbar_wait(&q_full, (uint32_t)(jobs_q & 1));
         ++jobs_q;
       }
@@ -570,16 +544,51 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         if (tr && k == 0) tr[kTraceStride - 10] = globaltimer_ns();  // first S issued
       }
       __syncwarp();
-      if (pend >= 0) issue_pv(pend, pend_flags);
-      pend = k;
-      pend_flags = mk.x;
-      if (mk.x & DK_FINAL) break;  // the CTA's last chunk-first unit: its P V follows at once
+      if (mk.x & DK_FINAL) break;  // the CTA's last chunk-first unit
     }
-    if (pend >= 0) issue_pv(pend, pend_flags);
-    // TMEM is released once the softmax warps have read the last job's O
-    if (jobs_done > 0) mbar_wait(&o_free, (uint32_t)((jobs_done - 1) & 1));
+    // TMEM is released once the P V issuer reports every job's O read
+    mbar_wait(&tm_done, 0);
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+   } else if (UM && warp == kPvIssuerWarp) {
+    // -------------------------------------------------------- P V issuer
+    // chunk k: O += P_{k&1} V_k (A = P from TMEM, 8 columns = 16 tokens per
+    // step; B = V MN-major from the V ring), once the softmax has published
+    // P_k (and the chunk's flags) and, at a job's first chunk, read the
+    // previous job's O.
+    const uint32_t tmem = tmem_base;
+    constexpr uint32_t idO = umma_idesc<T, kUmM>(D, true);
+    const uint32_t va0 = smem_u32(cfr) + nk * kCfTile;
+    int jobs_done = 0;
+    for (int k = 0;; ++k) {
+      const int b = k & 1, sv = k % nv;
+      mbar_wait(&p_full[b], (uint32_t)((k >> 1) & 1));
+      const int fj = pv_flags[b];
+      if (fj & DK_END) break;
+      if (tr && lane == 0 && k < 16) tr[86 + k] = globaltimer_ns();  // P_k in (issuer view)
+      mbar_wait(&v_full[sv], (uint32_t)((k / nv) & 1));
+      if ((fj & DK_FIRST) && jobs_done > 0) mbar_wait(&o_free, (uint32_t)((jobs_done - 1) & 1));
+      tc_fence_after();
+      if (lane == 0) {
+        const uint64_t db = umma_sdesc(va0 + sv * kCfTile, kUmC * 128, 1024);
+        const uint32_t tp = tmem + kTmemP + (uint32_t)(b * (kUmC / 2));
+#pragma unroll
+        for (int ks = 0; ks < kUmC / 16; ++ks)
+          if (!(ly.diag_cf & 5))
+            umma_f16_ta(tmem + 2 * kUmC, tp + (uint32_t)(ks * 8), db + (uint64_t)(ks * 16 * 128 >> 4), idO,
+                        (!(fj & DK_FIRST) || ks > 0) ? 1u : 0u);
+        umma_commit(&pv_done[b]);
+        umma_commit(&v_empty[sv]);
+        if (fj & DK_LAST) umma_commit(&o_ready);
+      }
+      __syncwarp();
+      if (fj & DK_LAST) ++jobs_done;
+      if (fj & DK_FINAL) break;
+    }
+    if (jobs_done > 0) mbar_wait(&o_free, (uint32_t)((jobs_done - 1) & 1));
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cta(&tm_done);
    }
    if (cs > 1) {
      cluster_wait();            // the cluster barrier phase begun at entry
@@ -673,7 +682,13 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         const int b = k & 1;
         mbar_wait(&s_meta_full[b], (uint32_t)((k >> 1) & 1));
         const int4 mt = s_meta[b];
-        if (mt.x & DK_END) break;
+        if (mt.x & DK_END) {  // no chunk-first unit: tell the P V issuer
+          if (lane == 0) {
+            if (qd == 0) pv_flags[b] = DK_END;
+            mbar_arrive_cta(&p_full[b]);
+          }
+          break;
+        }
         if (mt.x & DK_FIRST) {
           crow0 = mt.y;
           cnrows = mt.z;
@@ -765,7 +780,10 @@ __global__ void __launch_bounds__(kDkThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cta(&p_full[b]);
+        if (lane == 0) {
+          if (qd == 0) pv_flags[b] = mt.x;
+          mbar_arrive_cta(&p_full[b]);
+        }
         if (tr && sct == 0 && k < 16) tr[5 + 4 * k] = globaltimer_ns();
         if (mt.x & DK_LAST) {
           // job end: O from TMEM folded into the (head, row) chunk-first states
