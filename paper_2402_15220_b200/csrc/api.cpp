@@ -928,7 +928,7 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     // +64: 2-D TMA at d = 64 too (A/B); +128: DIAGNOSTIC ONLY, K5 CTAs return at entry (launch cost)
     // +256: DIAGNOSTIC, no private units; +512 / +1024: DIAGNOSTIC, no UMMA / no softmax math
     // +16384: 2-D maps at d = 128 (A/B); + 32768 v: V ring slots v (1..7)
-    h->dk_slots = (int)std::max<int64_t>(0, std::min<int64_t>(value, 262143));
+    h->dk_slots = (int)std::max<int64_t>(0, std::min<int64_t>(value, 1048575));  // + 262144 s: private-unit stages s
     return CA_OK;
   } else if (k == "sf_prefetch") {
     h->sf_prefetch = value < 0 ? 0 : (int)std::min<int64_t>(value, 31);

@@ -1252,7 +1252,7 @@ size_t state_bytes(int32_t d, int32_t n) { return (size_t)n * (d + 4) * 4; }
 // Shared-memory layout of a launch (kernel comment "DkLayout") and its size;
 // nk = 0 when the tcgen05 variant does not fit.
 DkLayout dk_layout(int32_t dtype, int32_t c, int32_t d, int32_t nstate, int32_t cs, bool um, size_t* smem,
-                   int max_slots = 0, int vslots = 0) {
+                   int max_slots = 0, int vslots = 0, int sf_stages = 0) {
   DkLayout L{};
   L.stage_bytes = (uint32_t)dk_stage_bytes(dtype, c, d);
   if (!um) {
@@ -1268,9 +1268,12 @@ DkLayout dk_layout(int32_t dtype, int32_t c, int32_t d, int32_t nstate, int32_t 
   const size_t fixed = 2 * state_bytes(d, nstate) + recv + 1024 + L.stage_bytes;
   *smem = 0;
   if (fixed + 4 * tile > kDkSmemBudget) return L;
-  int slots = (int)std::min<size_t>(2 * kUmMaxCf, (kDkSmemBudget - fixed) / tile);
+  // a second private-unit stage when 6 K/V slots still fit (the packs of the
+  // rows' last chunks then load together instead of one after the other)
+  L.nst = sf_stages > 0 ? sf_stages : (fixed + L.stage_bytes + 6 * tile <= kDkSmemBudget ? 2 : 1);
+  if (fixed + (L.nst - 1) * L.stage_bytes + 4 * tile > kDkSmemBudget) L.nst = 1;
+  int slots = (int)std::min<size_t>(2 * kUmMaxCf, (kDkSmemBudget - fixed - (L.nst - 1) * L.stage_bytes) / tile);
   if (max_slots >= 4) slots = std::min(slots, max_slots);
-  L.nst = 1;
   L.nv = vslots > 0 ? std::min(vslots, slots - 2) : std::min(3, slots / 2);  // V slots wait for P V: K slots come free sooner
   L.nk = std::min(kUmMaxCf, slots - L.nv);
   L.cf_off = (uint32_t)(L.nst * L.stage_bytes + 2 * state_bytes(d, nstate) + recv);
@@ -1284,7 +1287,8 @@ cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend&
   const int cs = t.dk_cs;
   bool um = t.dk_um != 0 && dk_umma_supported(p);
   size_t smem = 0;
-  DkLayout ly = dk_layout(p.dtype, p.c, D, t.dk_hg * t.dk_max_rows, cs, um, &smem, a.dk_slots & 63, (a.dk_slots >> 15) & 7);
+  DkLayout ly = dk_layout(p.dtype, p.c, D, t.dk_hg * t.dk_max_rows, cs, um, &smem, a.dk_slots & 63, (a.dk_slots >> 15) & 7,
+                          (a.dk_slots >> 18) & 3);
   if (um && ly.nk < 2) {
     um = false;
     ly = dk_layout(p.dtype, p.c, D, t.dk_hg * t.dk_max_rows, cs, false, &smem);
