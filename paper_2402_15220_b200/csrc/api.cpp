@@ -370,6 +370,7 @@ struct chunkattn {
     t.dk_blocks = ctx.dk_blocks;
     t.dk_hg = ctx.dk_hg;
     t.dk_um = ctx.dk_um ? 1 : 0;
+    t.dk_all_solo = ctx.dk_all_solo ? 1 : 0;
     t.sf_first = base + L.sf_first;
     t.last_chunk = base + L.last_chunk;
     t.last_start = base + L.last_start;
@@ -928,7 +929,8 @@ chunkattn_status chunkattn_set_option(chunkattn_t h, const char* key, int64_t va
     // +64: 2-D TMA at d = 64 too (A/B); +128: DIAGNOSTIC ONLY, K5 CTAs return at entry (launch cost)
     // +256: DIAGNOSTIC, no private units; +512 / +1024: DIAGNOSTIC, no UMMA / no softmax math
     // +16384: 2-D maps at d = 128 (A/B); + 32768 v: V ring slots v (1..7)
-    h->dk_slots = (int)std::max<int64_t>(0, std::min<int64_t>(value, 1048575));  // + 262144 s: private-unit stages s
+    // + 262144 s: private-unit stages s; + 1048576: keep the chunk-first state set (A/B)
+    h->dk_slots = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2097151));
     return CA_OK;
   } else if (k == "sf_prefetch") {
     h->sf_prefetch = value < 0 ? 0 : (int)std::min<int64_t>(value, 31);

@@ -255,6 +255,11 @@ bool build_context(const PrefixTree& tree, const ScheduleOptions& opt, Context* 
       else if (!(f & DK_PACK)) ++n_pv;
     }
     X.dk_um = opt.dk_umma_ok && n_cf > 0 && (opt.dk_umma == 2 || (opt.dk_umma == 1 && n_cf >= opt.dk_umma_ratio * n_pv));
+    X.dk_all_solo = true;  // every FINAL unit also SOLO
+    for (int64_t u = 0; u < X.dk_units; ++u) {
+      const int32_t f = dk_unit[(size_t)kDkUnitInts * u + 3];
+      if ((f & DK_FINAL) && !(f & DK_SOLO)) X.dk_all_solo = false;
+    }
   }
   // old schedules (two-kernel / fused persistent): not built when the K5
   // cluster decode runs the step

@@ -132,6 +132,7 @@ struct Context {
   int32_t dk_cs = 0, dk_blocks = 0, dk_groups = 0, dk_max_rows = 0, dk_hg = 1;
   int64_t dk_units = 0;
   bool dk_um = false;  // chunk-first units on tcgen05 requested (the launch checks the shared-memory layout)
+  bool dk_all_solo = false;  // every CTA's chunk-first units form at most one job (no second state set needed)
 };
 
 // Build the context of the current tree.  Returns false (and sets *err) when

@@ -155,6 +155,7 @@ CA_DEV void fold_weights(float ms, float mj, float& M, float& ws, float& wj) {
 // TMEM (UM, 512 columns): S [2][64] | O [D] | P [2][32] (16-bit pairs) | Q [D / 2].
 struct DkLayout {
   int32_t nst, nk, nv, scap;
+  int32_t nocst;  // UM: no chunk-first state set (every CTA folds its one job straight into the states)
   uint32_t stage_bytes, cf_off;
   int32_t bulk1d;  // d = 64: K/V tiles by one 1-D bulk copy (the pool tile is already the SWIZZLE_128B image)
   int32_t map3;        // d = 128: the maps are 3-D (one TMA op per tile)
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
   const uint32_t tile_bytes = (uint32_t)c * kRowBytes;
   float* st = reinterpret_cast<float*>(smem_raw + (size_t)nst * stage_bytes);  // (head, row) states
   float* cst = st + (size_t)ly.scap * SR;                 // UM: chunk-first states (same indexing)
-  float* recv = (UM ? cst : st) + (size_t)ly.scap * SR;  // [owned state][other rank][SR]: pushed by the other ranks
+  float* recv = (UM && !ly.nocst ? cst : st) + (size_t)ly.scap * SR;  // [owned state][other rank][SR]: pushed by the other ranks
   unsigned char* cfr = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + ly.cf_off + 1023) & ~uintptr_t(1023));  // UM: chunk-first ring
   auto state_row = [&](int hh, int row) { return st + (size_t)(hh * brows + row - brow0) * SR; };
@@ -669,8 +670,10 @@ __global__ void __launch_bounds__(kDkThreads, 1)
           qpre = true;
         }
       }
+      if (!ly.nocst) {
 #pragma unroll 1
-      for (int i = sct; i < hg * brows * SR; i += 128) cst[i] = (i % SR) == D ? -INFINITY : 0.f;
+        for (int i = sct; i < hg * brows * SR; i += 128) cst[i] = (i % SR) == D ? -INFINITY : 0.f;
+      }
       asm volatile("bar.sync 3, 128;" ::: "memory");  // chunk-first states initialised
       if (qpre) {
         store_q();
@@ -1107,7 +1110,7 @@ __global__ void __launch_bounds__(kDkThreads, 1)
     fence_proxy_async();  // the states' generic writes before the bulk copies read them
     dk_sync_merge(&merge_bar, 0);
     if (tr && tid == kConsumer0 * 32) tr[kTraceStride - 9] = globaltimer_ns();  // merge warps synced  // every warp's last fold is in the states
-    if (UM && !cf_direct) {
+    if (UM && !cf_direct && !ly.nocst) {
 #pragma unroll 1
       for (int i = mw; i < nstate; i += kMergeThreads / 32) {
         float* a = st + (size_t)i * SR;
@@ -1252,7 +1255,7 @@ size_t state_bytes(int32_t d, int32_t n) { return (size_t)n * (d + 4) * 4; }
 // Shared-memory layout of a launch (kernel comment "DkLayout") and its size;
 // nk = 0 when the tcgen05 variant does not fit.
 DkLayout dk_layout(int32_t dtype, int32_t c, int32_t d, int32_t nstate, int32_t cs, bool um, size_t* smem,
-                   int max_slots = 0, int vslots = 0, int sf_stages = 0) {
+                   int max_slots = 0, int vslots = 0, int sf_stages = 0, bool nocst = false) {
   DkLayout L{};
   L.stage_bytes = (uint32_t)dk_stage_bytes(dtype, c, d);
   if (!um) {
@@ -1265,7 +1268,8 @@ DkLayout dk_layout(int32_t dtype, int32_t c, int32_t d, int32_t nstate, int32_t 
   L.scap = nstate;
   const size_t tile = (size_t)(d / 64) * kUmC * 128;  // Q and P live in TMEM
   const size_t recv = dk_recv_bytes(d, nstate, cs);
-  const size_t fixed = 2 * state_bytes(d, nstate) + recv + 1024 + L.stage_bytes;
+  L.nocst = nocst ? 1 : 0;
+  const size_t fixed = (nocst ? 1 : 2) * state_bytes(d, nstate) + recv + 1024 + L.stage_bytes;
   *smem = 0;
   if (fixed + 4 * tile > kDkSmemBudget) return L;
   // a second private-unit stage when 6 K/V slots still fit (the packs of the
@@ -1276,7 +1280,7 @@ DkLayout dk_layout(int32_t dtype, int32_t c, int32_t d, int32_t nstate, int32_t 
   if (max_slots >= 4) slots = std::min(slots, max_slots);
   L.nv = vslots > 0 ? std::min(vslots, slots - 2) : std::min(3, slots / 2);  // V slots wait for P V: K slots come free sooner
   L.nk = std::min(kUmMaxCf, slots - L.nv);
-  L.cf_off = (uint32_t)(L.nst * L.stage_bytes + 2 * state_bytes(d, nstate) + recv);
+  L.cf_off = (uint32_t)(L.nst * L.stage_bytes + (nocst ? 1 : 2) * state_bytes(d, nstate) + recv);
   *smem = L.cf_off + 1024 + (L.nk + L.nv) * tile;
   return L;
 }
@@ -1288,7 +1292,7 @@ cudaError_t launch_dk_t(const AttnLaunch& a, const DevTables& t, const DkAppend&
   bool um = t.dk_um != 0 && dk_umma_supported(p);
   size_t smem = 0;
   DkLayout ly = dk_layout(p.dtype, p.c, D, t.dk_hg * t.dk_max_rows, cs, um, &smem, a.dk_slots & 63, (a.dk_slots >> 15) & 7,
-                          (a.dk_slots >> 18) & 3);
+                          (a.dk_slots >> 18) & 3, t.dk_all_solo != 0 && !(a.dk_slots & (1 << 20)));
   if (um && ly.nk < 2) {
     um = false;
     ly = dk_layout(p.dtype, p.c, D, t.dk_hg * t.dk_max_rows, cs, false, &smem);

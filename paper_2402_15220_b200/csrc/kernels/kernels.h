@@ -38,6 +38,7 @@ struct DevTables {
   const int32_t* dk_unit;     // [units][4] {chunk, row0, rows, DK_* flags}
   int32_t dk_cs, dk_groups, dk_max_rows, dk_blocks, dk_hg;
   int32_t dk_um;              // chunk-first units on tcgen05 (UM variant) when its layout fits
+  int32_t dk_all_solo;        // every CTA has at most one chunk-first job (UM: one state set suffices)
 };
 
 
