@@ -129,6 +129,7 @@ struct chunkattn {
   int sf_ctas_per_sm = 2;  // persistent seq-first residency (smem budget per CTA)
   int sf_prefetch = 0;     // seq-first L2 prefetch distance (units); measured slower on B200
   int dk_slots = 0;        // K5 tcgen05 variant: cap on K + V ring slots (0 = as many as fit)
+  bool perm_identity = false;  // the last attend order equals the DFS row order
   int diag_nocompute = 0;  // DIAGNOSTIC ONLY (wrong outputs): seq-first consumers skip the math
   bool use_pdl = true;
   int num_sms = 148;
@@ -266,6 +267,8 @@ struct chunkattn {
       }
       attend_ids.assign(seq_ids, seq_ids + n);
       attend_epoch = ctx.epoch;
+      perm_identity = true;  // the caller's order is the DFS row order: kernels may skip the indirection
+      for (int64_t r = 0; r < n; ++r) perm_identity = perm_identity && perm[r] == (int32_t)r;
     }
     return CA_OK;
   }
@@ -370,6 +373,7 @@ struct chunkattn {
     t.dk_blocks = ctx.dk_blocks;
     t.dk_hg = ctx.dk_hg;
     t.dk_um = ctx.dk_um ? 1 : 0;
+    t.row_identity = perm_identity ? 1 : 0;
     t.dk_all_solo = ctx.dk_all_solo ? 1 : 0;
     t.sf_first = base + L.sf_first;
     t.last_chunk = base + L.last_chunk;

@@ -636,12 +636,16 @@ __global__ void __launch_bounds__(kDkThreads, 1)
       // speculative: the CTA's first job usually spans the whole block, so the
       // caller indices of this thread's Q rows are loaded at entry
       const int js0 = job_row(m0, brows), js1 = job_row(m0 + 8, brows);
-      const int cs0 = js0 >= 0 ? t.row_caller[brow0 + js0] : 0, cs1 = js1 >= 0 ? t.row_caller[brow0 + js1] : 0;
+      const int cs0 = js0 < 0 ? 0 : t.row_identity ? brow0 + js0 : t.row_caller[brow0 + js0];
+      const int cs1 = js1 < 0 ? 0 : t.row_identity ? brow0 + js1 : t.row_caller[brow0 + js1];
       auto load_q = [&](int row0, int nrows, int hh) {
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           const int j = job_row(m0 + 8 * hf, nrows);
-          const int caller = j < 0 ? 0 : (row0 == brow0 && nrows == brows) ? (hf ? cs1 : cs0) : t.row_caller[row0 + j];
+          const int caller = j < 0                                  ? 0
+                             : (row0 == brow0 && nrows == brows) ? (hf ? cs1 : cs0)
+                             : t.row_identity                    ? row0 + j
+                                                                 : t.row_caller[row0 + j];
           const uint32_t* qrow =
               j >= 0 ? reinterpret_cast<const uint32_t*>(q + ((size_t)caller * h + head0 + hh) * D) : nullptr;
 #pragma unroll

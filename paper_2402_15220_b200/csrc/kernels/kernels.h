@@ -39,6 +39,7 @@ struct DevTables {
   int32_t dk_cs, dk_groups, dk_max_rows, dk_blocks, dk_hg;
   int32_t dk_um;              // chunk-first units on tcgen05 (UM variant) when its layout fits
   int32_t dk_all_solo;        // every CTA has at most one chunk-first job (UM: one state set suffices)
+  int32_t row_identity;       // row_caller[r] == r for every row (the caller's order is the row order)
 };
 
 
