@@ -33,7 +33,7 @@ namespace {
 
 constexpr int kUmRows = 128;   // UMMA M
 constexpr int kUmStages = 3;   // K/V ring depth
-constexpr int kUmThreads = 192;  // warps 0-3 softmax/epilogue, 4 TMA producer, 5 MMA issuer
+constexpr int kUmThreads = 224;  // warps 0-3 softmax/epilogue, 4 TMA producer, 5 S issuer, 6 P V issuer
 constexpr float kRescaleLog2 = 8.f;  // lazy O rescale threshold (P <= 2^8)
 
 
@@ -64,7 +64,7 @@ CA_DEV void store_row32(TO* dst, const uint32_t (&u)[32], float inv) {
 // O / n in TO (no partials).  NG = 2 softmax groups (two 128-row query tiles
 // of the same head) share every K/V stage and ping-pong on the tensor core.
 template <typename T, typename TO, int D, int C, bool PREFILL, int NG>
-__global__ void __launch_bounds__(NG * 128 + 64, 1)
+__global__ void __launch_bounds__(NG * 128 + 96, 1)
     cf_umma_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                    const T* __restrict__ q, float* __restrict__ pO, DevTables t, int32_t h, int64_t layer_rows,
                    float scale_log2, TO* __restrict__ out, const int32_t* __restrict__ pf_tiles,
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(NG * 128 + 64, 1)
   constexpr uint32_t kTmemCols = NG * kGroupCols <= 256 ? 256 : 512;
   static_assert(NG * kGroupCols <= 512, "TMEM columns");
   constexpr int PR = D + 4;
-  constexpr int kProducer = 4 * NG, kIssuer = 4 * NG + 1;
+  constexpr int kProducer = 4 * NG, kIssuer = 4 * NG + 1, kPvIssuer = 4 * NG + 2;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* sQ = sm;                       // [NG][kQBytes]
@@ -160,28 +160,14 @@ __global__ void __launch_bounds__(NG * 128 + 64, 1)
     }
     __syncwarp();
   } else if (warp == kIssuer) {
-    // ------------------------------------------------------------ MMA issuer
+    // ---------------------------------------------------------- S issuer
+    // S_{g,k} = Q_g K_k^T into S buffer k & 1; P V runs on its own issuer
+    // (warp kPvIssuer), so S of the next chunk never waits behind it
     if (lane == 0) {
-      constexpr uint32_t idS = umma_idesc<T>(C, false), idO = umma_idesc<T>(D, true);
-      const uint32_t qa = smem_u32(sQ), kva = smem_u32(sKV), pa = smem_u32(sP);
+      constexpr uint32_t idS = umma_idesc<T>(C, false);
+      const uint32_t qa = smem_u32(sQ), kva = smem_u32(sKV);
       for (int g = 0; g < NG; ++g) mbar_wait(&q_full[g], 0);
       tc_fence_after();
-      auto issue_pv = [&](int j) {  // O_g += P_{g,j} V_j for every group, then release the stage
-        const int b = j & 1, s = j % NST;
-        const uint32_t va = kva + s * kStageBytes + kTileBytes;
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-          mbar_wait(&p_full[g][b], (uint32_t)((j >> 1) & 1));
-          tc_fence_after();
-          const uint32_t pb = pa + (g * 2 + b) * kPBytes, tO = tmem + g * kGroupCols + 2 * C;
-#pragma unroll
-          for (int ks = 0; ks < C / 16; ++ks)
-            umma_f16(tO, umma_sdesc(pb + (ks / 4) * kUmRows * 128 + (ks % 4) * 32, 16, 1024),
-                     umma_sdesc(va + ks * 16 * 128, C * 128, 1024), idO, (j > 0 || ks > 0) ? 1u : 0u);
-          umma_commit(&pv_done[g][b]);
-        }
-        umma_commit(&kv_empty[s]);
-      };
       for (int k = 0; k < n_chunks; ++k) {
         const int s = k % NST, b = k & 1;
         mbar_wait(&kv_full[s], (uint32_t)((k / NST) & 1));
@@ -199,9 +185,33 @@ __global__ void __launch_bounds__(NG * 128 + 64, 1)
           }
           umma_commit(&s_full[g][b]);
         }
-        if (k >= 1) issue_pv(k - 1);
       }
-      if (n_chunks > 0) issue_pv(n_chunks - 1);
+    }
+    __syncwarp();
+  } else if (warp == kPvIssuer) {
+    // -------------------------------------------------------- P V issuer
+    // O_g += P_{g,k} V_k once the softmax has published P_{g,k}; the stage
+    // is released after the last group's P V
+    if (lane == 0) {
+      constexpr uint32_t idO = umma_idesc<T>(D, true);
+      const uint32_t kva = smem_u32(sKV), pa = smem_u32(sP);
+      for (int k = 0; k < n_chunks; ++k) {
+        const int s = k % NST, b = k & 1;
+        mbar_wait(&kv_full[s], (uint32_t)((k / NST) & 1));  // V of the stage (the S issuer saw it first)
+        const uint32_t va = kva + s * kStageBytes + kTileBytes;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+          mbar_wait(&p_full[g][b], (uint32_t)((k >> 1) & 1));
+          tc_fence_after();
+          const uint32_t pb = pa + (g * 2 + b) * kPBytes, tO = tmem + g * kGroupCols + 2 * C;
+#pragma unroll
+          for (int ks = 0; ks < C / 16; ++ks)
+            umma_f16(tO, umma_sdesc(pb + (ks / 4) * kUmRows * 128 + (ks % 4) * 32, 16, 1024),
+                     umma_sdesc(va + ks * 16 * 128, C * 128, 1024), idO, (k > 0 || ks > 0) ? 1u : 0u);
+          umma_commit(&pv_done[g][b]);
+        }
+        umma_commit(&kv_empty[s]);
+      }
       umma_commit(&o_ready);
     }
     __syncwarp();
@@ -490,7 +500,7 @@ cudaError_t launch_pf(const PrefillLaunch& a, cudaStream_t st) {
   auto kern = cf_umma_kernel<T, TO, D, C, true, kPfGroups>;
   cudaError_t e = set_smem_once((const void*)kern, um_smem<D, C, kPfGroups>());
   if (e != cudaSuccess) return e;
-  return launch_ex(kern, dim3(a.n_tiles, p.h), dim3(kPfGroups * 128 + 64), um_smem<D, C, kPfGroups>(), st, false, mk,
+  return launch_ex(kern, dim3(a.n_tiles, p.h), dim3(kPfGroups * 128 + 96), um_smem<D, C, kPfGroups>(), st, false, mk,
                    mv, (const T*)a.q,
                    (float*)nullptr, DevTables{}, (int32_t)p.h, (int64_t)a.layer * p.max_chunks * p.h * p.c,
                    a.scale_log2, (TO*)a.out, a.tiles, a.chunks);
